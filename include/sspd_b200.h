@@ -1,0 +1,221 @@
+/*
+ * sspd_b200.h -- C ABI of the B200 packet-scan / estimate path for the
+ * super-point detector of arXiv 1901.07306 (reference package `sspd`).
+ *
+ * Every entry point takes caller-owned DEVICE buffers (plain pointers and
+ * sizes), an explicit cudaStream_t passed as `void*`, and a host pointer to a
+ * POD `sspd_params` block that it copies by value into the kernel launch.
+ * Nothing allocates behind the caller's back and there is no global mutable
+ * state.  The return value is an `sspd_status`; the Python host layer maps
+ * it onto the reference exception classes (errors.py:7-53):
+ *   SSPD_ERR_CONFIG  -> ConfigError      (bad geometry / argument)
+ *   SSPD_ERR_DATA    -> DataError        (malformed input)
+ *   SSPD_ERR_CUDA    -> SspdError        (launch / runtime failure)
+ *
+ * The reference has no FFI layer: each function below
+ * replaces one Python method of the reference, cited per function.
+ */
+#ifndef SSPD_B200_H
+#define SSPD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SSPD_API __attribute__((visibility("default")))
+#else
+#define SSPD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSPD_ABI_VERSION 1
+#define SSPD_MAX_SR 16   /* SEAV rows supported by the kernels        */
+#define SSPD_MAX_LR 64   /* LDCA rows supported by the kernels        */
+
+typedef enum sspd_status {
+  SSPD_OK = 0,
+  SSPD_ERR_CONFIG = 2,
+  SSPD_ERR_DATA = 3,
+  SSPD_ERR_CUDA = 4,
+  SSPD_ERR_CAPACITY = 5 /* output buffer too small; *count holds the need */
+} sspd_status;
+
+/* Exact `x % d` for 64-bit x by a runtime divisor 1 <= d < 2^32
+ * (hashing.py:120-130 reduces the FULL 64-bit hash modulo m).  pow2 != 0
+ * means d is a power of two and the mask path is used; otherwise the
+ * Granlund-Montgomery round-up multiplier `magic` (65-bit, top bit implicit)
+ * with shifts sh1/sh2 gives the quotient.  Built by the host layer. */
+typedef struct sspd_divisor {
+  uint64_t d;
+  uint64_t magic;
+  uint32_t sh1;
+  uint32_t sh2;
+  uint32_t pow2;
+  uint32_t pad_;
+} sspd_divisor;
+
+/* Resolved detector geometry + hash family.  Field meanings follow the
+ * reference: SeedFamily (hashing.py:82-99), SeavConfig
+ * (short_sketch.py:116-181), LdcaConfig (long_sketch.py:72-90). */
+typedef struct sspd_params {
+  /* hash family: derive_seed(master, tag) for H1/H2/H3/ROUTE/LH_i */
+  uint64_t seed_h1, seed_h2, seed_h3, seed_route;
+  uint64_t seed_lh[SSPD_MAX_LR];
+  /* SEAV (short estimator array vector) */
+  uint32_t r, sr, a, g;
+  uint32_t addr_bits, lp_bits, tau, reg_bytes; /* reg_bytes: 1/2/4/8 */
+  uint32_t isb[SSPD_MAX_SR];
+  uint32_t ibn[SSPD_MAX_SR];
+  uint32_t sc[SSPD_MAX_SR];
+  uint64_t seav_row_off[SSPD_MAX_SR]; /* byte offset of row i (flat payload) */
+  uint64_t seav_bytes;                /* payload bytes = memory_bytes()      */
+  /* LDCA (linear distinct counter array) */
+  uint32_t lr, lc, k, pad0_;
+  uint64_t ldca_bytes;                /* lr*lc*k/8                           */
+  sspd_divisor div_g, div_k, div_lc;
+  /* sliding layout (sliding.py:119-146): slot bases, in timestamp slots */
+  uint64_t slot_row_base[SSPD_MAX_SR];
+  uint64_t slot_ldca_base;
+  uint64_t slot_total;
+} sspd_params;
+
+/* ---- library identity ------------------------------------------------- */
+SSPD_API int sspd_abi_version(void);
+SSPD_API size_t sspd_params_size(void);          /* sizeof(sspd_params) for checking  */
+SSPD_API int sspd_device_sm_count(int device);   /* -1 when no device is available     */
+
+/* ---- host-side helpers (no device work; used by the CPU test suite) ---- */
+/* hash_range(key, seed, d) exactly as hashing.py:120-124, via the same
+ * fast-modulo code the kernels run. */
+SSPD_API uint64_t sspd_hash_range_host(uint64_t key, uint64_t seed, const sspd_divisor* d);
+SSPD_API uint64_t sspd_mix64_host(uint64_t x);                   /* hashing.py:48-53 */
+
+/* ---- K1 discrete scan --------------------------------------------------
+ * Replaces DetectorState.process_batch (window_detector.py:100-103) =
+ * SeavSketch.update_batch (short_sketch.py:300-318) +
+ * LdcaSketch.update_batch (long_sketch.py:125-135).
+ * hips/oips: n uint32 host/opposite IPs (device).  seav: p->seav_bytes,
+ * ldca: p->ldca_bytes (both rounded up to 16 B by the caller, zero-padded).
+ * Either sketch pointer may be NULL to skip that sketch. */
+SSPD_API int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                       const sspd_params* p, uint8_t* seav, uint8_t* ldca,
+                       void* stream);
+
+/* ---- K2 sliding scan ---------------------------------------------------
+ * Replaces SlidingDetector.observe_batch (sliding.py:156-185) with
+ * TimestampPool.touch_batch (sliding.py:77-79): plain store of
+ * `now_wrapped` into every slot the discrete path would set.
+ * pool: p->slot_total timestamps of ts_bytes (1/2/4/8) each. */
+SSPD_API int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                      const sspd_params* p, void* pool, uint32_t ts_bytes,
+                      uint64_t now_wrapped, void* stream);
+
+/* ---- K3 sweep: TimestampPool._sweep (sliding.py:88-94) ---------------- */
+SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
+               uint64_t now_wrapped, uint64_t window_slices,
+               uint64_t clamp_value, void* stream);
+
+/* ---- K4 materialize ----------------------------------------------------
+ * materialize_seav (sliding.py:191-203): active slots -> SEAV payload.
+ * materialize_ldca (sliding.py:215-220): active slots -> packed LDCA bytes.
+ * active  <=>  ((now_wrapped - ts) & mask) < window_slices. */
+SSPD_API int sspd_materialize_seav(const void* pool, uint32_t ts_bytes,
+                          const sspd_params* p, uint64_t now_wrapped,
+                          uint64_t window_slices, uint8_t* seav_out,
+                          void* stream);
+SSPD_API int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes,
+                          const sspd_params* p, uint64_t now_wrapped,
+                          uint64_t window_slices, uint8_t* ldca_out,
+                          void* stream);
+/* pool ages: ((now_wrapped - ts) & mask) as uint64 (TimestampPool.ages,
+ * sliding.py:96-98) */
+SSPD_API int sspd_pool_ages(const void* pool, uint64_t n_slots, uint32_t ts_bytes,
+                   uint64_t now_wrapped, uint64_t* ages_out, void* stream);
+
+/* ---- K5 restore --------------------------------------------------------
+ * Replaces SeavSketch.restore_sea / restore (short_sketch.py:347-408).
+ * For every register array rp in [rp_begin, rp_begin+rp_count):
+ *   counts the consistent all-hot tuples (exact up to cap+1),
+ *   sets overflow[rp-rp_begin]=1 when the count exceeds `cap`,
+ *   otherwise emits every tuple whose register AND has weight >= 3 as
+ *   (ip, (rp<<8)|weight) -- unsorted.
+ * out_count (device uint64) receives the number of candidates found; when
+ * it exceeds out_capacity nothing beyond capacity is written and the host
+ * retries with a larger buffer.  Entries are sorted by ip by
+ * sspd_sort_candidates. */
+SSPD_API int sspd_restore(const uint8_t* seav, const sspd_params* p,
+                 uint32_t rp_begin, uint32_t rp_count, uint64_t cap,
+                 uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
+                 unsigned long long* out_count, uint8_t* overflow,
+                 void* stream);
+
+/* Sort (ip, aux) pairs by ip ascending on the device (restore's
+ * `sorted(found)`, short_sketch.py:408).  scratch may be NULL to query
+ * *scratch_bytes. */
+SSPD_API int sspd_sort_candidates(uint32_t* ip, uint32_t* aux, uint64_t n,
+                         void* scratch, size_t* scratch_bytes, void* stream);
+
+/* ---- K6 filter ---------------------------------------------------------
+ * Replaces LdcaSketch.union_register/estimate (long_sketch.py:137-148) and
+ * the keep test of finalize_window (window_detector.py:105-125):
+ *   z0[j] = k - popcount(AND_i data[i, c_i(ip_j)])
+ *   keep[j] = keep_table[z0[j]]   (host-built table of k+1 bytes that holds
+ *             the reference float test `saturated or est >= beta*theta`
+ *             evaluated once per possible z0, so the device stays integer)
+ * keep may be NULL. */
+SSPD_API int sspd_filter(const uint8_t* ldca, const sspd_params* p,
+                const uint32_t* ips, uint64_t n, const uint8_t* keep_table,
+                uint32_t* z0_out, uint8_t* keep_out, void* stream);
+
+/* Sliding filter: the same on the active view of the timestamp pool
+ * (SlidingDetector._estimate, sliding.py:222-230). */
+SSPD_API int sspd_filter_sliding(const void* pool, uint32_t ts_bytes,
+                        const sspd_params* p, uint64_t now_wrapped,
+                        uint64_t window_slices, const uint32_t* ips,
+                        uint64_t n, const uint8_t* keep_table,
+                        uint32_t* z0_out, uint8_t* keep_out, void* stream);
+
+/* Stable compaction of (ip, z0) by keep flag; *out_count (device). */
+SSPD_API int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0,
+                         const uint8_t* keep, uint64_t n, uint32_t* ip_out,
+                         uint32_t* z0_out, unsigned long long* out_count,
+                         void* scratch, size_t* scratch_bytes, void* stream);
+
+/* ---- K7 merge ----------------------------------------------------------
+ * Bytewise OR of n_src equal-length buffers into dst (dst may alias
+ * srcs[0]).  Sources may be peer-GPU pointers (CUDA IPC / P2P mapped):
+ * replaces merge_frames' payload OR (distributed.py:167-169),
+ * SeavSketch.merge (short_sketch.py:326-331), LdcaSketch.merge
+ * (long_sketch.py:150-153).  srcs is a HOST array of device pointers. */
+SSPD_API int sspd_merge_or(const void* const* srcs, int n_src, void* dst,
+                  uint64_t bytes, void* stream);
+
+/* ---- K8 merge_age_min --------------------------------------------------
+ * merge_timestamp_pools (distributed.py:176-192): per slot, the smallest
+ * wrapped age over all pools wins; dst = (now - min_age) & mask. */
+SSPD_API int sspd_merge_age_min(const void* const* srcs, int n_src, void* dst,
+                       uint64_t n_slots, uint32_t ts_bytes,
+                       uint64_t now_wrapped, void* stream);
+
+/* ---- route_pairs on the device (distributed.py:195-210) ---------------
+ * mode 0 = "hash": mix64(((hip<<32)|oip) ^ seed_route) % n_wp
+ * mode 1 = "round-robin": (index_base + j) % n_wp */
+SSPD_API int sspd_route_pairs(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                     const sspd_params* p, const sspd_divisor* n_wp,
+                     int mode, uint64_t index_base, int64_t* lanes_out,
+                     void* stream);
+
+/* ---- roofline microbenchmark ------------------------------------------
+ * Random red.global.or.b32 over `bytes` of device memory (pow2), issued the
+ * way the scan issues them; returns achieved ops/s in *ops_per_s.  Used by
+ * bench.py for the L2-atomic term of the scan roofline. */
+SSPD_API int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
+                        int iters, double* ops_per_s, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSPD_B200_H */

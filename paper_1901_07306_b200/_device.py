@@ -1,0 +1,73 @@
+"""Device plumbing: CUDA buffers and streams come from PyTorch, compute from
+libsspd_b200.so.  Nothing here computes on the CPU on the data path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._abi import check, lib
+from .errors import DataError, DeviceError
+
+try:
+    import torch
+except ImportError as exc:  # pragma: no cover - torch is part of the image
+    raise DeviceError("PyTorch is required for device buffers") from exc
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the sspd B200 path has no CPU fallback")
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def zeros_bytes(nbytes: int):
+    """Zeroed device byte buffer, padded to 16 B for vector access."""
+    return torch.zeros(((nbytes + 15) // 16) * 16, dtype=torch.uint8, device=device())
+
+
+def ips_to_device(a, name: str = "ips"):
+    """Accept a numpy array / sequence / torch tensor of IPv4 addresses and
+    return a contiguous 32-bit device tensor (bit pattern = uint32).
+
+    The reference casts inputs with astype(uint64) and would hash wider
+    keys in full (short_sketch.py:303-304); this build is IPv4-only and
+    rejects keys outside [0, 2^32) instead of silently truncating them.
+    """
+    if isinstance(a, torch.Tensor):
+        if a.dtype in (torch.int32, torch.uint32):
+            t = a
+        else:
+            if a.numel() and (int(a.min()) < 0 or int(a.max()) > 0xFFFFFFFF):
+                raise DataError(f"{name}: IPv4 keys must lie in [0, 2^32)")
+            t64 = a.to(torch.int64)
+            t = torch.where(t64 >= 2**31, t64 - 2**32, t64).to(torch.int32)
+        if t.device.type != "cuda":
+            t = t.to(device(), non_blocking=True)
+        return t.contiguous()
+    arr = np.asarray(a)
+    if arr.dtype.kind not in "ui":
+        raise DataError(f"{name}: integer array expected, got {arr.dtype}")
+    if arr.dtype != np.uint32:
+        if arr.size and (int(arr.min()) < 0 or int(arr.max()) > 0xFFFFFFFF):
+            raise DataError(f"{name}: IPv4 keys must lie in [0, 2^32)")
+        arr = arr.astype(np.uint32)
+    arr = np.ascontiguousarray(arr.reshape(-1))
+    return torch.from_numpy(arr.view(np.int32)).to(device(), non_blocking=False)
+
+
+def to_host_bytes(t, nbytes: int) -> bytes:
+    return t[:nbytes].cpu().numpy().tobytes()
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)

@@ -1,0 +1,555 @@
+// End-of-window estimate path: K5 restore, candidate sort, K6 filter,
+// report compaction.
+//
+// Reference: SeavSketch.restore_sea / restore   short_sketch.py:347-408
+//            LdcaSketch.union_register/estimate long_sketch.py:137-148
+//            DetectorState.finalize_window      window_detector.py:105-125
+//
+// Restore on the device.  One CTA owns one register array (SEA, index rp).
+// The reference walks rows depth-first and prunes a partial tuple as soon
+// as a row's column disagrees with already-fixed left-part (LP) bits
+// (`(acc_lp ^ v) & acc_mask & mask`, short_sketch.py:379-388).  The set of
+// LP positions that are already fixed when row i is reached,
+//     fixed_i = (mask_0 | ... | mask_{i-1}) & mask_i,
+// does not depend on the path, so the CTA buckets row i's hot columns by
+// their bits on fixed_i (counting sort in shared memory).  A walk then
+// reads exactly the consistent columns of each row as one contiguous
+// bucket -- no rejected candidates are ever visited.  Rows 0 and 1 are
+// flattened into one balanced work list (a prefix sum over row-0 entries
+// of their row-1 bucket sizes); deeper rows are walked with an explicit
+// stack.
+//
+// Cap semantics (short_sketch.py:373-376, 398-407): `survivors` counts
+// every complete consistent tuple, whatever its AND weight; more than `cap`
+// of them drops the whole SEA.  A tuple is one-to-one with an LP whose
+// registers are all hot, so the count is order-independent: pass 1 counts
+// (stopping early once the shared total exceeds cap), pass 2 emits the
+// weight >= 3 tuples only for SEAs that did not overflow.
+#include <cstring>
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include "sspd_common.cuh"
+#include "launch.cuh"
+
+namespace sspd {
+
+struct RestorePlan {
+  uint32_t sr, w, r, reg_bytes;
+  uint32_t full_bits_lo, full_bits_hi;  // (1<<g)-1
+  uint32_t isb[SSPD_MAX_SR], ibn[SSPD_MAX_SR], sc[SSPD_MAX_SR];
+  uint32_t keymask[SSPD_MAX_SR];  // column bits that sit on fixed_i
+  uint32_t nk[SSPD_MAX_SR];       // popcount(keymask)
+  uint32_t off_regs[SSPD_MAX_SR], off_cols[SSPD_MAX_SR], off_bstart[SSPD_MAX_SR];
+  uint32_t off_pref0, off_misc, smem_bytes, pad_;
+  uint64_t seav_row_off[SSPD_MAX_SR];
+};
+
+__device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
+  uint32_t r = 0, bb = 1;
+  while (m) {
+    const uint32_t low = m & (0u - m);
+    if (x & low) r |= bb;
+    bb <<= 1;
+    m &= m - 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t load_reg(const uint8_t* base, uint32_t idx, uint32_t rb) {
+  switch (rb) {
+    case 1: return base[idx];
+    case 2: return reinterpret_cast<const uint16_t*>(base)[idx];
+    case 4: return reinterpret_cast<const uint32_t*>(base)[idx];
+    default: return reinterpret_cast<const uint64_t*>(base)[idx];
+  }
+}
+
+struct Misc {
+  unsigned long long total;  // consistent complete tuples counted so far
+  uint32_t abort;
+  uint32_t pairs;
+  uint32_t hot[SSPD_MAX_SR];
+};
+
+// In-place exclusive scan of a[0..m) by one warp; returns the total.
+__device__ uint32_t warp_exclusive_scan(uint32_t* a, uint32_t m) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < m; base += 32) {
+    const uint32_t i = base + lane;
+    const uint32_t v = i < m ? a[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (i < m) a[i] = carry + x - v;
+    carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+  }
+  return carry;
+}
+
+template <bool kEmit>
+__device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uint64_t cap, uint32_t* out_ip,
+                             uint32_t* out_aux, uint64_t out_capacity, unsigned long long* out_count) {
+  Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
+  const uint32_t* pref0 = reinterpret_cast<const uint32_t*>(sm + P.off_pref0);
+  const uint32_t npairs = misc->pairs;
+  const uint32_t h0 = misc->hot[0];
+  const uint64_t full_bits = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
+  const uint32_t sr = P.sr, w = P.w;
+  const uint16_t* cols0 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[0]);
+  const uint16_t* cols1 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[1]);
+  const uint32_t* b1 = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[1]);
+
+  uint64_t since_flush = 0;
+  volatile uint32_t* abort_flag = &misc->abort;
+
+  for (uint32_t t = threadIdx.x; t < npairs; t += blockDim.x) {
+    if (!kEmit && *abort_flag) break;
+    // locate the row-0 entry owning pair t: last j with pref0[j] <= t
+    uint32_t lo = 0, hi = h0;  // pref0 has h0+1 entries, pref0[h0] = npairs
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pref0[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t j0 = lo;
+    const uint32_t c0 = cols0[j0];
+    const uint64_t v0 = scatter_col(c0, P.isb[0], P.ibn[0], w);
+    const uint32_t key1 = pext32(index_of(v0, P.isb[1], P.ibn[1], w) & P.keymask[1], P.keymask[1]);
+    const uint32_t c1 = cols1[b1[key1] + (t - pref0[j0])];
+    const uint64_t v1 = scatter_col(c1, P.isb[1], P.ibn[1], w);
+    uint64_t lp_stack[SSPD_MAX_SR];
+    uint64_t and_stack[SSPD_MAX_SR];
+    uint32_t lo_stack[SSPD_MAX_SR], hi_stack[SSPD_MAX_SR];
+    const uint64_t and01 = full_bits & load_reg(sm + P.off_regs[0], c0, P.reg_bytes) &
+                           load_reg(sm + P.off_regs[1], c1, P.reg_bytes);
+    const uint64_t lp01 = v0 | v1;
+
+    auto leaf = [&](uint64_t lp, uint64_t acc_and) {
+      if (kEmit) {
+        const uint32_t wgt = (uint32_t)__popcll(acc_and);
+        if (wgt >= 3) {
+          const unsigned long long slot = atomicAdd(out_count, 1ull);
+          if (slot < out_capacity) {
+            out_ip[slot] = (uint32_t)((lp << P.r) | rp);
+            out_aux[slot] = (rp << 8) | wgt;
+          }
+        }
+      } else {
+        if (++since_flush == 64) {
+          const unsigned long long before = atomicAdd(&misc->total, since_flush);
+          since_flush = 0;
+          if (before + 64 > cap) *abort_flag = 1u;
+        }
+      }
+    };
+
+    if (sr == 2) {
+      leaf(lp01, and01);
+      continue;
+    }
+    // explicit-stack walk over rows 2 .. sr-1
+    uint32_t lvl = 2;
+    lp_stack[2] = lp01;
+    and_stack[2] = and01;
+    {
+      const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[2]);
+      const uint32_t key = pext32(index_of(lp01, P.isb[2], P.ibn[2], w) & P.keymask[2], P.keymask[2]);
+      lo_stack[2] = bs[key];
+      hi_stack[2] = bs[key + 1];
+    }
+    while (true) {
+      if (lo_stack[lvl] < hi_stack[lvl]) {
+        const uint16_t* cols = reinterpret_cast<const uint16_t*>(sm + P.off_cols[lvl]);
+        const uint32_t c = cols[lo_stack[lvl]++];
+        const uint64_t nlp = lp_stack[lvl] | scatter_col(c, P.isb[lvl], P.ibn[lvl], w);
+        const uint64_t nand = and_stack[lvl] & load_reg(sm + P.off_regs[lvl], c, P.reg_bytes);
+        if (lvl + 1 == sr) {
+          leaf(nlp, nand);
+          if (!kEmit && *abort_flag) break;
+        } else {
+          ++lvl;
+          lp_stack[lvl] = nlp;
+          and_stack[lvl] = nand;
+          const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[lvl]);
+          const uint32_t key =
+              pext32(index_of(nlp, P.isb[lvl], P.ibn[lvl], w) & P.keymask[lvl], P.keymask[lvl]);
+          lo_stack[lvl] = bs[key];
+          hi_stack[lvl] = bs[key + 1];
+        }
+      } else {
+        if (--lvl < 2) break;
+      }
+    }
+  }
+  if (!kEmit && since_flush) {
+    const unsigned long long before = atomicAdd(&misc->total, since_flush);
+    if (before + since_flush > cap) *abort_flag = 1u;
+  }
+}
+
+__global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict__ seav,
+                                                      const __grid_constant__ RestorePlan P, uint32_t rp_begin,
+                                                      uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
+                                                      uint64_t out_capacity, unsigned long long* out_count,
+                                                      uint8_t* overflow) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t rp = rp_begin + blockIdx.x;
+  Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
+  const uint32_t sr = P.sr;
+
+  // stage the SEA's registers and clear the bucket tables
+  for (uint32_t i = 0; i < sr; ++i) {
+    const uint32_t nbytes = P.sc[i] * P.reg_bytes;
+    const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * nbytes;
+    uint8_t* dst = sm + P.off_regs[i];
+    if ((nbytes & 15u) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+      for (uint32_t o = threadIdx.x * 16; o < nbytes; o += blockDim.x * 16)
+        *reinterpret_cast<uint4*>(dst + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
+    } else {
+      for (uint32_t o = threadIdx.x; o < nbytes; o += blockDim.x) dst[o] = src[o];
+    }
+    uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
+    for (uint32_t o = threadIdx.x; o <= (1u << P.nk[i]); o += blockDim.x) bs[o] = 0;
+  }
+  if (threadIdx.x == 0) {
+    misc->total = 0;
+    misc->abort = 0;
+    misc->pairs = 0;
+    for (uint32_t i = 0; i < SSPD_MAX_SR; ++i) misc->hot[i] = 0;
+  }
+  __syncthreads();
+
+  // hot registers (weight >= 3, short_sketch.py:355-362) counted per bucket
+  for (uint32_t i = 0; i < sr; ++i) {
+    uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
+    const uint8_t* regs = sm + P.off_regs[i];
+    for (uint32_t c = threadIdx.x; c < P.sc[i]; c += blockDim.x) {
+      if (__popcll(load_reg(regs, c, P.reg_bytes)) >= 3) {
+        atomicAdd(&bs[pext32(c, P.keymask[i]) + 1], 1u);
+        atomicAdd(&misc->hot[i], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = 0; i < sr; ++i)
+    if (misc->hot[i] == 0) return;  // a row without hot registers: no tuple (short_sketch.py:360-361)
+
+  // bucket starts: exclusive scan of counts stored at [1 .. 2^nk]
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t i = warp; i < sr; i += blockDim.x >> 5) {
+    uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
+    warp_exclusive_scan(bs + 1, 1u << P.nk[i]);
+  }
+  __syncthreads();
+  // scatter hot columns into their buckets; bs[key+1] advances to the end
+  // of bucket key, leaving bs[key] = start of bucket key for every key.
+  for (uint32_t i = 0; i < sr; ++i) {
+    uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
+    uint16_t* cols = reinterpret_cast<uint16_t*>(sm + P.off_cols[i]);
+    const uint8_t* regs = sm + P.off_regs[i];
+    for (uint32_t c = threadIdx.x; c < P.sc[i]; c += blockDim.x) {
+      if (__popcll(load_reg(regs, c, P.reg_bytes)) >= 3) {
+        const uint32_t pos = atomicAdd(&bs[pext32(c, P.keymask[i]) + 1], 1u);
+        cols[pos] = (uint16_t)c;
+      }
+    }
+  }
+  __syncthreads();
+
+  // flatten rows 0 x 1: pref0[j] = number of row-1 partners of row-0 entry j
+  {
+    uint32_t* pref0 = reinterpret_cast<uint32_t*>(sm + P.off_pref0);
+    const uint16_t* cols0 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[0]);
+    const uint32_t* b1 = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[1]);
+    const uint32_t h0 = misc->hot[0];
+    for (uint32_t j = threadIdx.x; j < h0; j += blockDim.x) {
+      const uint64_t v0 = scatter_col(cols0[j], P.isb[0], P.ibn[0], P.w);
+      const uint32_t key = pext32(index_of(v0, P.isb[1], P.ibn[1], P.w) & P.keymask[1], P.keymask[1]);
+      pref0[j] = b1[key + 1] - b1[key];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t total = warp_exclusive_scan(pref0, h0);
+      if (threadIdx.x == 0) {
+        pref0[h0] = total;
+        misc->pairs = total;
+      }
+    }
+    __syncthreads();
+  }
+
+  restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count);
+  __syncthreads();
+  if (misc->total > cap) {
+    if (threadIdx.x == 0) overflow[blockIdx.x] = 1;
+    return;
+  }
+  restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count);
+}
+
+// ------------------------------------------------------------------ filter
+// One warp per candidate: AND of the LR row cells, popcount, z0 = k - pop.
+__global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__ ldca,
+                                                     const __grid_constant__ sspd_params p,
+                                                     const uint32_t* __restrict__ ips, uint64_t n,
+                                                     const uint8_t* __restrict__ keep_table, uint32_t* z0_out,
+                                                     uint8_t* keep_out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t cell_bytes = p.k >> 3;
+  for (uint64_t j = warp; j < n; j += nwarps) {
+    const uint32_t ip = ips[j];
+    // lane i (and i+32) hashes row i once; cells are broadcast by shuffle
+    const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, p.seed_lh[lane], p.div_lc)) * cell_bytes : 0;
+    const uint64_t off_b =
+        lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, p.seed_lh[lane + 32], p.div_lc)) * cell_bytes : 0;
+    uint32_t pop = 0;
+    if ((p.k & 31u) == 0) {
+      const uint32_t words = p.k >> 5;
+      for (uint32_t base = 0; base < words; base += 32) {
+        const uint32_t wd = base + lane;
+        uint32_t acc = 0xFFFFFFFFu;
+        for (uint32_t i = 0; i < p.lr; ++i) {
+          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+          if (wd < words) acc &= __ldg(reinterpret_cast<const uint32_t*>(ldca + off) + wd);
+        }
+        if (wd < words) pop += __popc(acc);
+      }
+    } else {
+      for (uint32_t base = 0; base < cell_bytes; base += 32) {
+        const uint32_t by = base + lane;
+        uint32_t acc = 0xFFu;
+        for (uint32_t i = 0; i < p.lr; ++i) {
+          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+          if (by < cell_bytes) acc &= ldca[off + by];
+        }
+        if (by < cell_bytes) pop += __popc(acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
+    if (lane == 0) {
+      const uint32_t z0 = p.k - pop;
+      z0_out[j] = z0;
+      if (keep_out) keep_out[j] = keep_table ? keep_table[z0] : 1;
+    }
+  }
+}
+
+// Sliding variant: a slot is a set bit iff ((now - ts) & mask) < window.
+template <typename T>
+__global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict__ pool,
+                                                             const __grid_constant__ sspd_params p, T now,
+                                                             uint64_t window, const uint32_t* __restrict__ ips,
+                                                             uint64_t n, const uint8_t* __restrict__ keep_table,
+                                                             uint32_t* z0_out, uint8_t* keep_out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t j = warp; j < n; j += nwarps) {
+    const uint32_t ip = ips[j];
+    uint32_t pop = 0;
+    for (uint32_t s = lane; s < p.k; s += 32) {
+      bool all = true;
+      for (uint32_t i = 0; i < p.lr && all; ++i) {
+        const uint64_t c = hash_range(ip, p.seed_lh[i], p.div_lc);
+        const T ts = pool[p.slot_ldca_base + ((uint64_t)i * p.lc + c) * p.k + s];
+        all = (uint64_t)(T)(now - ts) < window;
+      }
+      pop += all ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
+    if (lane == 0) {
+      const uint32_t z0 = p.k - pop;
+      z0_out[j] = z0;
+      if (keep_out) keep_out[j] = keep_table ? keep_table[z0] : 1;
+    }
+  }
+}
+
+// Stable single-CTA compaction (the report list is small: it is bounded by
+// the candidate count).
+__global__ void __launch_bounds__(1024) compact_kernel(const uint32_t* __restrict__ ip,
+                                                       const uint32_t* __restrict__ z0,
+                                                       const uint8_t* __restrict__ keep, uint64_t n,
+                                                       uint32_t* ip_out, uint32_t* z0_out,
+                                                       unsigned long long* out_count) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ unsigned long long base_s;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t start = 0; start < n; start += blockDim.x) {
+    const uint64_t j = start + threadIdx.x;
+    const uint32_t f = (j < n && keep[j]) ? 1u : 0u;
+    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, f);
+    const uint32_t before_in_warp = __popc(ballot & ((1u << lane) - 1u));
+    if (lane == 0) warp_sums[wid] = __popc(ballot);
+    __syncthreads();
+    uint32_t before_warps = 0, total = 0;
+    for (uint32_t wv = 0; wv < (blockDim.x >> 5); ++wv) {
+      if (wv < wid) before_warps += warp_sums[wv];
+      total += warp_sums[wv];
+    }
+    if (f) {
+      const unsigned long long o = base_s + before_warps + before_in_warp;
+      ip_out[o] = ip[j];
+      z0_out[o] = z0[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base_s += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out_count = base_s;
+}
+
+static int build_plan(const sspd_params& p, RestorePlan& P) {
+  memset(&P, 0, sizeof(P));
+  P.sr = p.sr;
+  P.w = p.lp_bits;
+  P.r = p.r;
+  P.reg_bytes = p.reg_bytes;
+  const uint64_t full = p.g >= 64 ? ~0ull : ((1ull << p.g) - 1ull);
+  P.full_bits_lo = (uint32_t)full;
+  P.full_bits_hi = (uint32_t)(full >> 32);
+  uint64_t seen = 0;
+  uint32_t off = 0;
+  auto align = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
+  off = align(sizeof(Misc), 16);
+  P.off_misc = 0;
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    P.isb[i] = p.isb[i];
+    P.ibn[i] = p.ibn[i];
+    P.sc[i] = p.sc[i];
+    P.seav_row_off[i] = p.seav_row_off[i];
+    const uint64_t mask = row_mask(p.isb[i], p.ibn[i], p.lp_bits);
+    const uint64_t fixed = seen & mask;
+    seen |= mask;
+    P.keymask[i] = index_of(fixed, p.isb[i], p.ibn[i], p.lp_bits);
+    P.nk[i] = (uint32_t)__builtin_popcount(P.keymask[i]);
+    P.off_bstart[i] = off;
+    off = align(off + 4u * ((1u << P.nk[i]) + 1u), 16);
+  }
+  P.off_pref0 = off;
+  off = align(off + 4u * (p.sc[0] + 1u), 16);
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    P.off_regs[i] = off;
+    off = align(off + p.sc[i] * p.reg_bytes, 16);
+  }
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    P.off_cols[i] = off;
+    off = align(off + 2u * p.sc[i], 16);
+  }
+  P.smem_bytes = off;
+  return SSPD_OK;
+}
+
+}  // namespace sspd
+
+using namespace sspd;
+
+extern "C" int sspd_restore(const uint8_t* seav, const sspd_params* p, uint32_t rp_begin, uint32_t rp_count,
+                            uint64_t cap, uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
+                            unsigned long long* out_count, uint8_t* overflow, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if ((uint64_t)rp_begin + rp_count > (1ull << p->r)) return SSPD_ERR_CONFIG;
+  if (!seav || !out_count || !overflow) return SSPD_ERR_DATA;
+  if (rp_count == 0) return SSPD_OK;
+  RestorePlan P;
+  build_plan(*p, P);
+  int dev = 0, max_smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if ((int)P.smem_bytes > max_smem) return SSPD_ERR_CONFIG;
+  if (P.smem_bytes > 48 * 1024)
+    cudaFuncSetAttribute(restore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  restore_kernel<<<rp_count, 128, P.smem_bytes, st>>>(seav, P, rp_begin, cap, out_ip, out_aux, out_capacity,
+                                                      out_count, overflow);
+  return check_launch();
+}
+
+extern "C" int sspd_sort_candidates(uint32_t* ip, uint32_t* aux, uint64_t n, void* scratch, size_t* scratch_bytes,
+                                    void* stream) {
+  if (!scratch_bytes) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t alt = ((n * sizeof(uint32_t) + 255) / 256) * 256;
+  size_t temp = 0;
+  cub::DoubleBuffer<uint32_t> keys(ip, ip), vals(aux, aux);
+  if (cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, vals, (int)(n ? n : 1), 0, 32, st) != cudaSuccess)
+    return SSPD_ERR_CUDA;
+  const size_t need = 2 * alt + temp + 256;
+  if (!scratch) {
+    *scratch_bytes = need;
+    return SSPD_OK;
+  }
+  if (*scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  if (n <= 1) return SSPD_OK;
+  uint8_t* s = static_cast<uint8_t*>(scratch);
+  uint32_t* ip_alt = reinterpret_cast<uint32_t*>(s);
+  uint32_t* aux_alt = reinterpret_cast<uint32_t*>(s + alt);
+  void* tmp = s + 2 * alt;
+  cub::DoubleBuffer<uint32_t> k2(ip, ip_alt), v2(aux, aux_alt);
+  if (cub::DeviceRadixSort::SortPairs(tmp, temp, k2, v2, (int)n, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
+  if (k2.Current() != ip) {
+    cudaMemcpyAsync(ip, k2.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(aux, v2.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+  }
+  return check_launch();
+}
+
+extern "C" int sspd_filter(const uint8_t* ldca, const sspd_params* p, const uint32_t* ips, uint64_t n,
+                           const uint8_t* keep_table, uint32_t* z0_out, uint8_t* keep_out, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0) return SSPD_OK;
+  if (!ldca || !ips || !z0_out) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = grid_for(filter_kernel, 256, n * 32);
+  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, ips, n, keep_table, z0_out, keep_out);
+  return check_launch();
+}
+
+extern "C" int sspd_filter_sliding(const void* pool, uint32_t ts_bytes, const sspd_params* p, uint64_t now_wrapped,
+                                   uint64_t window_slices, const uint32_t* ips, uint64_t n,
+                                   const uint8_t* keep_table, uint32_t* z0_out, uint8_t* keep_out, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0) return SSPD_OK;
+  if (!pool || !ips || !z0_out) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (ts_bytes) {
+#define SSPD_FS(T)                                                                                       \
+  {                                                                                                      \
+    const int grid = grid_for(filter_sliding_kernel<T>, 256, n * 32);                                   \
+    filter_sliding_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, *p, (T)now_wrapped, window_slices, ips, n, \
+                                                   keep_table, z0_out, keep_out);                        \
+    break;                                                                                               \
+  }
+    case 1: SSPD_FS(uint8_t)
+    case 2: SSPD_FS(uint16_t)
+    case 4: SSPD_FS(uint32_t)
+    case 8: SSPD_FS(uint64_t)
+#undef SSPD_FS
+    default:
+      return SSPD_ERR_CONFIG;
+  }
+  return check_launch();
+}
+
+extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, const uint8_t* keep, uint64_t n,
+                                    uint32_t* ip_out, uint32_t* z0_out, unsigned long long* out_count, void* scratch,
+                                    size_t* scratch_bytes, void* stream) {
+  (void)scratch;
+  if (scratch_bytes) *scratch_bytes = 0;
+  if (!out_count) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  compact_kernel<<<1, 1024, 0, st>>>(ip, z0, keep, n, ip_out, z0_out, out_count);
+  return check_launch();
+}

@@ -1,0 +1,230 @@
+// K1 scan_discrete and K2 scan_sliding: the per-packet hot loop.
+//
+// Reference semantics (one packet = one (hip, oip) pair):
+//   LdcaSketch.update_batch  long_sketch.py:125-135
+//     b   = H3(oip) % k
+//     c_i = LH_i(hip) % lc                     for i < LR
+//     data[i, c_i, b>>3] |= 1 << (b & 7)       == flat bit (i*lc + c_i)*k + b
+//   SeavSketch.update_batch  short_sketch.py:300-318
+//     if lsb(H1(oip) & 0xFFFFFFFF) >= tau:
+//        bit = 1 << (H2(oip) % g); rp = hip & (2^r-1); lp = (hip>>r) & (2^w-1)
+//        rows[i][rp, index_of(i, lp)] |= bit   for i < SR
+//   SlidingDetector.observe_batch sliding.py:156-185 stamps the same slots
+//   (one slot per sketch bit) with `now & mask` (plain store, sliding.py:77-79).
+//
+// B200 mapping: the input is streamed once from HBM with 16-byte
+// evict-first loads (4 packets per thread per trip); every sketch bit-set
+// is a fire-and-forget `red.relaxed.gpu.global.or.b32` into the
+// L2-resident bit arrays (idempotent OR == the paper's "no data conflict"),
+// and every sliding stamp is a plain store (all writers of one slice store
+// the same value, so no atomic is needed and none would be correct across
+// the wrap -- see DESIGN.md).
+#include <cuda_runtime.h>
+#include "sspd_common.cuh"
+#include "launch.cuh"
+
+namespace sspd {
+
+__device__ __forceinline__ void red_or(uint32_t* addr, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// ---------------------------------------------------------------- sinks
+struct DiscreteSink {
+  uint32_t* seav;  // word view of the SEAV payload (may be null)
+  uint32_t* ldca;  // word view of the LDCA payload (may be null)
+  __device__ __forceinline__ void le(uint64_t bitpos) const {
+    red_or(ldca + (bitpos >> 5), 1u << (bitpos & 31));
+  }
+  // register byte offset + bit within the (little-endian) register
+  __device__ __forceinline__ void se(uint64_t reg_byte, uint32_t bit) const {
+    uint64_t abs_bit = reg_byte * 8 + bit;
+    red_or(seav + (abs_bit >> 5), 1u << (abs_bit & 31));
+  }
+};
+
+template <typename T>
+struct SlidingSink {
+  T* pool;
+  T now;
+  __device__ __forceinline__ void le_slot(uint64_t slot) const { pool[slot] = now; }
+  __device__ __forceinline__ void se_slot(uint64_t slot) const { pool[slot] = now; }
+};
+
+// ------------------------------------------------------------ per packet
+template <bool kSeav, bool kLdca>
+__device__ __forceinline__ void packet_discrete(uint32_t hip, uint32_t oip, const sspd_params& p,
+                                                const DiscreteSink& s, uint32_t tmask) {
+  if (kLdca) {
+    const uint64_t b = hash_range(oip, p.seed_h3, p.div_k);
+    const uint64_t k = p.k;
+    uint64_t cell = 0;  // i * lc
+#pragma unroll 8
+    for (uint32_t i = 0; i < p.lr; ++i) {
+      const uint64_t c = hash_range(hip, p.seed_lh[i], p.div_lc);
+      s.le((cell + c) * k + b);
+      cell += p.lc;
+    }
+  }
+  if (kSeav) {
+    if (sampled(oip, p.seed_h1, tmask)) {
+      const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+      const uint64_t rp = hip & ((1u << p.r) - 1u);
+      const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+      for (uint32_t i = 0; i < p.sr; ++i) {
+        const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+        s.se(p.seav_row_off[i] + (rp * p.sc[i] + col) * p.reg_bytes, bit);
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void packet_sliding(uint32_t hip, uint32_t oip, const sspd_params& p,
+                                               const SlidingSink<T>& s, uint32_t tmask) {
+  if (sampled(oip, p.seed_h1, tmask)) {
+    const uint64_t bit = hash_range(oip, p.seed_h2, p.div_g);
+    const uint64_t rp = hip & ((1u << p.r) - 1u);
+    const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+    for (uint32_t i = 0; i < p.sr; ++i) {
+      const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+      s.se_slot(p.slot_row_base[i] + (rp * p.sc[i] + col) * p.g + bit);
+    }
+  }
+  const uint64_t b = hash_range(oip, p.seed_h3, p.div_k);
+  const uint64_t k = p.k;
+  uint64_t cell = 0;
+#pragma unroll 8
+  for (uint32_t i = 0; i < p.lr; ++i) {
+    const uint64_t c = hash_range(hip, p.seed_lh[i], p.div_lc);
+    s.le_slot(p.slot_ldca_base + (cell + c) * k + b);
+    cell += p.lc;
+  }
+}
+
+// -------------------------------------------------------------- kernels
+// Grid-stride over 16-byte quads of hips/oips (both 16-byte aligned, checked
+// by the host); the scalar head/tail is handled by the same kernel.
+template <bool kSeav, bool kLdca>
+__global__ void __launch_bounds__(256) scan_discrete_kernel(const uint32_t* __restrict__ hips,
+                                                            const uint32_t* __restrict__ oips,
+                                                            uint64_t n, const __grid_constant__ sspd_params p,
+                                                            uint32_t* seav, uint32_t* ldca) {
+  const DiscreteSink s{seav, ldca};
+  const uint32_t tmask = tau_mask(p.tau);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nq = n >> 2;
+  const uint4* hq = reinterpret_cast<const uint4*>(hips);
+  const uint4* oq = reinterpret_cast<const uint4*>(oips);
+  for (uint64_t q = tid; q < nq; q += stride) {
+    const uint4 h = ld_stream(hq + q);
+    const uint4 o = ld_stream(oq + q);
+    packet_discrete<kSeav, kLdca>(h.x, o.x, p, s, tmask);
+    packet_discrete<kSeav, kLdca>(h.y, o.y, p, s, tmask);
+    packet_discrete<kSeav, kLdca>(h.z, o.z, p, s, tmask);
+    packet_discrete<kSeav, kLdca>(h.w, o.w, p, s, tmask);
+  }
+  for (uint64_t j = (nq << 2) + tid; j < n; j += stride)
+    packet_discrete<kSeav, kLdca>(hips[j], oips[j], p, s, tmask);
+}
+
+// Unaligned inputs (a numpy view at an odd offset): scalar loads only.
+template <bool kSeav, bool kLdca>
+__global__ void __launch_bounds__(256) scan_discrete_scalar_kernel(const uint32_t* __restrict__ hips,
+                                                                   const uint32_t* __restrict__ oips,
+                                                                   uint64_t n, const __grid_constant__ sspd_params p,
+                                                                   uint32_t* seav, uint32_t* ldca) {
+  const DiscreteSink s{seav, ldca};
+  const uint32_t tmask = tau_mask(p.tau);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+    packet_discrete<kSeav, kLdca>(hips[j], oips[j], p, s, tmask);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scan_sliding_kernel(const uint32_t* __restrict__ hips,
+                                                           const uint32_t* __restrict__ oips, uint64_t n,
+                                                           const __grid_constant__ sspd_params p, T* pool,
+                                                           T now) {
+  const SlidingSink<T> s{pool, now};
+  const uint32_t tmask = tau_mask(p.tau);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+    packet_sliding<T>(hips[j], oips[j], p, s, tmask);
+}
+
+template <bool S, bool L>
+static int launch_discrete(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params& p,
+                           uint8_t* seav, uint8_t* ldca, cudaStream_t st) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) == 0;
+  if (aligned) {
+    const int grid = grid_for(scan_discrete_kernel<S, L>, 256, (n + 3) / 4);
+    scan_discrete_kernel<S, L><<<grid, 256, 0, st>>>(hips, oips, n, p, reinterpret_cast<uint32_t*>(seav),
+                                                     reinterpret_cast<uint32_t*>(ldca));
+  } else {
+    const int grid = grid_for(scan_discrete_scalar_kernel<S, L>, 256, n);
+    scan_discrete_scalar_kernel<S, L><<<grid, 256, 0, st>>>(hips, oips, n, p, reinterpret_cast<uint32_t*>(seav),
+                                                            reinterpret_cast<uint32_t*>(ldca));
+  }
+  return check_launch();
+}
+
+}  // namespace sspd
+
+using namespace sspd;
+
+extern "C" int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                                  uint8_t* seav, uint8_t* ldca, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0 || (!seav && !ldca)) return SSPD_OK;
+  if (!hips || !oips) return SSPD_ERR_DATA;
+  if ((reinterpret_cast<uintptr_t>(seav) | reinterpret_cast<uintptr_t>(ldca)) & 3u) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (seav && ldca) return launch_discrete<true, true>(hips, oips, n, *p, seav, ldca, st);
+  if (seav) return launch_discrete<true, false>(hips, oips, n, *p, seav, ldca, st);
+  return launch_discrete<false, true>(hips, oips, n, *p, seav, ldca, st);
+}
+
+extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                                 void* pool, uint32_t ts_bytes, uint64_t now_wrapped, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0) return SSPD_OK;
+  if (!hips || !oips || !pool) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (ts_bytes) {
+    case 1: {
+      const int grid = grid_for(scan_sliding_kernel<uint8_t>, 256, n);
+      scan_sliding_kernel<uint8_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint8_t*)pool, (uint8_t)now_wrapped);
+      break;
+    }
+    case 2: {
+      const int grid = grid_for(scan_sliding_kernel<uint16_t>, 256, n);
+      scan_sliding_kernel<uint16_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped);
+      break;
+    }
+    case 4: {
+      const int grid = grid_for(scan_sliding_kernel<uint32_t>, 256, n);
+      scan_sliding_kernel<uint32_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint32_t*)pool, (uint32_t)now_wrapped);
+      break;
+    }
+    case 8: {
+      const int grid = grid_for(scan_sliding_kernel<uint64_t>, 256, n);
+      scan_sliding_kernel<uint64_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint64_t*)pool, (uint64_t)now_wrapped);
+      break;
+    }
+    default:
+      return SSPD_ERR_CONFIG;
+  }
+  return check_launch();
+}

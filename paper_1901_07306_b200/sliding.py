@@ -1,0 +1,282 @@
+"""Sliding-window detection over per-bit timestamps, device-backed.
+
+Mirrors `sspd/sliding.py`: every SEAV/LDCA bit becomes a wrapped
+last-active-slice stamp in one flat pool (SEAV slots first, then LDCA,
+sliding.py:119-146); a slot is live iff ((now - ts) & mask) < w
+(sliding.py:96-102); an amortised sweep every modulus - 2w slices clamps
+idle slots so wrapped ages never alias (sliding.py:81-94).
+
+The pool is one device buffer of the smallest unsigned stamp type; the
+observe path (K2) is a plain-store kernel, and detect materialises the SEAV
+view (K4), restores (K5) and filters straight from the pool (K6 sliding).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigError
+from .long_sketch import ldc_estimate
+from .short_sketch import SeavSketch
+from .window_detector import DetectionReport, DetectorParams, filter_candidates
+
+_UNSIGNED = ((1, np.uint8), (2, np.uint16), (4, np.uint32), (8, np.uint64))
+
+
+def timestamp_dtype(window_slices: int):
+    """Smallest unsigned dtype whose modulus is >= 2w + 2 (sliding.py:24-30)."""
+    need = 2 * window_slices + 2
+    for nbytes, dt in _UNSIGNED:
+        if need <= (1 << (8 * nbytes)):
+            return dt
+    raise ConfigError(f"window of {window_slices} slices is too large to timestamp")
+
+
+def _signed_torch(nbytes: int):
+    import torch
+
+    return {1: torch.int8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[nbytes]
+
+
+def _as_signed(value: int, nbytes: int) -> int:
+    bits = 8 * nbytes
+    value &= (1 << bits) - 1
+    return value - (1 << bits) if value >= (1 << (bits - 1)) else value
+
+
+class TimestampPool:
+    """Fixed pool of wrapped per-slot stamps with lazy expiry (sliding.py:33-106)."""
+
+    def __init__(self, n_slots: int, window_slices: int, slice_seconds: float = 1.0):
+        import torch
+
+        from ._device import device
+
+        if n_slots < 1:
+            raise ConfigError(f"slot count must be >= 1, got {n_slots}")
+        if window_slices < 1:
+            raise ConfigError(f"window must span >= 1 slice, got {window_slices}")
+        self.n_slots = n_slots
+        self.window_slices = window_slices
+        self.slice_seconds = slice_seconds
+        self.now = 0
+        self.dtype = timestamp_dtype(window_slices)
+        self.ts_bytes = np.dtype(self.dtype).itemsize
+        self._modulus = 1 << (8 * self.ts_bytes)
+        self._mask = self._modulus - 1
+        self._sweep_period = self._modulus - 2 * window_slices
+        self._since_sweep = 0
+        self.sweep_count = 0
+        init = (-window_slices) & self._mask  # age == window: just expired
+        self._buf = torch.full((n_slots,), _as_signed(init, self.ts_bytes),
+                               dtype=_signed_torch(self.ts_bytes), device=device())
+
+    # -- state --------------------------------------------------------------
+    def device_buffer(self):
+        return self._buf
+
+    @property
+    def ts(self) -> np.ndarray:
+        return self._buf.cpu().numpy().view(self.dtype)
+
+    @ts.setter
+    def ts(self, values: np.ndarray):
+        import torch
+
+        arr = np.ascontiguousarray(np.asarray(values, dtype=self.dtype))
+        if arr.shape != (self.n_slots,):
+            raise ConfigError("timestamp array shape mismatch")
+        signed = arr.view(_signed_torch_np(self.ts_bytes))
+        self._buf.copy_(torch.from_numpy(signed))
+
+    def memory_bytes(self) -> int:
+        return self.n_slots * self.ts_bytes
+
+    def _wrapped_now(self) -> int:
+        return self.now & self._mask
+
+    # -- updates ------------------------------------------------------------
+    def touch(self, slot_index: int, now: int | None = None):
+        """Stamp one slot; an older stamp never overwrites a newer one."""
+        if not 0 <= slot_index < self.n_slots:
+            raise ConfigError(f"slot {slot_index} out of range [0, {self.n_slots})")
+        now = self.now if now is None else now
+        candidate_age = self.now - now
+        if candidate_age < 0:
+            raise ConfigError(f"cannot stamp future slice {now} (pool is at {self.now})")
+        current = int(self._buf[slot_index].item()) & self._mask
+        existing_age = (self._wrapped_now() - current) & self._mask
+        if candidate_age < existing_age:
+            self._buf[slot_index] = _as_signed(now & self._mask, self.ts_bytes)
+
+    def touch_batch(self, slot_indexes):
+        import torch
+
+        idx = torch.as_tensor(np.asarray(slot_indexes, dtype=np.int64)).to(self._buf.device)
+        self._buf.index_fill_(0, idx, _as_signed(self._wrapped_now(), self.ts_bytes))
+
+    def advance_slice(self):
+        self.now += 1
+        self._since_sweep += 1
+        if self._since_sweep >= self._sweep_period:
+            self._sweep()
+
+    def _sweep(self):
+        from ._device import call, stream_ptr
+
+        clamp = (self.now - self.window_slices) & self._mask
+        call("sspd_sweep", self._buf.data_ptr(), self.n_slots, self.ts_bytes, self._wrapped_now(),
+             self.window_slices, clamp, stream_ptr())
+        self._since_sweep = 0
+        self.sweep_count += 1
+
+    # -- queries ------------------------------------------------------------
+    def ages(self) -> np.ndarray:
+        import torch
+
+        from ._device import call, stream_ptr
+
+        out = torch.empty(self.n_slots, dtype=torch.int64, device=self._buf.device)
+        call("sspd_pool_ages", self._buf.data_ptr(), self.n_slots, self.ts_bytes, self._wrapped_now(),
+             out.data_ptr(), stream_ptr())
+        return out.cpu().numpy().view(np.uint64)
+
+    def active(self) -> np.ndarray:
+        return self.ages() < self.window_slices
+
+    def is_active(self, slot_index: int) -> bool:
+        current = int(self._buf[slot_index].item()) & self._mask
+        return ((self._wrapped_now() - current) & self._mask) < self.window_slices
+
+
+def _signed_torch_np(nbytes: int):
+    return {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}[nbytes]
+
+
+def touch(pool: TimestampPool, slot_index: int, now: int) -> TimestampPool:
+    pool.touch(slot_index, now)
+    return pool
+
+
+def advance_slice(pool: TimestampPool) -> TimestampPool:
+    pool.advance_slice()
+    return pool
+
+
+@dataclass(frozen=True)
+class _SlotLayout:
+    seav_row_base: tuple[int, ...]
+    ldca_base: int
+    total: int
+
+
+class SlidingDetector:
+    """Sliding-window pipeline over one device timestamp pool (sliding.py:128-248)."""
+
+    def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
+                 slice_seconds: float = 1.0):
+        from ._abi import build_params
+        from .hashing import SeedFamily
+
+        self.params = params or DetectorParams()
+        self.seeds = SeedFamily(self.params.master_seed)
+        self.seav_config = self.params.seav_config()
+        self.ldca_config = self.params.ldca_config()
+        self._params = build_params(self.seav_config, self.ldca_config, self.seeds)
+        p = self._params
+        self.layout = _SlotLayout(tuple(int(p.slot_row_base[i]) for i in range(self.seav_config.sr)),
+                                  int(p.slot_ldca_base), int(p.slot_total))
+        self.pool = TimestampPool(self.layout.total, window_slices, slice_seconds)
+        self.pair_count = 0
+
+    @property
+    def now(self) -> int:
+        return self.pool.now
+
+    def advance_slice(self):
+        self.pool.advance_slice()
+
+    def observe_batch(self, hips, oips):
+        """K2: stamp every slot the discrete path would set (sliding.py:156-185)."""
+        from ._device import call, ips_to_device, stream_ptr
+
+        h = ips_to_device(hips, "hips")
+        o = ips_to_device(oips, "oips")
+        if h.numel() != o.numel():
+            raise ConfigError("hips and oips differ in length")
+        pool = self.pool
+        call("sspd_scan_sliding", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+             pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), stream_ptr())
+        self.pair_count += int(h.numel())
+
+    def observe(self, hip: int, oip: int):
+        self.observe_batch(np.array([hip], dtype=np.uint64), np.array([oip], dtype=np.uint64))
+
+    def _materialize_into(self, sketch: SeavSketch):
+        from ._device import call, stream_ptr
+
+        pool = self.pool
+        call("sspd_materialize_seav", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, sketch.device_buffer().data_ptr(), stream_ptr())
+
+    def materialize_seav(self) -> SeavSketch:
+        sketch = SeavSketch(self.seav_config, self.seeds, restore_cap=self.params.restore_cap,
+                            _ldca_config=self.ldca_config)
+        self._materialize_into(sketch)
+        return sketch
+
+    def materialize_ldca(self) -> np.ndarray:
+        from ._device import call, stream_ptr, zeros_bytes
+
+        pool = self.pool
+        lc = self.ldca_config
+        nbytes = lc.lr * lc.lc * lc.k // 8
+        out = zeros_bytes(nbytes)
+        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, out.data_ptr(), stream_ptr())
+        return out[:nbytes].cpu().numpy().reshape(lc.lr, lc.lc, lc.k // 8)
+
+    def materialize_ldca_cell(self, row: int, col: int) -> np.ndarray:
+        lc = self.ldca_config
+        base = self.layout.ldca_base + (row * lc.lc + col) * lc.k
+        ts = self.pool.device_buffer()[base:base + lc.k].cpu().numpy().view(self.pool.dtype).astype(np.uint64)
+        ages = (np.uint64(self.pool._wrapped_now()) - ts) & np.uint64(self.pool._mask)
+        return np.packbits((ages < self.pool.window_slices).astype(np.uint8), bitorder="little")
+
+    def _estimate(self, hip: int) -> tuple[float, bool]:
+        import torch
+
+        from ._device import call, ips_to_device, stream_ptr
+
+        h = ips_to_device(np.array([hip], dtype=np.uint64))
+        z0 = torch.empty(1, dtype=torch.int32, device=h.device)
+        pool = self.pool
+        call("sspd_filter_sliding", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, h.data_ptr(), 1, None, z0.data_ptr(), None,
+             stream_ptr())
+        return ldc_estimate(int(z0.item()) & 0xFFFFFFFF, self.ldca_config.k)
+
+    def detect(self, beta: float | None = None) -> list[DetectionReport]:
+        """Materialise (K4) -> restore (K5) -> filter on the pool (K6) (sliding.py:232-248)."""
+        beta = self.params.beta if beta is None else beta
+        cutoff = beta * self.params.theta
+        seav = self.materialize_seav()
+        pool = self.pool
+        k = self.ldca_config.k
+        ips, z0s = filter_candidates(
+            seav, None, self._params, k, cutoff,
+            sliding=(pool.device_buffer(), pool.ts_bytes, pool._wrapped_now(), pool.window_slices))
+        out = []
+        for ip, z0 in zip(ips, z0s):
+            est, saturated = ldc_estimate(z0, k)
+            out.append(DetectionReport(ip=ip, estimated_cardinality=est, saturated=saturated,
+                                       window_id=self.now, source="sliding"))
+        return out
+
+
+def detect_sliding(detector: SlidingDetector, theta: int | None = None, beta: float | None = None):
+    if theta is not None and theta != detector.params.theta:
+        raise ValueError(f"detector was configured with theta={detector.params.theta}, got {theta}")
+    return detector.detect(beta=beta)

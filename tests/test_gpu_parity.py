@@ -1,0 +1,210 @@
+"""CUDA path vs the reference's golden vectors and the pinned CPU oracle.
+
+Every test here drives the drop-in API (paper_1901_07306_b200) -> ctypes ->
+libsspd_b200.so kernels on the GPU.  Bar: bit-exact bytes, identical
+candidate lists, identical reports (float estimates compared with ==).
+"""
+
+import hashlib
+import warnings
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import params_block, params_from
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def rep_list(reps):
+    return [[r.ip, repr(r.estimated_cardinality), r.saturated, r.window_id, r.source] for r in reps]
+
+
+def make_state(dp):
+    from paper_1901_07306_b200 import DetectorState
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return DetectorState.create(dp)
+
+
+@pytest.mark.parametrize("idx", range(12))
+def test_golden_sketch_cases(cuda, golden, garr, idx):
+    if idx >= len(golden["sketches"]):
+        pytest.skip("no such case")
+    case = golden["sketches"][idx]
+    dp = params_from(case["params"])
+    st = make_state(dp)
+    st.process_batch(garr[case["hips"]], garr[case["oips"]])
+    assert sha(st.seav.payload_bytes()) == case["seav_sha"], case["name"]
+    assert sha(st.ldca.payload_bytes()) == case["ldca_sha"], case["name"]
+    with warnings.catch_warnings(record=True) as wl:
+        warnings.simplefilter("always")
+        cands = st.seav.restore(on_overflow="warn")
+    over = sorted(int(str(w.message).split("rp=")[1].split()[0]) for w in wl if "rp=" in str(w.message))
+    assert over == case["overflow"]
+    assert [[c.ip, c.source_sea, c.union_weight] for c in cands] == case["candidates"]
+    for ip, z0 in case["z0"]:
+        assert int(st.ldca.zero_counts(np.array([ip]))[0]) == z0
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        assert rep_list(st.finalize_window()) == [r[:3] + [0, "discrete"] for r in case["reports"]]
+
+
+def test_config1_end_to_end(cuda, golden):
+    from paper_1901_07306_b200 import DetectorParams
+    from tools.workloads import CONFIG1, generate
+
+    c = golden["config1"]
+    hips, oips, _ = generate(CONFIG1)
+    st = make_state(DetectorParams())
+    for lo in range(0, len(hips), 1 << 16):  # the CLI's 64 Ki-pair buffers (cli.py:215-217)
+        st.process_batch(hips[lo:lo + (1 << 16)], oips[lo:lo + (1 << 16)])
+    assert sha(st.seav.payload_bytes()) == c["seav_sha"]
+    assert sha(st.ldca.payload_bytes()) == c["ldca_sha"]
+    assert [[x.ip, x.source_sea, x.union_weight] for x in st.seav.restore()] == c["candidates"]
+    assert rep_list(st.finalize_window()) == c["reports"]
+    # one launch over the whole window gives the same state
+    st2 = make_state(DetectorParams())
+    st2.process_batch(hips, oips)
+    assert st2.seav.payload_bytes() == st.seav.payload_bytes()
+    assert st2.ldca.payload_bytes() == st.ldca.payload_bytes()
+
+
+def test_config1_device_generated_stream(cuda, golden):
+    """The torch/CUDA generator backend emits the identical stream."""
+    import torch
+
+    from tools.workloads import CONFIG1, generate
+
+    h, o, _ = generate(CONFIG1, "torch", cuda)
+    hb = h.cpu().numpy().view(np.uint32)
+    ob = o.cpu().numpy().view(np.uint32)
+    assert sha(hb.tobytes() + ob.tobytes()) == golden["config1"]["stream_sha"]
+    del torch
+
+
+def test_overflow_semantics(cuda, golden, garr):
+    from paper_1901_07306_b200 import SeaOverflowError, SeavConfig, SeavSketch, SeedFamily
+
+    g = golden["overflow"]
+    sk = SeavSketch(SeavConfig(), SeedFamily(), restore_cap=g["cap"])
+    sk.load_payload(garr[g["payload"]].tobytes())
+    with pytest.warns(RuntimeWarning, match="rp=3"):
+        cands = sk.restore(on_overflow="warn")
+    assert [[c.ip, c.source_sea, c.union_weight] for c in cands] == g["candidates"]
+    with pytest.raises(SeaOverflowError) as err:
+        sk.restore()
+    assert err.value.rp == 3
+    with pytest.raises(SeaOverflowError):
+        sk.restore_sea(7)
+    assert sk.restore_sea(1) == [c for c in cands if c.source_sea == 1]
+    big = SeavSketch(SeavConfig(), SeedFamily(), restore_cap=10**9)
+    big.load_payload(garr[g["payload"]].tobytes())
+    # 3.3 M tuples counted exactly, emitted only when weight >= 3
+    assert len(big.restore_sea(7)) == g["rp7_uncapped_count"]
+
+
+@pytest.mark.parametrize("geom", [
+    dict(theta=64, r=4, k=1024, lr=3, lc=32),
+    dict(theta=32, r=2, sr=5, a=1, k=2048, lr=4, lc=100),
+    dict(theta=128, r=8, g=16, k=1000, lr=5, lc=77),
+    dict(theta=16, r=2, sr=6, a=1, g=32, k=512, lr=9, lc=64),
+    dict(theta=4096, r=8, sr=3, a=4, g=64, k=2048, lr=2, lc=512),
+    dict(theta=1024, r=12, k=8192, lr=8, lc=1024),
+    dict(theta=256, r=16, k=4096, lr=2, lc=4096),
+    dict(theta=8, r=4, addr_bits=16, k=256, lr=2, lc=16),
+])
+def test_random_streams_vs_oracle(cuda, oracle, geom):
+    """Geometries beyond the golden set, checked against the pinned oracle."""
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(design_n=1e5, **geom)
+    _, lcfg, p = params_block(dp)
+    rng = np.random.default_rng(zlib.crc32(repr(sorted(geom.items())).encode()))
+    n = 300_000
+    span = 1 << dp.addr_bits
+    hips = rng.integers(0, span, size=n, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    heavy = rng.integers(0, span, size=12, dtype=np.uint64)
+    for i, h in enumerate(heavy):
+        hips[i * 6000:(i + 1) * 6000 - i * 300] = h
+    st = make_state(dp)
+    st.process_batch(hips, oips)
+    seav, ldca = oracle.scan(p, hips, oips, threads=8)
+    assert st.seav.payload_bytes() == seav.tobytes()
+    assert st.ldca.payload_bytes() == ldca.tobytes()
+    ips, rps, ws, over = oracle.restore(p, seav, dp.restore_cap)
+    with warnings.catch_warnings(record=True):
+        warnings.simplefilter("always")
+        got = st.seav.restore(on_overflow="warn")
+    assert [(c.ip, c.source_sea, c.union_weight) for c in got] == list(
+        zip(ips.tolist(), rps.tolist(), ws.tolist()))
+    z0 = oracle.filter_z0(p, ldca, ips)
+    assert (st.ldca.zero_counts(ips) == z0).all()
+
+
+def test_edge_inputs(cuda):
+    from paper_1901_07306_b200 import DataError, DetectorParams
+
+    st = make_state(DetectorParams(design_n=2e5))
+    st.process_batch(np.array([], dtype=np.uint32), np.array([], dtype=np.uint32))
+    assert st.seav.total_set_bits() == 0 and st.finalize_window() == []
+    st.process_pair(0xC0A80101, 0xDEADBEEF)
+    assert st.pair_count == 1
+    assert 1 <= int(np.unpackbits(st.ldca.data).sum()) <= st.ldca.config.lr
+    with pytest.raises(DataError):
+        st.process_batch(np.array([2**32], dtype=np.uint64), np.array([1], dtype=np.uint64))
+    with pytest.raises(DataError):
+        st.process_batch(np.array([-1], dtype=np.int64), np.array([1], dtype=np.int64))
+
+
+def test_unaligned_and_ragged_batches(cuda, oracle):
+    """Odd offsets take the scalar kernel; any split gives the same state."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(theta=64, design_n=2e5)
+    _, _, p = params_block(dp)
+    rng = np.random.default_rng(3)
+    n = 100_003
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    seav, ldca = oracle.scan(p, hips, oips, threads=8)
+    st = make_state(dp)
+    h = torch.from_numpy(hips.view(np.int32)).cuda()
+    o = torch.from_numpy(oips.view(np.int32)).cuda()
+    for lo, hi in [(0, 1), (1, 7), (7, 4099), (4099, 50_000), (50_000, n)]:
+        st.process_batch(h[lo:hi], o[lo:hi])  # device views at unaligned offsets
+    assert st.seav.payload_bytes() == seav.tobytes()
+    assert st.ldca.payload_bytes() == ldca.tobytes()
+
+
+def test_reset_replay_and_merge(cuda):
+    from paper_1901_07306_b200 import DetectorParams
+
+    rng = np.random.default_rng(10)
+    hips = rng.integers(0, 2**32, size=50_000, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=50_000, dtype=np.uint64)
+    dp = DetectorParams(theta=128, design_n=2e5)
+    st = make_state(dp)
+    st.process_batch(hips, oips)
+    a, b = st.seav.payload_bytes(), st.ldca.payload_bytes()
+    st.reset()
+    assert st.window_id == 1 and st.seav.total_set_bits() == 0 and not st.ldca.data.any()
+    st.process_batch(hips, oips)
+    st.process_batch(hips, oips)  # idempotent OR
+    assert st.seav.payload_bytes() == a and st.ldca.payload_bytes() == b
+    shards = [make_state(dp) for _ in range(4)]
+    for w in range(4):
+        shards[w].process_batch(hips[w::4], oips[w::4])
+    for s in shards[1:]:
+        shards[0].seav.merge(s.seav)
+        shards[0].ldca.merge(s.ldca)
+    assert shards[0].seav.payload_bytes() == a and shards[0].ldca.payload_bytes() == b

@@ -1,0 +1,180 @@
+"""Sliding-window pool kernels and the distributed merge on the GPU vs the
+reference's golden vectors."""
+
+import hashlib
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import params_from
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def rep_list(reps):
+    return [[r.ip, repr(r.estimated_cardinality), r.saturated, r.window_id, r.source] for r in reps]
+
+
+def test_sliding_golden_steps(cuda, golden, garr):
+    from paper_1901_07306_b200 import SlidingDetector
+
+    g = golden["sliding"]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(params_from(g["params"]), window_slices=g["w"])
+    hips, oips, slices = garr[g["hips"]], garr[g["oips"]], garr[g["slices"]]
+    for step in g["steps"]:
+        sel = slices == step["slice"]
+        det.observe_batch(hips[sel], oips[sel])
+        assert det.now == step["now"]
+        assert sha(det.pool.ts.tobytes()) == step["pool_sha"], step["slice"]
+        if step["seav_view_sha"]:
+            assert sha(det.materialize_seav().payload_bytes()) == step["seav_view_sha"]
+            assert sha(det.materialize_ldca().tobytes()) == step["ldca_view_sha"]
+        if step["reports"] is not None:
+            assert rep_list(det.detect()) == step["reports"], step["slice"]
+        det.advance_slice()
+
+
+def test_wraparound_sweep_golden(cuda, golden):
+    from paper_1901_07306_b200 import TimestampPool
+
+    pool = TimestampPool(64, window_slices=100)
+    assert pool.ts.dtype == np.uint8
+    rng = np.random.default_rng(9)
+    snaps = iter(golden["wrap"]["snaps"])
+    for now in range(1, 1200):
+        pool.advance_slice()
+        if now % 7 == 0 and now <= 900:
+            pool.touch_batch(rng.integers(0, 64, size=5))
+        if now % 50 == 0:
+            snap = next(snaps)
+            assert pool.sweep_count == snap[1]
+            assert sha(pool.ts.tobytes()) == snap[2]
+            assert pool.active().astype(np.uint8).tolist() == snap[3]
+
+
+def test_pool_scalar_api(cuda):
+    from paper_1901_07306_b200 import ConfigError, TimestampPool
+
+    pool = TimestampPool(4, window_slices=10)
+    for _ in range(6):
+        pool.advance_slice()
+    pool.touch(1, now=6)
+    pool.touch(1, now=3)  # older stamp loses
+    for _ in range(9):
+        pool.advance_slice()
+    assert pool.is_active(1)
+    pool.advance_slice()
+    assert not pool.is_active(1)
+    with pytest.raises(ConfigError):
+        pool.touch(0, now=pool.now + 1)
+    with pytest.raises(ConfigError):
+        pool.touch(4)
+
+
+def test_merge_pools_golden(cuda, golden, garr):
+    from paper_1901_07306_b200 import TimestampPool, merge_timestamp_pools
+
+    g = golden["merge_pools"]
+    pools = []
+    for name in g["inputs"]:
+        p = TimestampPool(len(garr[name]), window_slices=g["w"])
+        p.now = g["now"]
+        p.ts = garr[name]
+        pools.append(p)
+    merged = merge_timestamp_pools(pools)
+    assert (merged.ts == garr[g["merged"]]).all()
+
+
+def test_sliding_equals_discrete(cuda):
+    """One slide covering the whole stream == the discrete window, bit-exact
+    (test_acceptance.py:190-218 criterion 8)."""
+    from paper_1901_07306_b200 import DetectorParams, DetectorState, SlidingDetector
+
+    params = DetectorParams(theta=1024, k=8192, lr=2, lc=512, design_n=3e4)
+    w = 300
+    rng = np.random.default_rng(800)
+    n = 300_000
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    hips[:3000] = 0x0A0B0C0D
+    hips[3000:4000] = 0x0A0B0C0E
+    slices = rng.integers(0, w, size=n)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        disc = DetectorState.create(params)
+        det = SlidingDetector(params, window_slices=w)
+    disc.process_batch(hips, oips)
+    for s in range(w):
+        sel = slices == s
+        det.observe_batch(hips[sel], oips[sel])
+        if s < w - 1:
+            det.advance_slice()
+    assert det.materialize_seav().payload_bytes() == disc.seav.payload_bytes()
+    assert (det.materialize_ldca() == disc.ldca.data).all()
+    a = [(r.ip, r.estimated_cardinality, r.saturated) for r in det.detect()]
+    b = [(r.ip, r.estimated_cardinality, r.saturated) for r in disc.finalize_window()]
+    assert a == b and len(b) >= 1
+
+
+def test_route_golden(cuda, golden, garr):
+    from paper_1901_07306_b200 import SeedFamily, route_pairs
+
+    g = golden["route"]
+    for n_wp in (1, 3, 7, 8, 16):
+        assert (route_pairs(garr[g["hips"]], garr[g["oips"]], n_wp, "hash", SeedFamily())
+                == garr[g[f"hash_{n_wp}"]]).all()
+    rr = route_pairs(garr[g["hips"]], garr[g["oips"]], 3, "round-robin", SeedFamily())
+    assert (rr == np.arange(len(rr)) % 3).all()
+
+
+def test_frames_and_merge_golden(cuda, golden, garr):
+    from paper_1901_07306_b200 import DetectorState, merge_frames, parse_frame, serialize, simulate_window
+
+    g = golden["frames"]
+    params = params_from(g["params"])
+    states = []
+    for wp in range(3):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            st = DetectorState.create(params)
+        st.process_batch(garr[f"frames/h{wp}"], garr[f"frames/o{wp}"])
+        states.append(st)
+    blobs = [serialize(s.seav, 5) for s in states] + [serialize(s.ldca, 5) for s in states]
+    assert [sha(b) for b in blobs] == g["frame_sha"]
+    mseav, mldca = merge_frames([parse_frame(b) for b in blobs])
+    assert sha(mseav.payload_bytes()) == g["merged_seav_sha"]
+    assert sha(mldca.payload_bytes()) == g["merged_ldca_sha"]
+    hips = np.concatenate([garr[f"frames/h{i}"] for i in range(3)])
+    oips = np.concatenate([garr[f"frames/o{i}"] for i in range(3)])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        sim = simulate_window(params, 3, hips, oips, 4)
+    assert rep_list(sim.reports) == g["sim_reports"]
+    assert sha(sim.global_seav.payload_bytes()) == g["sim_seav_sha"]
+    assert sha(sim.global_ldca.payload_bytes()) == g["sim_ldca_sha"]
+
+
+@pytest.mark.parametrize("route", ["hash", "round-robin"])
+@pytest.mark.parametrize("n_wp", [1, 4, 16])
+def test_partition_invariance(cuda, route, n_wp):
+    from paper_1901_07306_b200 import DetectorParams, simulate_window
+
+    params = DetectorParams(theta=1024, k=4096, lr=2, lc=64, design_n=4e3)
+    rng = np.random.default_rng(6)
+    hips = rng.integers(0, 2**32, size=12_000, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=12_000, dtype=np.uint64)
+    hips[:3000] = 0x11223344
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = simulate_window(params, 0, hips, oips, 1)
+        res = simulate_window(params, 0, hips, oips, n_wp, route=route, buffer_pairs=37 if n_wp == 4 else 65536)
+    assert res.global_seav.payload_bytes() == ref.global_seav.payload_bytes()
+    assert res.global_ldca.payload_bytes() == ref.global_ldca.payload_bytes()
+    assert res.reports == ref.reports and len(res.reports) >= 1

@@ -1,0 +1,247 @@
+"""Seeded synthetic packet streams for the BASELINE.json configs.
+
+The paper's CAIDA traces are not available (no network), so
+seeded synthetic streams with the configs' shapes stand in for them.  The
+generator is counter-based: every random draw is mix64 of a (tag, seed,
+index) counter, all arithmetic is int64 bit patterns with explicit logical
+shifts, so the numpy backend (small streams, CPU oracle checks) and the
+torch/CUDA backend (full-size bench streams, generated in HBM) produce
+BIT-IDENTICAL streams for the same spec.
+
+Config resolutions (BASELINE.md §5 asks the builder to record them):
+* background cardinalities are rank-size Zipf, c_i = clip(floor(C i^-s),
+  1, c_max), C solved by bisection so distinct pairs x mean duplicates
+  fills the packet budget (SURVEY.md §8d recommendation);
+* duplicates are geometric(p) on {1, 2, ...} (mean 1/p), drawn by integer
+  inverse-CDF lookup; the stream is cut/padded to EXACTLY n packets while
+  every distinct pair is kept at least once;
+* source IPs are distinct (a keyed 32-bit bijection of the source index);
+  destination IPs are distinct per source (the same bijection of a
+  per-source random offset plus a counter).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+T_SRC, T_OFF, T_CARD, T_DUP, T_PICK, T_ORDER, T_PAD, T_DST, T_SPLIT, T_TIME = range(1, 11)
+
+
+def mix64_int(x: int) -> int:
+    z = (x + GOLDEN) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _signed(v: int) -> int:
+    v &= M64
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+@dataclass(frozen=True)
+class StreamSpec:
+    name: str
+    n_packets: int
+    n_sources: int
+    n_super: int
+    super_card: tuple[int, int]          # inclusive range
+    zipf_s: float
+    zipf_max: int
+    dup_p: float
+    seed: int = 0
+    super_log_uniform: bool = False
+
+
+CONFIG1 = StreamSpec("config1", 1 << 20, 65_536, 32, (2048, 2048), 1.1, 200, 0.4, seed=0)
+CONFIG2 = StreamSpec("config2", 1 << 28, 16_777_216, 512, (1500, 50_000), 1.05, 1000, 0.3, seed=2)
+
+
+def scaled(spec: StreamSpec, factor: int) -> StreamSpec:
+    """The same law at 1/factor size (packets and sources), for CPU checks."""
+    return replace(spec, name=f"{spec.name}/{factor}", n_packets=spec.n_packets // factor,
+                   n_sources=max(spec.n_super + 1, spec.n_sources // factor),
+                   n_super=max(1, spec.n_super // factor))
+
+
+# ---------------------------------------------------------------- backends
+class _Backend:
+    def shr(self, x, s):
+        return (x >> s) & ((1 << (64 - s)) - 1)
+
+    def mix64(self, x):
+        z = x + _signed(GOLDEN)
+        z = (z ^ self.shr(z, 30)) * _signed(0xBF58476D1CE4E5B9)
+        z = (z ^ self.shr(z, 27)) * _signed(0x94D049BB133111EB)
+        return z ^ self.shr(z, 31)
+
+    def draw(self, tag: int, seed: int, idx):
+        key = _signed(mix64_int(((seed & 0xFFFFFFFF) << 8) | tag))
+        return self.mix64(idx ^ key)
+
+    def perm32(self, x, key: int):
+        m = 0xFFFFFFFF
+        x = (x ^ (key & m)) & m
+        for mul in (0x7FEB352D, 0x846CA68B, 0x9E3779B1):
+            x = (x ^ (x >> 16)) & m
+            x = (x * mul) & m
+        return (x ^ (x >> 16)) & m
+
+
+class _NP(_Backend):
+    def __init__(self):
+        import warnings
+
+        warnings.filterwarnings("ignore", "overflow encountered", RuntimeWarning)
+
+    def arange(self, n):
+        return np.arange(n, dtype=np.int64)
+
+    def host(self, a):
+        return np.asarray(a, dtype=np.int64)
+
+    def repeat(self, v, c):
+        return np.repeat(v, c)
+
+    def cumsum(self, x):
+        return np.cumsum(x)
+
+    def argsort(self, k):
+        return np.argsort(k, kind="stable")
+
+    def searchsorted_left(self, t, x):
+        return np.searchsorted(t, x, side="left")
+
+    def cat(self, xs):
+        return np.concatenate(xs)
+
+    def total(self, x):
+        return int(x.sum())
+
+
+class _Torch(_Backend):
+    def __init__(self, device):
+        import torch
+
+        self.t = torch
+        self.dev = device
+
+    def arange(self, n):
+        return self.t.arange(n, dtype=self.t.int64, device=self.dev)
+
+    def host(self, a):
+        return self.t.as_tensor(np.asarray(a, dtype=np.int64), device=self.dev)
+
+    def repeat(self, v, c):
+        return self.t.repeat_interleave(v, c)
+
+    def cumsum(self, x):
+        return self.t.cumsum(x, 0)
+
+    def argsort(self, k):
+        return self.t.sort(k, stable=True).indices
+
+    def searchsorted_left(self, t, x):
+        return self.t.searchsorted(t, x, right=False)
+
+    def cat(self, xs):
+        return self.t.cat(xs)
+
+    def total(self, x):
+        return int(x.sum().item())
+
+
+# ------------------------------------------------------------ host tables
+def zipf_rank_size(n: int, s: float, cmax: int, target_total: int) -> np.ndarray:
+    ranks = np.arange(1, n + 1, dtype=np.float64) ** (-s)
+
+    def total(c):
+        return int(np.clip(np.floor(c * ranks), 1, cmax).sum())
+
+    lo, hi = 0.0, 1.0
+    while total(hi) < target_total and hi < 1e18:
+        hi *= 2
+    for _ in range(200):
+        mid = (lo + hi) / 2
+        if total(mid) < target_total:
+            lo = mid
+        else:
+            hi = mid
+    return np.clip(np.floor(hi * ranks), 1, cmax).astype(np.int64)
+
+
+def geometric_table(p: float, kmax: int = 96) -> np.ndarray:
+    """-floor((1-p)^k 2^53) for k = 1..kmax, ascending.  With u uniform on
+    [0, 2^53): count = 1 + #{k : u < t_k} = 1 + searchsorted_left(table, -u)."""
+    return np.array([-int(math.floor((1.0 - p) ** k * (1 << 53))) for k in range(1, kmax + 1)],
+                    dtype=np.int64)
+
+
+def cardinalities(spec: StreamSpec) -> np.ndarray:
+    """Per-source distinct-peer counts: supers first, then background."""
+    lo, hi = spec.super_card
+    key = mix64_int(((spec.seed & 0xFFFFFFFF) << 8) | T_CARD)
+    draws = np.array([mix64_int(i ^ key) for i in range(spec.n_super)], dtype=np.uint64)
+    if spec.super_log_uniform:
+        u = (draws >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+        sup = np.floor(np.exp(math.log(lo) + u * (math.log(hi + 1) - math.log(lo)))).astype(np.int64)
+        sup = np.clip(sup, lo, hi)
+    else:
+        sup = lo + (draws % np.uint64(hi - lo + 1)).astype(np.int64)
+    budget = int(spec.n_packets * spec.dup_p) - int(sup.sum())
+    n_bg = spec.n_sources - spec.n_super
+    if budget < n_bg:
+        raise ValueError(f"{spec.name}: packet budget too small for {n_bg} background sources")
+    return np.concatenate([sup, zipf_rank_size(n_bg, spec.zipf_s, spec.zipf_max, budget)])
+
+
+# -------------------------------------------------------------- generator
+def generate(spec: StreamSpec, backend: str = "numpy", device=None):
+    """(hips, oips, supers): exactly spec.n_packets pairs.
+
+    numpy backend -> uint32 arrays; torch backend -> int32 device tensors
+    holding the uint32 bit patterns.  `supers` = sorted planted IPs (numpy).
+    """
+    xp = _NP() if backend == "numpy" else _Torch(device)
+    seed = spec.seed
+    cards_h = cardinalities(spec)
+    n_src = spec.n_sources
+    n_edges = int(cards_h.sum())
+    if n_edges > spec.n_packets:
+        raise ValueError(f"{spec.name}: {n_edges} distinct pairs exceed {spec.n_packets} packets")
+    src_ip = xp.perm32(xp.arange(n_src), mix64_int(seed ^ (T_SRC << 40)))
+    cards = xp.host(cards_h)
+    host_of = xp.repeat(xp.arange(n_src), cards)
+    starts = xp.cumsum(cards) - cards
+    eidx = xp.arange(n_edges)
+    rank = eidx - starts[host_of]
+    off = xp.draw(T_OFF, seed, host_of) & 0xFFFFFFFF
+    dst = xp.perm32((off + rank) & 0xFFFFFFFF, mix64_int(seed ^ (T_DST << 40)))
+    table = xp.host(geometric_table(spec.dup_p))
+    u53 = xp.shr(xp.draw(T_DUP, seed, eidx), 11)
+    counts = 1 + xp.searchsorted_left(table, -u53)
+    extra_pool = xp.repeat(eidx, counts - 1)
+    need = spec.n_packets - n_edges
+    pool_n = int(extra_pool.shape[0])
+    if pool_n >= need:
+        pri = xp.shr(xp.draw(T_PICK, seed, xp.arange(pool_n)), 1)
+        extra = extra_pool[xp.argsort(pri)[:need]]
+    else:
+        pad = xp.shr(xp.draw(T_PAD, seed, xp.arange(need - pool_n)), 1) % n_edges
+        extra = xp.cat([extra_pool, pad])
+    edges = xp.cat([eidx, extra])
+    order = xp.argsort(xp.shr(xp.draw(T_ORDER, seed, xp.arange(spec.n_packets)), 1))
+    stream = edges[order]
+    hips = src_ip[host_of[stream]]
+    oips = dst[stream]
+    supers = src_ip[: spec.n_super]
+    if backend == "numpy":
+        return hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32))
+    t = xp.t
+    to32 = lambda x: t.where(x >= 2**31, x - 2**32, x).to(t.int32)  # noqa: E731
+    return to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32))
