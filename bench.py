@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Headline benchmark: packets/s of scan + detect (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], "config 2"): one discrete window of
+268,435,456 (src,dst) uint32 pairs -- 16,777,216 sources, 512 planted super
+points with 1,500-50,000 peers, Zipf(1.05) background clipped to 1,000,
+geometric(0.3) duplicates -- seeded synthetic data generated on the GPU
+(tools/workloads.py).  Threshold 1,024; LDCA 8 MiB (LR=8, LC=1024,
+k=8192); SEAV r=12 (2 MiB) because the reference default r=4 overflows
+every register array at this scale.
+
+One step = K1 scan of the whole window + finalize (K5 restore, sort, K6
+filter, compaction, report D2H) + reset.  `value` is timed with the inputs
+resident in HBM; `e2e` is the same step through the public API from pinned
+HOST buffers (DetectorState.process_host_stream: H2D inside the timed
+region, double-buffered) with the report list read back.
+
+N > 1 (torchrun, one process per GPU): weak scaling -- every rank is one
+border router scanning its own config-2-sized window (seed 2 + rank); the
+per-rank sketches are OR-merged on rank 0 (multigpu.py: CUDA-IPC peer
+reads over NVLink, NCCL gather as fallback) and rank 0 detects once.
+
+--impl reference: the reference path on the host CPU (the oracle port,
+oracle/sspd_oracle.c, all host threads) on a bounded sample of the same
+workload, printed on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+import warnings
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "packets/sec (Mpps) scan+detect"
+UNIT = "Mpps"
+WORKLOAD = "config2: 1 window x 268,435,456 pkts, 16.8M sources, 512 supers, LDCA 8 MiB, SEAV r=12"
+
+
+def detector_params():
+    from paper_1901_07306_b200 import DetectorParams
+
+    # LDCA 8 MiB (LR=8, LC=1024, k=8192) as the config states; SEAV r=12
+    return DetectorParams(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=80.5e6)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------- reference arm
+def run_reference(args) -> dict:
+    """The reference path on the host: oracle port, all host threads."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1901_07306_b200._abi import build_params
+    from paper_1901_07306_b200.hashing import SeedFamily
+    from tools.workloads import CONFIG2, generate, scaled
+
+    dp = detector_params()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        p = build_params(dp.seav_config(), dp.ldca_config(), SeedFamily(dp.master_seed))
+    spec = scaled(CONFIG2, args.cpu_scale)
+    hips, oips, _ = generate(spec)
+    threads = oracle.cpu_threads()
+    seav = np.zeros(p.seav_bytes, dtype=np.uint8)
+    ldca = np.zeros(p.ldca_bytes, dtype=np.uint8)
+
+    def step():
+        seav.fill(0)
+        ldca.fill(0)
+        oracle.scan(p, hips, oips, seav, ldca, threads=threads)
+        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+        oracle.filter_z0(p, ldca, ips)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    mpps = len(hips) / dt / 1e6
+    sample = f"{spec.name}: {len(hips)} pkts of the config-2 law (1/{args.cpu_scale} scale), scan+restore+filter"
+    return {
+        "metric": METRIC, "value": round(mpps, 3), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u8 (integer)",
+        "data": "synthetic (seeded, tools/workloads.py)",
+        "config": {"workload": WORKLOAD, "global_batch": len(hips), "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(mpps, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(mpps, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def cpu_baseline_quick(scale: int) -> dict:
+    """Bounded CPU sample for the b200 line's cpu_baseline (rank 0, N=1)."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1901_07306_b200._abi import build_params
+    from paper_1901_07306_b200.hashing import SeedFamily
+    from tools.workloads import CONFIG2, generate, scaled
+
+    dp = detector_params()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        p = build_params(dp.seav_config(), dp.ldca_config(), SeedFamily(dp.master_seed))
+    spec = scaled(CONFIG2, scale)
+    hips, oips, _ = generate(spec)
+    threads = oracle.cpu_threads()
+    best = None
+    for _ in range(2):
+        seav = np.zeros(p.seav_bytes, dtype=np.uint8)
+        ldca = np.zeros(p.ldca_bytes, dtype=np.uint8)
+        t0 = time.perf_counter()
+        oracle.scan(p, hips, oips, seav, ldca, threads=threads)
+        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+        oracle.filter_z0(p, ldca, ips)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": round(len(hips) / best / 1e6, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(hips)} pkts of the config-2 law (1/{scale} scale), scan+restore+filter, best of 2"}
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu(args) -> dict | None:
+    import torch
+
+    from paper_1901_07306_b200 import DetectorState
+    from paper_1901_07306_b200._abi import lib
+    from tools.workloads import CONFIG2, generate
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib()
+
+    from dataclasses import replace
+
+    spec = replace(CONFIG2, seed=CONFIG2.seed + rank)
+    if args.packets:
+        spec = replace(spec, n_packets=args.packets, n_sources=max(1024, args.packets // 16))
+    t_gen = time.perf_counter()
+    hips, oips, supers = generate(spec, "torch", dev)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    n = int(hips.numel())
+    dp = detector_params()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        st = DetectorState.create(dp)
+    merger = None
+    if world > 1:
+        from paper_1901_07306_b200.multigpu import OrMerger
+
+        merger = OrMerger(st, dist)
+
+    stream = torch.cuda.current_stream()
+    scan_ev = []
+
+    def step(reports_out=None, time_scan=False):
+        if time_scan:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        st.process_batch(hips, oips)
+        if time_scan:
+            b.record(stream)
+            scan_ev.append((a, b))
+        if merger is not None:
+            merger.merge_to_root()
+        reps = st.finalize_window() if rank == 0 else []
+        st.reset()
+        if reports_out is not None:
+            reports_out.append(len(reps))
+        return reps
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if dist is not None:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # warm-up (also checks the planted supers come out)
+    first = None
+    for _ in range(args.warmup):
+        r = step()
+        first = first if first is not None else r
+    found = {x.ip for x in first} if first else set()
+    planted_found = len(set(supers.tolist()) & found) if rank == 0 else None
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    counts: list[int] = []
+    ms = timed(lambda: step(counts, time_scan=True), args.steps)
+    clk = clocks.stop()
+    scan_ms = statistics.mean(a.elapsed_time(b) for a, b in scan_ev)
+    scan_share = scan_ms / ms
+
+    # e2e: same step through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_host = hips.cpu().pin_memory()
+        o_host = oips.cpu().pin_memory()
+        h2d = [0]
+        d2h = [0]
+
+        def step_e2e():
+            h2d[0] = st.process_host_stream(h_host, o_host, chunk_pairs=args.chunk)
+            if merger is not None:
+                merger.merge_to_root()
+            reps = st.finalize_window() if rank == 0 else []
+            d2h[0] = 8 * len(reps) + 16  # (ip, z0) pairs + counts read back
+            st.reset()
+
+        for _ in range(max(1, args.warmup // 2)):
+            step_e2e()
+        e2e_ms = timed(step_e2e, args.steps)
+        e2e = {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d[0], "d2h_bytes_per_step": d2h[0], "ms_per_step": round(e2e_ms, 3)}
+
+    if rank != 0:
+        return None
+
+    # roofline: the dominant kernel is K1 (scan).  Algorithmic bytes = 8 B
+    # input per packet; the binding term is the L2 RED rate,
+    # measured live with the scan's own instruction.
+    import ctypes
+
+    peaks = measured_peaks()
+    buf = torch.empty(8 << 20, dtype=torch.uint8, device=dev)
+    red = ctypes.c_double(0.0)
+    lib().sspd_microbench_red(buf.data_ptr(), 8 << 20, 8, 256, ctypes.byref(red), stream.cuda_stream)
+    red_per_s = red.value
+    reds_per_pkt = dp.ldca_config().lr + dp.seav_config().sr / (1 << dp.seav_config().tau)
+    scan_pps = n / (scan_ms * 1e-3)
+    hbm_gbs = peaks.get("hbm_gbs", 6650.0)
+    achieved_gbs = 8 * n / (scan_ms * 1e-3) / 1e9
+    roof_pps = min(hbm_gbs * 1e9 / 8, red_per_s / reds_per_pkt)
+    traffic = None
+    tf = ROOT / "profiles" / "scan_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+
+    value = world * n / (ms * 1e-3) / 1e6
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 keys / u8 bit arrays (integer)",
+        "data": "synthetic (seeded counter-based generator, tools/workloads.py; no CAIDA traces offline)",
+        "config": {"workload": WORKLOAD, "global_batch": world * n, "packets_per_gpu": n,
+                   "parallelism": f"dp{world} (one border router per GPU, OR-merge to rank 0)",
+                   "l2": "inputs (2 GiB/window) exceed the 126 MB L2; no flush needed",
+                   "seav_r": dp.r, "ldca": "LR=8 LC=1024 k=8192 (8 MiB)"},
+        "e2e": e2e,
+        "gpu_launches": args.steps * (5 + (1 if merger else 0)),
+        "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback",
+                     "kernel": "scan_discrete_kernel<true,true> (K1)"},
+        "scan_roofline": {"bound": "l2_red", "l2_red_ops_per_s": round(red_per_s / 1e9, 2),
+                          "reds_per_packet": round(reds_per_pkt, 4), "roofline_gpps": round(roof_pps / 1e9, 3),
+                          "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / roof_pps, 4),
+                          "scan_ms": round(scan_ms, 4), "scan_share_of_step": round(scan_share, 4),
+                          "note": "min(HBM 8 B/pkt, L2 red.or rate / reds per pkt) -- SURVEY.md §8d"},
+        "clocks": clk,
+        "detect": {"reports_per_window": counts[0] if counts else None,
+                   "planted_supers_found": planted_found, "planted": len(supers)},
+        "gen_s": round(t_gen, 2),
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_quick(args.cpu_scale)
+    if dist is not None:
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--packets", type=int, default=0, help="override packets per window (debug)")
+    ap.add_argument("--chunk", type=int, default=1 << 23, help="e2e staging chunk (pairs)")
+    ap.add_argument("--cpu-scale", type=int, default=32, help="CPU sample = config 2 / scale")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        print(json.dumps(run_reference(args)))
+        return
+    line = run_gpu(args)
+    if line is not None:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -215,6 +215,18 @@ SSPD_API int sspd_route_pairs(const uint32_t* hips, const uint32_t* oips, uint64
 SSPD_API int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
                         int iters, double* ops_per_s, void* stream);
 
+/* ---- multi-GPU plumbing (CUDA IPC) -------------------------------------
+ * One cudaMalloc block per rank holds SEAV+LDCA; its 64-byte IPC handle is
+ * exchanged over torch.distributed and opened by the peers, whose merge
+ * kernels (sspd_merge_or) then read it over NVLink.  Replaces the
+ * in-process frame list of simulate_window (distributed.py:231-271). */
+SSPD_API int sspd_ipc_alloc(uint64_t bytes, void** ptr);
+SSPD_API int sspd_ipc_free(void* ptr);
+SSPD_API int sspd_ipc_get_handle(void* ptr, uint8_t* handle_out /* 64 B */);
+SSPD_API int sspd_ipc_open(const uint8_t* handle /* 64 B */, void** ptr);
+SSPD_API int sspd_ipc_close(void* ptr);
+SSPD_API int sspd_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

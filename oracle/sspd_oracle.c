@@ -93,23 +93,57 @@ void or_ldca_update(const sspd_params* p, const uint32_t* hips, const uint32_t* 
   for (uint64_t j = 0; j < n; ++j) or_ldca_pair(p, hips[j], oips[j], ldca);
 }
 
-/* DetectorState.process_batch (window_detector.py:100-103) over nthreads
- * private copies, OR-combined at the end (the WP shard + merge of
- * distributed.py:231-271, which is exact by OR monotonicity). */
+/* DetectorState.process_batch (window_detector.py:100-103) on nthreads.
+ * Work is split by SKETCH ROW (LDCA row i, or the whole SEAV) so each
+ * thread's working set is one 1 MiB row that stays in its private cache;
+ * when there are more threads than row tasks the packet range is split too
+ * and those threads OR with relaxed atomics (exact: OR is monotone). */
 typedef struct {
   const sspd_params* p;
   const uint32_t* hips;
   const uint32_t* oips;
   uint64_t lo, hi;
+  int row;      /* LDCA row, or -1 for the SEAV task */
+  int atomic;
   uint8_t* seav;
   uint8_t* ldca;
 } or_job;
 
 static void* or_scan_job(void* arg) {
   or_job* j = (or_job*)arg;
+  const sspd_params* p = j->p;
+  if (j->row < 0) {
+    if (!j->atomic) {
+      for (uint64_t t = j->lo; t < j->hi; ++t) or_seav_pair(p, j->hips[t], j->oips[t], j->seav);
+      return NULL;
+    }
+    for (uint64_t t = j->lo; t < j->hi; ++t) {
+      uint64_t oip = j->oips[t], hip = j->hips[t];
+      uint32_t h1 = (uint32_t)(or_mix64(oip ^ p->seed_h1) & 0xFFFFFFFFull);
+      if (or_lsb32(h1) < (int)p->tau) continue;
+      uint64_t bit = or_hash_range(oip, p->seed_h2, p->g);
+      uint64_t rp = hip & ((1ull << p->r) - 1ull);
+      uint64_t lp = (hip >> p->r) & ((1ull << p->lp_bits) - 1ull);
+      for (uint32_t i = 0; i < p->sr; ++i) {
+        uint64_t col = or_index_of(p, i, lp);
+        uint64_t byte = p->seav_row_off[i] + (rp * p->sc[i] + col) * p->reg_bytes + (bit >> 3);
+        __atomic_fetch_or(&j->seav[byte], (uint8_t)(1u << (bit & 7)), __ATOMIC_RELAXED);
+      }
+    }
+    return NULL;
+  }
+  const uint64_t kb = p->k / 8;
+  uint8_t* row = j->ldca + (uint64_t)j->row * p->lc * kb;
+  const uint64_t seed = p->seed_lh[j->row];
   for (uint64_t t = j->lo; t < j->hi; ++t) {
-    if (j->seav) or_seav_pair(j->p, j->hips[t], j->oips[t], j->seav);
-    if (j->ldca) or_ldca_pair(j->p, j->hips[t], j->oips[t], j->ldca);
+    uint64_t b = or_hash_range(j->oips[t], p->seed_h3, p->k);
+    uint64_t c = or_hash_range(j->hips[t], seed, p->lc);
+    uint8_t* cell = row + c * kb + (b >> 3);
+    uint8_t m = (uint8_t)(1u << (b & 7));
+    if (j->atomic)
+      __atomic_fetch_or(cell, m, __ATOMIC_RELAXED);
+    else
+      *cell |= m;
   }
   return NULL;
 }
@@ -117,30 +151,37 @@ static void* or_scan_job(void* arg) {
 int or_scan(const sspd_params* p, const uint32_t* hips, const uint32_t* oips, uint64_t n, uint8_t* seav,
             uint8_t* ldca, int nthreads) {
   if (nthreads <= 1 || n < 4096) {
-    or_job j = {p, hips, oips, 0, n, seav, ldca};
-    or_scan_job(&j);
+    for (uint64_t t = 0; t < n; ++t) {
+      if (seav) or_seav_pair(p, hips[t], oips[t], seav);
+      if (ldca) or_ldca_pair(p, hips[t], oips[t], ldca);
+    }
     return 0;
   }
-  pthread_t* th = (pthread_t*)calloc(nthreads, sizeof(pthread_t));
-  or_job* jobs = (or_job*)calloc(nthreads, sizeof(or_job));
-  for (int t = 0; t < nthreads; ++t) {
-    jobs[t].p = p;
-    jobs[t].hips = hips;
-    jobs[t].oips = oips;
-    jobs[t].lo = n * t / nthreads;
-    jobs[t].hi = n * (t + 1) / nthreads;
-    jobs[t].seav = seav ? (uint8_t*)calloc(p->seav_bytes, 1) : NULL;
-    jobs[t].ldca = ldca ? (uint8_t*)calloc(p->ldca_bytes, 1) : NULL;
-    pthread_create(&th[t], NULL, or_scan_job, &jobs[t]);
+  int tasks = (ldca ? (int)p->lr : 0) + (seav ? 1 : 0);
+  int parts = nthreads / tasks;
+  if (parts < 1) parts = 1;
+  int total = tasks * parts;
+  pthread_t* th = (pthread_t*)calloc(total, sizeof(pthread_t));
+  or_job* jobs = (or_job*)calloc(total, sizeof(or_job));
+  int q = 0;
+  for (int t = 0; t < tasks; ++t) {
+    for (int part = 0; part < parts; ++part, ++q) {
+      jobs[q].p = p;
+      jobs[q].hips = hips;
+      jobs[q].oips = oips;
+      jobs[q].lo = n * part / parts;
+      jobs[q].hi = n * (part + 1) / parts;
+      jobs[q].row = (ldca && t < (int)p->lr) ? t : -1;
+      jobs[q].atomic = parts > 1;
+      jobs[q].seav = seav;
+      jobs[q].ldca = ldca;
+    }
   }
-  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
-  for (int t = 0; t < nthreads; ++t) {
-    if (seav)
-      for (uint64_t b = 0; b < p->seav_bytes; ++b) seav[b] |= jobs[t].seav[b];
-    if (ldca)
-      for (uint64_t b = 0; b < p->ldca_bytes; ++b) ldca[b] |= jobs[t].ldca[b];
-    free(jobs[t].seav);
-    free(jobs[t].ldca);
+  /* more threads than tasks x parts would idle; fewer run in waves */
+  for (int base = 0; base < total; base += nthreads) {
+    int end = base + nthreads < total ? base + nthreads : total;
+    for (int t = base; t < end; ++t) pthread_create(&th[t], NULL, or_scan_job, &jobs[t]);
+    for (int t = base; t < end; ++t) pthread_join(th[t], NULL);
   }
   free(th);
   free(jobs);

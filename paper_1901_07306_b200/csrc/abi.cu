@@ -1,4 +1,5 @@
 // Library identity, host-side helpers and the roofline microbenchmark.
+#include <cstring>
 #include <cuda_runtime.h>
 #include "sspd_common.cuh"
 #include "launch.cuh"
@@ -75,4 +76,46 @@ extern "C" int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
   cudaEventDestroy(b);
   *ops_per_s = (double)grid * 256.0 * iters / (best * 1e-3);
   return check_launch();
+}
+
+// ---- CUDA IPC plumbing for the multi-GPU OR-merge (multigpu.py) --------
+// A rank's sketch block is one cudaMalloc allocation so that its IPC
+// handle maps exactly that block into every peer process.
+extern "C" int sspd_ipc_alloc(uint64_t bytes, void** ptr) {
+  if (!ptr || bytes == 0) return SSPD_ERR_DATA;
+  if (cudaMalloc(ptr, bytes) != cudaSuccess) return SSPD_ERR_CUDA;
+  if (cudaMemset(*ptr, 0, bytes) != cudaSuccess) return SSPD_ERR_CUDA;
+  return SSPD_OK;
+}
+
+extern "C" int sspd_ipc_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? SSPD_OK : SSPD_ERR_CUDA; }
+
+extern "C" int sspd_ipc_get_handle(void* ptr, uint8_t* handle_out) {
+  if (!ptr || !handle_out) return SSPD_ERR_DATA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, ptr) != cudaSuccess) return SSPD_ERR_CUDA;
+  memcpy(handle_out, &h, sizeof(h));
+  return SSPD_OK;
+}
+
+extern "C" int sspd_ipc_open(const uint8_t* handle, void** ptr) {
+  if (!handle || !ptr) return SSPD_ERR_DATA;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return SSPD_ERR_CUDA;
+  }
+  return SSPD_OK;
+}
+
+extern "C" int sspd_ipc_close(void* ptr) {
+  return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? SSPD_OK : SSPD_ERR_CUDA;
+}
+
+extern "C" int sspd_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return SSPD_OK;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SSPD_OK
+             : SSPD_ERR_CUDA;
 }

@@ -255,6 +255,14 @@ class SeavSketch:
         """The flat payload on the device (torch uint8, 16-byte padded)."""
         return self._buf
 
+    def _rebind(self, view):
+        """Move the payload into `view` (a 16-byte aligned device uint8 view,
+        e.g. a slice of a CUDA-IPC block shared with peer ranks)."""
+        if view.numel() < self.nbytes:
+            raise ValueError("view too small for the sketch payload")
+        view[: self.nbytes].copy_(self._buf[: self.nbytes])
+        self._buf = view
+
     @property
     def rows(self) -> list[np.ndarray]:
         """Host snapshot of the registers, one (2^r, SC_i) array per row."""

@@ -20,7 +20,7 @@ import numpy as np
 from .errors import ConfigError
 from .long_sketch import ldc_estimate
 from .short_sketch import SeavSketch
-from .window_detector import DetectionReport, DetectorParams, filter_candidates
+from .window_detector import DetectionReport, DetectorParams, ReportList, filter_candidates
 
 _UNSIGNED = ((1, np.uint8), (2, np.uint16), (4, np.uint32), (8, np.uint64))
 
@@ -268,12 +268,7 @@ class SlidingDetector:
         ips, z0s = filter_candidates(
             seav, None, self._params, k, cutoff,
             sliding=(pool.device_buffer(), pool.ts_bytes, pool._wrapped_now(), pool.window_slices))
-        out = []
-        for ip, z0 in zip(ips, z0s):
-            est, saturated = ldc_estimate(z0, k)
-            out.append(DetectionReport(ip=ip, estimated_cardinality=est, saturated=saturated,
-                                       window_id=self.now, source="sliding"))
-        return out
+        return ReportList(ips, z0s, k, self.now, "sliding")
 
 
 def detect_sliding(detector: SlidingDetector, theta: int | None = None, beta: float | None = None):

@@ -15,6 +15,7 @@ Mirrors `sspd/window_detector.py` (DetectorParams :39-69, DetectorState
 from __future__ import annotations
 
 import warnings
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -42,6 +43,85 @@ class DetectionReport:
     saturated: bool
     window_id: int
     source: str = "discrete"
+
+
+_EST_CACHE: dict = {}
+
+
+def estimate_table(k: int) -> list:
+    """est[z0] for z0 in [0, k] with the reference formula (long_sketch.py:33-44),
+    computed once per k with math.log so every float is bit-identical."""
+    t = _EST_CACHE.get(k)
+    if t is None:
+        t = [ldc_estimate(z0, k)[0] for z0 in range(k + 1)]
+        _EST_CACHE[k] = t
+    return t
+
+
+class ReportList(Sequence):
+    """The kept (ip, z0) pairs of one finalize, as a read-only sequence of
+    DetectionReport built on access.
+
+    Behaves like the reference's list[DetectionReport] (len, iteration,
+    indexing, ==, `list += reports`); objects are only created when touched,
+    so a window with tens of thousands of saturated candidates does not pay
+    Python object construction unless the caller asks for them."""
+
+    __slots__ = ("ips", "z0s", "k", "window_id", "source", "_est")
+
+    def __init__(self, ips: np.ndarray, z0s: np.ndarray, k: int, window_id: int, source: str):
+        self.ips = ips
+        self.z0s = z0s
+        self.k = k
+        self.window_id = window_id
+        self.source = source
+        self._est = estimate_table(k)
+
+    def __len__(self) -> int:
+        return len(self.ips)
+
+    def _make(self, i: int) -> DetectionReport:
+        z0 = int(self.z0s[i])
+        return DetectionReport(ip=int(self.ips[i]), estimated_cardinality=self._est[z0], saturated=z0 == 0,
+                               window_id=self.window_id, source=self.source)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._make(j) for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("report index out of range")
+        return self._make(i)
+
+    def __iter__(self):
+        est, wid, src = self._est, self.window_id, self.source
+        for ip, z0 in zip(self.ips.tolist(), self.z0s.tolist()):
+            yield DetectionReport(ip=ip, estimated_cardinality=est[z0], saturated=z0 == 0, window_id=wid,
+                                  source=src)
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, ReportList):
+            return (self.k == other.k and self.window_id == other.window_id and self.source == other.source
+                    and np.array_equal(self.ips, other.ips) and np.array_equal(self.z0s, other.z0s))
+        try:
+            return list(self) == list(other)
+        except TypeError:
+            return NotImplemented
+
+    def __ne__(self, other) -> bool:
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    def __add__(self, other):
+        return list(self) + list(other)
+
+    def __radd__(self, other):
+        return list(other) + list(self)
+
+    def __repr__(self) -> str:
+        return f"ReportList({len(self)} reports, window_id={self.window_id}, source={self.source!r})"
 
 
 @dataclass
@@ -116,7 +196,7 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
             raise err
         warnings.warn(str(err), RuntimeWarning, stacklevel=3)
     if n == 0:
-        return [], []
+        return np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32)
     dev = ip.device
     table = device_keep_table(k, cutoff)
     z0 = torch.empty(n, dtype=torch.int32, device=dev)
@@ -134,9 +214,8 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
     call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
          z0_out.data_ptr(), cnt.data_ptr(), None, None, stream_ptr())
     m = int(cnt.item())
-    ips = ip_out[:m].cpu().numpy().view(np.uint32).tolist()
-    z0s = z0_out[:m].cpu().numpy().view(np.uint32).tolist()
-    return ips, z0s
+    both = torch.stack((ip_out[:m], z0_out[:m])).cpu().numpy().view(np.uint32)
+    return both[0], both[1]
 
 
 @dataclass
@@ -180,23 +259,84 @@ class DetectorState:
              self.seav.device_buffer().data_ptr(), self.ldca.device_buffer().data_ptr(), stream_ptr())
         self.pair_count += int(h.numel())
 
-    def finalize_window(self, beta: float | None = None, source: str = "discrete") -> list[DetectionReport]:
+    def process_host_stream(self, hips, oips, chunk_pairs: int = 1 << 23):
+        """Stream HOST arrays through two device staging buffers: the H2D copy
+        of chunk i+1 (copy stream) overlaps the K1 scan of chunk i (compute
+        stream) -- the paper's watch-point buffer (PAPER.md:199;
+        distributed.py:222-228 is the CPU analogue).  Pinned torch CPU
+        tensors give truly asynchronous copies; numpy arrays are accepted
+        (pageable copies).  Returns the number of H2D bytes moved."""
+        import torch
+
+        from ._device import call, device, stream_ptr
+        from .errors import ConfigError, DataError
+
+        dev = device()
+        h = _host_u32_tensor(hips, "hips")
+        o = _host_u32_tensor(oips, "oips")
+        n = int(h.numel())
+        if n != int(o.numel()):
+            raise ConfigError("hips and oips differ in length")
+        if h.device.type != "cpu" or o.device.type != "cpu":
+            raise DataError("process_host_stream takes host arrays; use process_batch for device tensors")
+        chunk = max(1024, min(chunk_pairs, n))
+        stage = getattr(self, "_stage", None)
+        if stage is None or stage[0][0].numel() < chunk:
+            stage = [(torch.empty(chunk, dtype=torch.int32, device=dev),
+                      torch.empty(chunk, dtype=torch.int32, device=dev)) for _ in range(2)]
+            self._stage = stage
+            self._copy_stream = torch.cuda.Stream(device=dev)
+            self._free = [torch.cuda.Event(), torch.cuda.Event()]
+            self._ready = [torch.cuda.Event(), torch.cuda.Event()]
+        compute = torch.cuda.current_stream(dev)
+        cs = self._copy_stream
+        for i, lo in enumerate(range(0, n, chunk)):
+            b = i & 1
+            m = min(chunk, n - lo)
+            with torch.cuda.stream(cs):
+                cs.wait_event(self._free[b])
+                stage[b][0][:m].copy_(h[lo:lo + m], non_blocking=True)
+                stage[b][1][:m].copy_(o[lo:lo + m], non_blocking=True)
+                self._ready[b].record(cs)
+            compute.wait_event(self._ready[b])
+            call("sspd_scan_discrete", stage[b][0].data_ptr(), stage[b][1].data_ptr(), m, self.seav._params,
+                 self.seav.device_buffer().data_ptr(), self.ldca.device_buffer().data_ptr(), stream_ptr())
+            self._free[b].record(compute)
+        self.pair_count += n
+        return 8 * n
+
+    def finalize_window(self, beta: float | None = None, source: str = "discrete") -> "ReportList":
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.theta
         k = self.ldca.config.k
         ips, z0s = filter_candidates(self.seav, self.ldca.device_buffer(), self.seav._params, k, cutoff)
-        reports = []
-        for ip, z0 in zip(ips, z0s):
-            est, saturated = ldc_estimate(z0, k)
-            reports.append(DetectionReport(ip=ip, estimated_cardinality=est, saturated=saturated,
-                                           window_id=self.window_id, source=source))
-        return reports
+        return ReportList(ips, z0s, k, self.window_id, source)
 
     def reset(self):
         self.seav.clear()
         self.ldca.clear()
         self.window_id += 1
         self.pair_count = 0
+
+
+def _host_u32_tensor(a, name: str):
+    """Host IPv4 array as an int32 torch CPU tensor (uint32 bit pattern)."""
+    import torch
+
+    from .errors import DataError
+
+    if isinstance(a, torch.Tensor):
+        if a.dtype in (torch.int32, torch.uint32):
+            return a.contiguous()
+        a = a.cpu().numpy()
+    arr = np.asarray(a)
+    if arr.dtype.kind not in "ui":
+        raise DataError(f"{name}: integer array expected, got {arr.dtype}")
+    if arr.dtype != np.uint32:
+        if arr.size and (int(arr.min()) < 0 or int(arr.max()) > 0xFFFFFFFF):
+            raise DataError(f"{name}: IPv4 keys must lie in [0, 2^32)")
+        arr = arr.astype(np.uint32)
+    return torch.from_numpy(np.ascontiguousarray(arr).view(np.int32))
 
 
 def process_pair(state: DetectorState, hip: int, oip: int) -> DetectorState:
