@@ -100,6 +100,8 @@ _SIGS = {
     "sspd_hash_range_host": (_U64, [_U64, _U64, C.POINTER(Divisor_t)]),
     "sspd_mix64_host": (_U64, [_U64]),
     "sspd_scan_discrete": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP]),
+    "sspd_scan_partitioned": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "sspd_scan_partitioned_scratch": (_U64, [_PP, _U64]),
     "sspd_scan_sliding": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _VP]),
     "sspd_sweep": (C.c_int, [_VP, _U64, _U32, _U64, _U64, _U64, _VP]),
     "sspd_materialize_seav": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP]),

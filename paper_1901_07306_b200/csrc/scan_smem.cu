@@ -1,0 +1,346 @@
+// K1p: the partitioned scan -- the LDCA lives in the SMs' shared memory.
+//
+// Why: every packet sets LR (=8) bits at uniformly random words of the
+// 8 MiB LDCA.  Done as L2 atomics that is 8 random `red.or` per packet and
+// the scan is capped by the L2 atomic rate (~190-215 G/s measured, ~23.7
+// Gpps); random L2 loads cap at ~287 G/s as well.  Shared-memory atomics
+// run at ~2,000 G/s per chip, and 148 SMs x 227 KB = 33 MB of shared memory
+// holds the whole 8 MiB LDCA.  So:
+//
+//   * the LDCA word space is cut into P contiguous partitions, one per CTA
+//     (one persistent 1024-thread CTA per SM, cooperative launch); each CTA
+//     keeps its partition in shared memory for the whole launch;
+//   * the stream is processed in chunks.  Producer phase: every CTA hashes
+//     its slice of chunk t tile by tile, appends each LDCA update
+//     (local word << 5 | bit, one u32) to a per-destination shared-memory
+//     staging area, and flushes the staging areas as coalesced runs into
+//     its OWN region of each destination's bucket -- region (src, dst) is
+//     private to one producer CTA, so no global atomics are needed; the
+//     run lengths are published once per chunk;
+//   * consumer phase: CTA q ORs every region (src, q) of chunk t-1 into its
+//     partition with shared-memory atomics.  Buckets are double-buffered,
+//     so ONE grid barrier per chunk separates "chunk t produced" from
+//     "chunk t consumed";
+//   * at the end each CTA ORs its partition into the global LDCA.
+//
+// Per packet the L2 sees 32 B of coalesced bucket writes + 32 B of reads
+// instead of 8 random atomics.  Anything that does not fit (a staging area
+// or a region overflowing under a skewed stream) falls back to a direct L2
+// `red.or` on the global LDCA -- exact, because OR is commutative and
+// idempotent.  SEAV updates (0.78 % of packets at tau=7) stay direct reds.
+//
+// Reference semantics are unchanged from K1 (scan.cu): bit (i*lc + c_i)*k + b
+// of the LDCA, c_i = LH_i(hip) % lc, b = H3(oip) % k (long_sketch.py:125-135),
+// and the SEAV update of short_sketch.py:300-318.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include "sspd_common.cuh"
+#include "launch.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sspd {
+
+__device__ __forceinline__ void red_or_g(uint32_t* addr, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+// floor(x / d) with the same round-up multiplier as sspd::mod
+__device__ __forceinline__ uint64_t div_fast(uint64_t x, const sspd_divisor& dv) {
+  if (dv.pow2) return x >> (63 - __clzll(dv.d));
+  const uint64_t t = __umul64hi(dv.magic, x);
+  return (t + ((x - t) >> dv.sh1)) >> dv.sh2;
+}
+
+constexpr uint32_t kThreads = 1024;
+constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile
+constexpr uint32_t kTile = kThreads * kPktPerThread;
+
+struct PartPlan {
+  uint32_t nparts;        // = gridDim.x (producers == consumers)
+  uint32_t part_words;    // words per partition (last one may be shorter)
+  uint64_t total_words;   // LDCA words (ceil(bits / 32))
+  sspd_divisor div_part;  // divisor by part_words
+  uint32_t stage_slots;   // staging slots per destination per tile
+  uint32_t region_cap;    // entries per (src, dst) region per chunk
+  uint64_t chunk;         // packets per chunk
+  uint64_t n;             // packets
+  uint32_t* buckets;      // [2][dst][src][region_cap]
+  uint32_t* counts;       // [2][dst][src]
+  // 32-bit fast path (k, lc powers of two, < 2^32 LDCA bits)
+  uint32_t k_mask, lc_mask, log2k;
+  uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w
+};
+
+// Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor]
+template <bool kSeav, bool kFast>
+__global__ void __launch_bounds__(kThreads, 1)
+    scan_partitioned_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
+                            const __grid_constant__ sspd_params p, const __grid_constant__ PartPlan P,
+                            uint32_t* seav, uint32_t* ldca) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* part = smem;
+  uint32_t* stage = smem + P.part_words;
+  uint32_t* cnt = stage + (size_t)P.nparts * P.stage_slots;
+  uint32_t* cursor = cnt + P.nparts;
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t self = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = kThreads >> 5;
+  const uint32_t tmask = tau_mask(p.tau);
+  const uint32_t np = P.nparts;
+
+  for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
+  for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = cursor[i] = 0;
+  __syncthreads();
+
+  const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
+  const uint64_t k = p.k;
+  for (uint64_t t = 0; t <= nchunks; ++t) {
+    // ---------------- consume chunk t-1 into the shared partition --------
+    if (t >= 1) {
+      const uint32_t b = (uint32_t)((t - 1) & 1);
+      const uint32_t* cnts = P.counts + ((size_t)b * np + self) * np;
+      const uint32_t* regions = P.buckets + ((size_t)b * np + self) * (size_t)np * P.region_cap;
+      for (uint32_t src = warp; src < np; src += nwarps) {
+        const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
+        const uint32_t* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
+        const uint32_t m4 = m >> 2;
+#pragma unroll 2
+        for (uint32_t j = lane; j < m4; j += 32) {
+          const uint4 u = __ldcg(reinterpret_cast<const uint4*>(reg) + j);
+          atomicOr(&part[u.x >> 5], 1u << (u.x & 31));
+          atomicOr(&part[u.y >> 5], 1u << (u.y & 31));
+          atomicOr(&part[u.z >> 5], 1u << (u.z & 31));
+          atomicOr(&part[u.w >> 5], 1u << (u.w & 31));
+        }
+        for (uint32_t j = (m4 << 2) + lane; j < m; j += 32) {
+          const uint32_t u = __ldcg(reg + j);
+          atomicOr(&part[u >> 5], 1u << (u & 31));
+        }
+      }
+    }
+    // ---------------- produce chunk t ------------------------------------
+    if (t < nchunks) {
+      const uint32_t b = (uint32_t)(t & 1);
+      const uint64_t c0 = t * P.chunk;
+      const uint64_t c1 = min(P.n, c0 + P.chunk);
+      const uint64_t per = (c1 - c0 + gridDim.x - 1) / gridDim.x;
+      const uint64_t lo = min(c1, c0 + per * self);
+      const uint64_t hi = min(c1, lo + per);
+      for (uint64_t base = lo; base < hi; base += kTile) {
+#pragma unroll
+        for (uint32_t e = 0; e < kPktPerThread; ++e) {
+          const uint64_t j = base + e * kThreads + tid;
+          if (j < hi) {
+            const uint32_t hip = __ldcs(hips + j), oip = __ldcs(oips + j);
+            if (kFast) {
+              // k, lc powers of two and < 2^32 LDCA bits: the modulo is a mask
+              // of the low hash word and all index math is 32-bit.
+              const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
+              uint32_t cellbase = 0;
+              uint64_t ovf = 0;  // rows whose staging slot overflowed (rare)
+#pragma unroll 8
+              for (uint32_t i = 0; i < p.lr; ++i) {
+                const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
+                const uint32_t bit = ((cellbase + c) << P.log2k) | bb;
+                const uint32_t w = bit >> 5;
+                const uint32_t th = __umulhi(w, P.magic32);
+                const uint32_t q = (th + ((w - th) >> 1)) >> P.sh32;
+                const uint32_t local = w - q * P.part_words;
+                const uint32_t slot = atomicAdd(&cnt[q], 1u);
+                const bool fits = slot < P.stage_slots;
+                if (fits) stage[q * P.stage_slots + slot] = (local << 5) | (bit & 31u);
+                ovf |= (uint64_t)(!fits) << i;
+                cellbase += p.lc;
+              }
+              while (ovf) {  // staging full: apply those rows directly (exact)
+                const uint32_t i = __ffsll((long long)ovf) - 1;
+                ovf &= ovf - 1;
+                const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
+                const uint32_t bit = ((i * p.lc + c) << P.log2k) | bb;
+                red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
+              }
+            } else {
+              const uint64_t bb = hash_range(oip, p.seed_h3, p.div_k);
+              uint64_t cell = 0;
+#pragma unroll 4
+              for (uint32_t i = 0; i < p.lr; ++i) {
+                const uint64_t c = hash_range(hip, p.seed_lh[i], p.div_lc);
+                const uint64_t bit = (cell + c) * k + bb;
+                const uint64_t w = bit >> 5;
+                const uint32_t q = (uint32_t)div_fast(w, P.div_part);
+                const uint32_t local = (uint32_t)(w - (uint64_t)q * P.part_words);
+                const uint32_t slot = atomicAdd(&cnt[q], 1u);
+                if (slot < P.stage_slots)
+                  stage[q * P.stage_slots + slot] = (local << 5) | (uint32_t)(bit & 31);
+                else
+                  red_or_g(ldca + w, 1u << (bit & 31));  // staging full: direct (exact)
+                cell += p.lc;
+              }
+            }
+            if (kSeav && sampled(oip, p.seed_h1, tmask)) {
+              const uint32_t sbit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+              const uint64_t rp = hip & ((1u << p.r) - 1u);
+              const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+              for (uint32_t i = 0; i < p.sr; ++i) {
+                const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+                const uint64_t abs_bit = (p.seav_row_off[i] + (rp * p.sc[i] + col) * p.reg_bytes) * 8 + sbit;
+                red_or_g(seav + (abs_bit >> 5), 1u << (abs_bit & 31));
+              }
+            }
+          }
+        }
+        __syncthreads();
+        // flush: one warp per destination; each run goes to this CTA's own
+        // region of the destination bucket (no global atomics)
+        for (uint32_t q = warp; q < np; q += nwarps) {
+          const uint32_t m = min(cnt[q], P.stage_slots);
+          if (m == 0) continue;
+          const uint32_t pos = cursor[q];
+          const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
+          const uint32_t* src = stage + q * P.stage_slots;
+          uint32_t* dst = P.buckets + (((size_t)b * np + q) * np + self) * P.region_cap + pos;
+          for (uint32_t s = lane; s < fit; s += 32) __stcg(dst + s, src[s]);
+          for (uint32_t s = fit + lane; s < m; s += 32) {  // region full: direct (exact)
+            const uint32_t u = src[s];
+            red_or_g(ldca + (uint64_t)q * P.part_words + (u >> 5), 1u << (u & 31));
+          }
+          __syncwarp();
+          if (lane == 0) {
+            cursor[q] = pos + fit;
+            cnt[q] = 0;
+          }
+        }
+        __syncthreads();
+      }
+      // publish this CTA's run lengths for chunk t and reset the cursors
+      for (uint32_t q = tid; q < np; q += kThreads) {
+        __stcg(P.counts + ((size_t)b * np + q) * np + self, cursor[q]);
+        cursor[q] = 0;
+      }
+    }
+    grid.sync();  // chunk t produced everywhere; chunk t-1 consumed everywhere
+  }
+  // fold the shared partition into the global LDCA (after the last barrier
+  // no direct reds are in flight, so plain read-modify-write is exact)
+  __syncthreads();
+  const uint64_t w0 = (uint64_t)self * P.part_words;
+  for (uint32_t i = tid; i < P.part_words; i += kThreads) {
+    const uint64_t w = w0 + i;
+    if (w < P.total_words && part[i]) ldca[w] |= part[i];
+  }
+}
+
+static bool bits_fit32(const sspd_params* p) { return (uint64_t)p->lr * p->lc * p->k <= 0xFFFFFFFFull; }
+
+static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int max_smem,
+                             PartPlan& P, uint64_t& smem, uint64_t& scratch) {
+  const uint64_t bits = (uint64_t)p->lr * p->lc * p->k;
+  P.nparts = (uint32_t)sms;
+  P.total_words = (bits + 31) / 32;
+  P.part_words = (uint32_t)(((P.total_words + P.nparts - 1) / P.nparts + 3) & ~3ull);
+  // staging: expected kTile*lr/nparts per destination per tile, + 6 sigma
+  const double mean = (double)kTile * p->lr / P.nparts;
+  P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
+  smem = 4ull * (P.part_words + (uint64_t)P.nparts * P.stage_slots + 2ull * P.nparts);
+  if ((int64_t)smem > max_smem || P.part_words >= (1u << 27)) return false;
+  const uint64_t d = P.part_words;
+  P.div_part.d = d;
+  P.div_part.pad_ = 0;
+  if ((d & (d - 1)) == 0) {
+    P.div_part.pow2 = 1;
+    P.div_part.magic = 0;
+    P.div_part.sh1 = P.div_part.sh2 = 0;
+  } else {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    const unsigned __int128 num = ((unsigned __int128)1 << 64) * (((unsigned __int128)1 << l) - d);
+    P.div_part.magic = (uint64_t)(num / d) + 1;
+    P.div_part.sh1 = 1;
+    P.div_part.sh2 = l - 1;
+    P.div_part.pow2 = 0;
+  }
+  P.chunk = chunk ? chunk : (1ull << 21);
+  const double rmean = (double)P.chunk * p->lr / ((double)P.nparts * P.nparts);
+  P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
+  P.region_cap = (P.region_cap + 31u) & ~31u;
+  P.n = n;
+  scratch = 4ull * (2ull * P.nparts * P.nparts * P.region_cap + 2ull * P.nparts * P.nparts);
+  // 32-bit division by part_words (Granlund-Montgomery, N = 32)
+  {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    P.magic32 = (d & (d - 1)) == 0 ? 0u : (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+    P.sh32 = l - 1;
+  }
+  P.k_mask = p->k - 1;
+  P.lc_mask = p->lc - 1;
+  P.log2k = 0;
+  while ((1u << P.log2k) < p->k) ++P.log2k;
+  return true;
+}
+
+}  // namespace sspd
+
+using namespace sspd;
+
+// Returns SSPD_ERR_CONFIG when the geometry/device cannot host the
+// partitioned scan (the caller then uses the direct kernel).
+extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                                     uint8_t* seav, uint8_t* ldca, void* scratch, uint64_t scratch_bytes,
+                                     uint64_t chunk, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0) return SSPD_OK;
+  if (!hips || !oips || !ldca) return SSPD_ERR_DATA;
+  int dev = 0, sms = 0, max_smem = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return SSPD_ERR_CONFIG;
+  PartPlan P;
+  uint64_t smem = 0, need = 0;
+  if (!plan_partitioned(p, n, chunk, sms, max_smem, P, smem, need)) return SSPD_ERR_CONFIG;
+  if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  P.buckets = static_cast<uint32_t*>(scratch);
+  P.counts = P.buckets + 2ull * P.nparts * P.nparts * P.region_cap;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool fast = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0 && bits_fit32(p);
+  void* kern = seav ? (fast ? (void*)scan_partitioned_kernel<true, true> : (void*)scan_partitioned_kernel<true, false>)
+                    : (fast ? (void*)scan_partitioned_kernel<false, true> : (void*)scan_partitioned_kernel<false, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) return SSPD_ERR_CONFIG;
+  const uint32_t* h = hips;
+  const uint32_t* o = oips;
+  sspd_params pv = *p;
+  uint32_t* sv = reinterpret_cast<uint32_t*>(seav);
+  uint32_t* lv = reinterpret_cast<uint32_t*>(ldca);
+  void* args[] = {(void*)&h, (void*)&o, (void*)&pv, (void*)&P, (void*)&sv, (void*)&lv};
+  if (cudaLaunchCooperativeKernel(kern, dim3(P.nparts), dim3(kThreads), args, smem, st) != cudaSuccess) {
+    cudaGetLastError();
+    return SSPD_ERR_CUDA;
+  }
+  return check_launch();
+}
+
+// Scratch bytes the partitioned scan needs for a given chunk size (0 when
+// the LDCA cannot be partitioned into shared memory on this device).
+extern "C" uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t chunk) {
+  if (!p) return 0;
+  int dev = 0, sms = 148, max_smem = 232448;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+    max_smem = 232448;
+  }
+  PartPlan P;
+  uint64_t smem = 0, need = 0;
+  if (!plan_partitioned(p, 1, chunk, sms, max_smem, P, smem, need)) return 0;
+  return need;
+}

@@ -255,9 +255,36 @@ class DetectorState:
         o = ips_to_device(oips, "oips")
         if h.numel() != o.numel():
             raise ConfigError("hips and oips differ in length")
-        call("sspd_scan_discrete", h.data_ptr(), o.data_ptr(), h.numel(), self.seav._params,
-             self.seav.device_buffer().data_ptr(), self.ldca.device_buffer().data_ptr(), stream_ptr())
+        self._scan(h.data_ptr(), o.data_ptr(), int(h.numel()))
         self.pair_count += int(h.numel())
+
+    # "auto": the shared-memory partitioned scan (K1p) for large batches when
+    # the LDCA fits in the SMs' shared memory, else the direct L2 scan (K1).
+    scan_mode = "auto"  # or "direct" / "partitioned" (class attributes, not dataclass fields)
+    partitioned_min_packets = 1 << 22
+    partitioned_chunk = 1 << 21
+
+    def _scan(self, h_ptr: int, o_ptr: int, n: int):
+        from ._abi import ERR_CONFIG, check, lib
+        from ._device import call, stream_ptr
+
+        mode = self.scan_mode
+        seav_p = self.seav.device_buffer().data_ptr()
+        ldca_p = self.ldca.device_buffer().data_ptr()
+        if mode == "partitioned" or (mode == "auto" and n >= self.partitioned_min_packets):
+            scratch = getattr(self, "_part_scratch", None)
+            need = int(lib().sspd_scan_partitioned_scratch(self.seav._params, self.partitioned_chunk))
+            if scratch is None or scratch.numel() < need:
+                import torch
+
+                scratch = torch.empty(need, dtype=torch.uint8, device=self.ldca.device_buffer().device)
+                self._part_scratch = scratch
+            rc = lib().sspd_scan_partitioned(h_ptr, o_ptr, n, self.seav._params, seav_p, ldca_p,
+                                             scratch.data_ptr(), need, self.partitioned_chunk, stream_ptr())
+            if rc != ERR_CONFIG or mode == "partitioned":
+                check(rc, "sspd_scan_partitioned")
+                return
+        call("sspd_scan_discrete", h_ptr, o_ptr, n, self.seav._params, seav_p, ldca_p, stream_ptr())
 
     def process_host_stream(self, hips, oips, chunk_pairs: int = 1 << 23):
         """Stream HOST arrays through two device staging buffers: the H2D copy
@@ -299,8 +326,7 @@ class DetectorState:
                 stage[b][1][:m].copy_(o[lo:lo + m], non_blocking=True)
                 self._ready[b].record(cs)
             compute.wait_event(self._ready[b])
-            call("sspd_scan_discrete", stage[b][0].data_ptr(), stage[b][1].data_ptr(), m, self.seav._params,
-                 self.seav.device_buffer().data_ptr(), self.ldca.device_buffer().data_ptr(), stream_ptr())
+            self._scan(stage[b][0].data_ptr(), stage[b][1].data_ptr(), m)
             self._free[b].record(compute)
         self.pair_count += n
         return 8 * n

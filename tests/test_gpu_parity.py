@@ -208,3 +208,32 @@ def test_reset_replay_and_merge(cuda):
         shards[0].seav.merge(s.seav)
         shards[0].ldca.merge(s.ldca)
     assert shards[0].seav.payload_bytes() == a and shards[0].ldca.payload_bytes() == b
+
+
+@pytest.mark.parametrize("case", ["uniform", "skewed", "nonpow2", "tiny_chunks"])
+def test_partitioned_scan_vs_oracle(cuda, oracle, case):
+    """K1p (LDCA in shared memory, bucketed exchange) is bit-identical to the
+    oracle, including the overflow fallbacks a skewed stream triggers."""
+    from paper_1901_07306_b200 import DetectorParams
+
+    geom = dict(theta=1024, r=12, k=8192, lr=8, lc=1024)
+    if case == "nonpow2":
+        geom = dict(theta=512, r=8, k=1000, lr=7, lc=333)
+    dp = DetectorParams(design_n=1e6, **geom)
+    _, _, p = params_block(dp)
+    rng = np.random.default_rng(77)
+    n = 3_000_017
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    if case == "skewed":
+        hips[: n // 2] = 0xC0A80001  # one host: its 8 cells take half of all updates
+        hips[n // 2: n // 2 + 100_000] = 0x0A000001
+    seav, ldca = oracle.scan(p, hips, oips, threads=8)
+    st = make_state(dp)
+    st.scan_mode = "partitioned"
+    if case == "tiny_chunks":
+        st.partitioned_chunk = 1 << 14
+    st.process_batch(hips[: n // 3], oips[: n // 3])
+    st.process_batch(hips[n // 3:], oips[n // 3:])
+    assert st.seav.payload_bytes() == seav.tobytes()
+    assert st.ldca.payload_bytes() == ldca.tobytes()
