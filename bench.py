@@ -226,6 +226,9 @@ def run_gpu(args) -> dict | None:
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         st = DetectorState.create(dp)
+    st.scan_mode = args.scan_mode
+    if args.part_chunk:
+        st.partitioned_chunk = args.part_chunk
     merger = None
     if world > 1:
         from paper_1901_07306_b200.multigpu import OrMerger
@@ -380,6 +383,8 @@ def main():
     ap.add_argument("--cpu-scale", type=int, default=32, help="CPU sample = config 2 / scale")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scan-mode", default="auto", choices=["auto", "direct", "partitioned"])
+    ap.add_argument("--part-chunk", type=int, default=0, help="partitioned-scan chunk (packets); 0 = default")
     args = ap.parse_args()
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:

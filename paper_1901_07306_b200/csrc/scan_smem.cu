@@ -106,13 +106,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
         const uint32_t* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
         const uint32_t m4 = m >> 2;
-#pragma unroll 2
-        for (uint32_t j = lane; j < m4; j += 32) {
-          const uint4 u = __ldcg(reinterpret_cast<const uint4*>(reg) + j);
-          atomicOr(&part[u.x >> 5], 1u << (u.x & 31));
-          atomicOr(&part[u.y >> 5], 1u << (u.y & 31));
-          atomicOr(&part[u.z >> 5], 1u << (u.z & 31));
-          atomicOr(&part[u.w >> 5], 1u << (u.w & 31));
+        const uint4* r4 = reinterpret_cast<const uint4*>(reg);
+        for (uint32_t j0 = lane; j0 < m4; j0 += 128) {  // 4 independent 16-B loads in flight per lane
+          uint4 u[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (j0 + 32 * g < m4) u[g] = __ldcg(r4 + j0 + 32 * g);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (j0 + 32 * g < m4) {
+              atomicOr(&part[u[g].x >> 5], 1u << (u[g].x & 31));
+              atomicOr(&part[u[g].y >> 5], 1u << (u[g].y & 31));
+              atomicOr(&part[u[g].z >> 5], 1u << (u[g].z & 31));
+              atomicOr(&part[u[g].w >> 5], 1u << (u[g].w & 31));
+            }
+          }
         }
         for (uint32_t j = (m4 << 2) + lane; j < m; j += 32) {
           const uint32_t u = __ldcg(reg + j);
@@ -128,12 +136,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t per = (c1 - c0 + gridDim.x - 1) / gridDim.x;
       const uint64_t lo = min(c1, c0 + per * self);
       const uint64_t hi = min(c1, lo + per);
+      // software pipeline: the next tile's (hip, oip) are loaded into
+      // registers while the current tile is hashed and flushed
+      uint32_t nh[kPktPerThread], no[kPktPerThread];
+#pragma unroll
+      for (uint32_t e = 0; e < kPktPerThread; ++e) {
+        const uint64_t j = lo + e * kThreads + tid;
+        nh[e] = j < hi ? __ldcs(hips + j) : 0u;
+        no[e] = j < hi ? __ldcs(oips + j) : 0u;
+      }
       for (uint64_t base = lo; base < hi; base += kTile) {
+        uint32_t ch[kPktPerThread], co[kPktPerThread];
+#pragma unroll
+        for (uint32_t e = 0; e < kPktPerThread; ++e) {
+          ch[e] = nh[e];
+          co[e] = no[e];
+          const uint64_t jn = base + kTile + e * kThreads + tid;
+          nh[e] = jn < hi ? __ldcs(hips + jn) : 0u;
+          no[e] = jn < hi ? __ldcs(oips + jn) : 0u;
+        }
 #pragma unroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
           const uint64_t j = base + e * kThreads + tid;
           if (j < hi) {
-            const uint32_t hip = __ldcs(hips + j), oip = __ldcs(oips + j);
+            const uint32_t hip = ch[e], oip = co[e];
             if (kFast) {
               // k, lc powers of two and < 2^32 LDCA bits: the modulo is a mask
               // of the low hash word and all index math is 32-bit.
@@ -261,7 +287,8 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
     P.div_part.sh2 = l - 1;
     P.div_part.pow2 = 0;
   }
-  P.chunk = chunk ? chunk : (1ull << 21);
+  // default chunk: 4 full tiles per CTA, so every producer slice is whole tiles
+  P.chunk = chunk ? chunk : (uint64_t)P.nparts * kTile * 4;
   const double rmean = (double)P.chunk * p->lr / ((double)P.nparts * P.nparts);
   P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
   P.region_cap = (P.region_cap + 31u) & ~31u;
