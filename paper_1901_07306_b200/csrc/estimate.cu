@@ -372,40 +372,93 @@ __global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict
   }
 }
 
-// Stable single-CTA compaction (the report list is small: it is bounded by
-// the candidate count).
-__global__ void __launch_bounds__(1024) compact_kernel(const uint32_t* __restrict__ ip,
-                                                       const uint32_t* __restrict__ z0,
-                                                       const uint8_t* __restrict__ keep, uint64_t n,
-                                                       uint32_t* ip_out, uint32_t* z0_out,
-                                                       unsigned long long* out_count) {
+// Stable compaction of the kept candidates.  Segment b of kSeg entries is
+// owned by block b: pass 1 counts each segment, pass 2 sums the preceding
+// counts (<= 1024 of them) and scatters its segment in order with a
+// ballot-based block scan.
+constexpr uint32_t kSeg = 8192;
+
+__device__ void compact_segment(const uint32_t* __restrict__ ip, const uint32_t* __restrict__ z0,
+                                const uint8_t* __restrict__ keep, uint64_t lo, uint64_t hi, uint32_t* ip_out,
+                                uint32_t* z0_out, unsigned long long base) {
   __shared__ uint32_t warp_sums[32];
-  __shared__ unsigned long long base_s;
-  if (threadIdx.x == 0) base_s = 0;
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint64_t start = 0; start < n; start += blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (uint64_t start = lo; start < hi; start += blockDim.x) {
     const uint64_t j = start + threadIdx.x;
-    const uint32_t f = (j < n && keep[j]) ? 1u : 0u;
+    const uint32_t f = (j < hi && keep[j]) ? 1u : 0u;
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, f);
-    const uint32_t before_in_warp = __popc(ballot & ((1u << lane) - 1u));
     if (lane == 0) warp_sums[wid] = __popc(ballot);
     __syncthreads();
-    uint32_t before_warps = 0, total = 0;
-    for (uint32_t wv = 0; wv < (blockDim.x >> 5); ++wv) {
-      if (wv < wid) before_warps += warp_sums[wv];
+    uint32_t before = __popc(ballot & ((1u << lane) - 1u)), total = 0;
+    for (uint32_t wv = 0; wv < nw; ++wv) {
+      if (wv < wid) before += warp_sums[wv];
       total += warp_sums[wv];
     }
     if (f) {
-      const unsigned long long o = base_s + before_warps + before_in_warp;
-      ip_out[o] = ip[j];
-      z0_out[o] = z0[j];
+      ip_out[base + before] = ip[j];
+      z0_out[base + before] = z0[j];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) base_s += total;
+    base += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out_count = base_s;
+}
+
+__global__ void __launch_bounds__(1024) compact_count_kernel(const uint8_t* __restrict__ keep, uint64_t n,
+                                                             uint32_t* seg_counts) {
+  const uint64_t lo = (uint64_t)blockIdx.x * kSeg, hi = min(n, lo + kSeg);
+  uint32_t c = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += keep[j] ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  __shared__ uint32_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += ws[w];
+    seg_counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) compact_scatter_kernel(const uint32_t* __restrict__ ip,
+                                                               const uint32_t* __restrict__ z0,
+                                                               const uint8_t* __restrict__ keep, uint64_t n,
+                                                               const uint32_t* __restrict__ seg_counts,
+                                                               uint32_t* ip_out, uint32_t* z0_out,
+                                                               unsigned long long* out_count) {
+  __shared__ unsigned long long base_s;
+  __shared__ uint32_t ws[32];
+  uint32_t pre = 0;
+  for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += seg_counts[b];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = pre;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += ws[w];
+    base_s = t;
+    if (blockIdx.x == gridDim.x - 1) *out_count = t + seg_counts[blockIdx.x];
+  }
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * kSeg, hi = min(n, lo + kSeg);
+  compact_segment(ip, z0, keep, lo, hi, ip_out, z0_out, base_s);
+}
+
+__global__ void __launch_bounds__(1024) compact_single_kernel(const uint32_t* __restrict__ ip,
+                                                              const uint32_t* __restrict__ z0,
+                                                              const uint8_t* __restrict__ keep, uint64_t n,
+                                                              uint32_t* ip_out, uint32_t* z0_out,
+                                                              unsigned long long* out_count) {
+  __shared__ uint32_t cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  compact_segment(ip, z0, keep, 0, n, ip_out, z0_out, 0);
+  uint32_t c = 0;
+  for (uint64_t j = threadIdx.x; j < n; j += blockDim.x) c += keep[j] ? 1u : 0u;
+  atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) *out_count = cnt;
 }
 
 static int build_plan(const sspd_params& p, RestorePlan& P) {
@@ -546,10 +599,23 @@ extern "C" int sspd_filter_sliding(const void* pool, uint32_t ts_bytes, const ss
 extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, const uint8_t* keep, uint64_t n,
                                     uint32_t* ip_out, uint32_t* z0_out, unsigned long long* out_count, void* scratch,
                                     size_t* scratch_bytes, void* stream) {
-  (void)scratch;
-  if (scratch_bytes) *scratch_bytes = 0;
   if (!out_count) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  compact_kernel<<<1, 1024, 0, st>>>(ip, z0, keep, n, ip_out, z0_out, out_count);
+  const uint64_t segs = (n + kSeg - 1) / kSeg;
+  const size_t need = 4 * (segs ? segs : 1);
+  if (!scratch) {
+    if (scratch_bytes) {  // size query
+      *scratch_bytes = need;
+      return SSPD_OK;
+    }
+    compact_single_kernel<<<1, 1024, 0, st>>>(ip, z0, keep, n, ip_out, z0_out, out_count);
+    return check_launch();
+  }
+  if (!scratch_bytes || *scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  if (n == 0) return cudaMemsetAsync(out_count, 0, sizeof(unsigned long long), st) == cudaSuccess ? SSPD_OK
+                                                                                                 : SSPD_ERR_CUDA;
+  uint32_t* seg_counts = static_cast<uint32_t*>(scratch);
+  compact_count_kernel<<<(unsigned)segs, 1024, 0, st>>>(keep, n, seg_counts);
+  compact_scatter_kernel<<<(unsigned)segs, 1024, 0, st>>>(ip, z0, keep, n, seg_counts, ip_out, z0_out, out_count);
   return check_launch();
 }

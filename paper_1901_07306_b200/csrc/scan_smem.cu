@@ -126,6 +126,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t u = __ldcg(reg + j);
           atomicOr(&part[u >> 5], 1u << (u & 31));
         }
+        // the region is dead once read: drop its L2 lines without write-back
+        // so bucket traffic stays on-chip instead of spilling to HBM
+        __syncwarp();
+        for (uint32_t line = lane; line * 32 < m; line += 32)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(reg + line * 32) : "memory");
       }
     }
     // ---------------- produce chunk t ------------------------------------

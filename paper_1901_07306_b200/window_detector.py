@@ -14,6 +14,7 @@ Mirrors `sspd/window_detector.py` (DetectorParams :39-69, DetectorState
 
 from __future__ import annotations
 
+import ctypes
 import warnings
 from collections.abc import Sequence
 from dataclasses import dataclass, field
@@ -211,8 +212,12 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
     ip_out = torch.empty(n, dtype=torch.int32, device=dev)
     z0_out = torch.empty(n, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    need = ctypes.c_size_t(0)
     call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
-         z0_out.data_ptr(), cnt.data_ptr(), None, None, stream_ptr())
+         z0_out.data_ptr(), cnt.data_ptr(), None, ctypes.byref(need), stream_ptr())
+    scratch = torch.empty(max(16, need.value), dtype=torch.uint8, device=dev)
+    call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
+         z0_out.data_ptr(), cnt.data_ptr(), scratch.data_ptr(), ctypes.byref(need), stream_ptr())
     m = int(cnt.item())
     both = torch.stack((ip_out[:m], z0_out[:m])).cpu().numpy().view(np.uint32)
     return both[0], both[1]

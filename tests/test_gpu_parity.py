@@ -237,3 +237,37 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case):
     st.process_batch(hips[n // 3:], oips[n // 3:])
     assert st.seav.payload_bytes() == seav.tobytes()
     assert st.ldca.payload_bytes() == ldca.tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 1000, 8192, 8193, 100_003])
+def test_compaction_is_stable(cuda, n):
+    """sspd_compact_reports (multi-segment and single-CTA forms) keeps order."""
+    import ctypes
+
+    import torch
+
+    from paper_1901_07306_b200._device import call, stream_ptr
+
+    rng = np.random.default_rng(n)
+    ip = torch.from_numpy(rng.integers(0, 2**31, n, dtype=np.int64).astype(np.int32)).cuda()
+    z0 = torch.from_numpy(rng.integers(0, 8193, n, dtype=np.int64).astype(np.int32)).cuda()
+    keep = torch.from_numpy((rng.random(n) < 0.37).astype(np.uint8)).cuda()
+    want = keep.cpu().numpy().astype(bool)
+    for multi in (True, False):
+        ip_o = torch.zeros(n, dtype=torch.int32, device="cuda")
+        z0_o = torch.zeros(n, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        need = ctypes.c_size_t(0)
+        if multi:
+            call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_o.data_ptr(),
+                 z0_o.data_ptr(), cnt.data_ptr(), None, ctypes.byref(need), stream_ptr())
+            scratch = torch.empty(need.value, dtype=torch.uint8, device="cuda")
+            call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_o.data_ptr(),
+                 z0_o.data_ptr(), cnt.data_ptr(), scratch.data_ptr(), ctypes.byref(need), stream_ptr())
+        else:
+            call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_o.data_ptr(),
+                 z0_o.data_ptr(), cnt.data_ptr(), None, None, stream_ptr())
+        m = int(cnt.item())
+        assert m == int(want.sum())
+        assert (ip_o[:m].cpu().numpy() == ip.cpu().numpy()[want]).all()
+        assert (z0_o[:m].cpu().numpy() == z0.cpu().numpy()[want]).all()
