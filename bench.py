@@ -203,20 +203,27 @@ def run_gpu(args) -> dict | None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:  # protocol test: all ranks share GPU 0 (host barriers only)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     lib()
 
     from dataclasses import replace
 
     spec = replace(CONFIG2, seed=CONFIG2.seed + rank)
     if args.packets:
-        spec = replace(spec, n_packets=args.packets, n_sources=max(1024, args.packets // 16))
+        from tools.workloads import scaled
+
+        spec = scaled(spec, max(1, CONFIG2.n_packets // args.packets))
     t_gen = time.perf_counter()
     hips, oips, supers = generate(spec, "torch", dev)
     torch.cuda.synchronize()
@@ -270,7 +277,7 @@ def run_gpu(args) -> dict | None:
         barrier()
         ms = e0.elapsed_time(e1) / steps
         if dist is not None:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if args.backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -331,13 +338,27 @@ def run_gpu(args) -> dict | None:
     hbm_gbs = peaks.get("hbm_gbs", 6650.0)
     achieved_gbs = 8 * n / (scan_ms * 1e-3) / 1e9
     roof_pps = min(hbm_gbs * 1e9 / 8, red_per_s / reds_per_pkt)
-    traffic = None
-    tf = ROOT / "profiles" / "scan_traffic.json"
-    if tf.exists():
+    kernel = getattr(st, "last_scan", "direct")
+    kname = ("scan_partitioned_kernel<true,true> (K1p, LDCA in shared memory)" if kernel == "partitioned"
+             else "scan_discrete_kernel<true,true> (K1, L2 red.or)")
+    # per-kernel ncu evidence committed under profiles/ (bytes and issue slots per packet)
+    prof = {}
+    pf = ROOT / "profiles" / "scan_ncu_summary.json"
+    if pf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+            prof = json.loads(pf.read_text()).get(kernel, {})
         except ValueError:
-            traffic = None
+            prof = {}
+    traffic = prof.get("dram_bytes_per_packet")
+    traffic = round(traffic * n) if traffic else None
+    issue = None
+    if prof.get("warp_inst_per_packet"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk_hz = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        issue_pps = sms * 4 * clk_hz / prof["warp_inst_per_packet"]  # 4 schedulers x 1 warp-inst/clk
+        issue = {"bound": "sm_issue", "warp_inst_per_packet": prof["warp_inst_per_packet"],
+                 "roofline_gpps": round(issue_pps / 1e9, 3), "frac": round(scan_pps / issue_pps, 4),
+                 "source": prof.get("source")}
 
     value = world * n / (ms * 1e-3) / 1e6
     line = {
@@ -354,12 +375,15 @@ def run_gpu(args) -> dict | None:
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": hbm_gbs, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback",
-                     "kernel": "scan_discrete_kernel<true,true> (K1)"},
+                     "kernel": kname, "algorithmic_bytes_per_packet": 8},
         "scan_roofline": {"bound": "l2_red", "l2_red_ops_per_s": round(red_per_s / 1e9, 2),
                           "reds_per_packet": round(reds_per_pkt, 4), "roofline_gpps": round(roof_pps / 1e9, 3),
                           "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / roof_pps, 4),
                           "scan_ms": round(scan_ms, 4), "scan_share_of_step": round(scan_share, 4),
-                          "note": "min(HBM 8 B/pkt, L2 red.or rate / reds per pkt) -- SURVEY.md §8d"},
+                          "note": ("SURVEY.md §8d roofline min(HBM 8 B/pkt, L2 red.or rate / reds per pkt), red "
+                                   "rate measured live; K1p keeps the LDCA in shared memory so it is not bound "
+                                   "by L2 atomics -- see issue_roofline")},
+        "issue_roofline": issue,
         "clocks": clk,
         "detect": {"reports_per_window": counts[0] if counts else None,
                    "planted_supers_found": planted_found, "planted": len(supers)},
@@ -385,6 +409,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "direct", "partitioned"])
     ap.add_argument("--part-chunk", type=int, default=0, help="partitioned-scan chunk (packets); 0 = default")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
     args = ap.parse_args()
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:

@@ -288,8 +288,10 @@ class DetectorState:
                                              scratch.data_ptr(), need, self.partitioned_chunk, stream_ptr())
             if rc != ERR_CONFIG or mode == "partitioned":
                 check(rc, "sspd_scan_partitioned")
+                self.last_scan = "partitioned"
                 return
         call("sspd_scan_discrete", h_ptr, o_ptr, n, self.seav._params, seav_p, ldca_p, stream_ptr())
+        self.last_scan = "direct"
 
     def process_host_stream(self, hips, oips, chunk_pairs: int = 1 << 23):
         """Stream HOST arrays through two device staging buffers: the H2D copy
