@@ -396,6 +396,84 @@ def run_gpu(args) -> dict | None:
     return line
 
 
+def run_sliding(args) -> dict:
+    """Config 4 (BASELINE configs[3]): 2^29 packets with millisecond
+    timestamps (Poisson 1.8 M pkt/s, ~298 one-second slices), w = 300
+    slices, super-point list at EVERY slide.  One step = the whole trace:
+    per slice K2 observe (plain u16 stores) + detect (K4 materialize,
+    K5 restore, K6 filter on the pool) + advance."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+    from tools.workloads import CONFIG4, CONFIG4_TIMING, TimingSpec, generate, scaled
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    spec, timing = CONFIG4, CONFIG4_TIMING
+    if args.packets:
+        spec = scaled(CONFIG4, max(1, CONFIG4.n_packets // args.packets))
+        timing = TimingSpec(rate_pps=spec.n_packets / (CONFIG4.n_packets / CONFIG4_TIMING.rate_pps))
+    t_gen = time.perf_counter()
+    hips, oips, supers, ts = generate(spec, "torch", dev, timing=timing)
+    slices = ts // 1000
+    n_sl = int(slices[-1].item()) + 1
+    bounds = torch.searchsorted(slices, torch.arange(n_sl + 1, device=dev, dtype=slices.dtype)).cpu().tolist()
+    t_gen = time.perf_counter() - t_gen
+    n = int(hips.numel())
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=1024, design_n=2.15e8),
+                              window_slices=300)
+    stream = torch.cuda.current_stream()
+    counts = []
+
+    def step(record=None):
+        det.reset()
+        total = 0
+        for s in range(n_sl):
+            lo, hi = bounds[s], bounds[s + 1]
+            if hi > lo:
+                det.observe_batch(hips[lo:hi], oips[lo:hi])
+            total += len(det.detect())
+            det.advance_slice()
+        if record is not None:
+            record.append(total)
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(counts)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    # roofline of K2: 8 scattered 2-byte stores/packet into a 403 MB pool (> L2):
+    # HBM sector read-modify-write bound (SURVEY.md §8d: 8 + 8.031 x 32 B)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    bytes_pp = 8 + 8.031 * 32
+    value = n / (ms * 1e-3) / 1e6
+    return {
+        "metric": "packets/sec (Mpps) sliding scan+detect at every slide", "value": round(value, 3), "unit": UNIT,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 keys / u16 stamps",
+        "data": "synthetic (seeded, tools/workloads.py CONFIG4)",
+        "config": {"workload": f"config4: {n} pkts, {n_sl} slices, w=300, r=16, LDCA 8x1024x8192, detect every slide",
+                   "pool_bytes": det.pool.memory_bytes(), "l2": "pool 403 MB exceeds L2; inputs 4 GiB"},
+        "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
+                     "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
+                     "kernel": "whole trace (K2 + per-slide K4/K5/K6)", "bytes_per_packet_model": bytes_pp},
+        "clocks": clk, "detect": {"reports_total": counts[0] if counts else None, "slides": n_sl,
+                                  "planted": len(supers)},
+        "gen_s": round(t_gen, 2),
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -411,13 +489,15 @@ def main():
     ap.add_argument("--part-chunk", type=int, default=0, help="partitioned-scan chunk (packets); 0 = default")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4],
+                    help="2 = headline discrete window; 4 = sliding window, detect every slide")
     args = ap.parse_args()
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return
         print(json.dumps(run_reference(args)))
         return
-    line = run_gpu(args)
+    line = run_sliding(args) if args.config == 4 else run_gpu(args)
     if line is not None:
         print(json.dumps(line))
 

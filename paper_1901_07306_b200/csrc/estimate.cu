@@ -92,7 +92,8 @@ __device__ uint32_t warp_exclusive_scan(uint32_t* a, uint32_t m) {
 
 template <bool kEmit>
 __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uint64_t cap, uint32_t* out_ip,
-                             uint32_t* out_aux, uint64_t out_capacity, unsigned long long* out_count) {
+                             uint32_t* out_aux, uint64_t out_capacity, unsigned long long* out_count,
+                             uint32_t gtid, uint32_t gsize) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t* pref0 = reinterpret_cast<const uint32_t*>(sm + P.off_pref0);
   const uint32_t npairs = misc->pairs;
@@ -106,7 +107,7 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
   uint64_t since_flush = 0;
   volatile uint32_t* abort_flag = &misc->abort;
 
-  for (uint32_t t = threadIdx.x; t < npairs; t += blockDim.x) {
+  for (uint32_t t = gtid; t < npairs; t += gsize) {
     if (!kEmit && *abort_flag) break;
     // locate the row-0 entry owning pair t: last j with pref0[j] <= t
     uint32_t lo = 0, hi = h0;  // pref0 has h0+1 entries, pref0[h0] = npairs
@@ -190,13 +191,25 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
   }
 }
 
-__global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict__ seav,
-                                                      const __grid_constant__ RestorePlan P, uint32_t rp_begin,
-                                                      uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
-                                                      uint64_t out_capacity, unsigned long long* out_count,
-                                                      uint8_t* overflow) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  const uint32_t rp = rp_begin + blockIdx.x;
+// A "group" restores one SEA: the whole CTA (large arrays) or one warp
+// (small arrays, e.g. r=16 with 256 registers per SEA, where a CTA per SEA
+// would spend its life in barriers).  Only the synchronisation differs.
+template <bool kWarp>
+struct Group {
+  uint32_t tid, size, warp, nwarps;
+  __device__ __forceinline__ void sync() const {
+    if (kWarp)
+      __syncwarp();
+    else
+      __syncthreads();
+  }
+};
+
+template <bool kWarp>
+__device__ void restore_sea_group(const uint8_t* __restrict__ seav, const RestorePlan& P, uint8_t* sm, uint32_t rp,
+                                  uint32_t slot, uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
+                                  uint64_t out_capacity, unsigned long long* out_count, uint8_t* overflow,
+                                  const Group<kWarp> G) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t sr = P.sr;
 
@@ -206,58 +219,57 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
     const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * nbytes;
     uint8_t* dst = sm + P.off_regs[i];
     if ((nbytes & 15u) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
-      for (uint32_t o = threadIdx.x * 16; o < nbytes; o += blockDim.x * 16)
+      for (uint32_t o = G.tid * 16; o < nbytes; o += G.size * 16)
         *reinterpret_cast<uint4*>(dst + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
     } else {
-      for (uint32_t o = threadIdx.x; o < nbytes; o += blockDim.x) dst[o] = src[o];
+      for (uint32_t o = G.tid; o < nbytes; o += G.size) dst[o] = src[o];
     }
     uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
-    for (uint32_t o = threadIdx.x; o <= (1u << P.nk[i]); o += blockDim.x) bs[o] = 0;
+    for (uint32_t o = G.tid; o <= (1u << P.nk[i]); o += G.size) bs[o] = 0;
   }
-  if (threadIdx.x == 0) {
+  if (G.tid == 0) {
     misc->total = 0;
     misc->abort = 0;
     misc->pairs = 0;
     for (uint32_t i = 0; i < SSPD_MAX_SR; ++i) misc->hot[i] = 0;
   }
-  __syncthreads();
+  G.sync();
 
   // hot registers (weight >= 3, short_sketch.py:355-362) counted per bucket
   for (uint32_t i = 0; i < sr; ++i) {
     uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
     const uint8_t* regs = sm + P.off_regs[i];
-    for (uint32_t c = threadIdx.x; c < P.sc[i]; c += blockDim.x) {
+    for (uint32_t c = G.tid; c < P.sc[i]; c += G.size) {
       if (__popcll(load_reg(regs, c, P.reg_bytes)) >= 3) {
         atomicAdd(&bs[pext32(c, P.keymask[i]) + 1], 1u);
         atomicAdd(&misc->hot[i], 1u);
       }
     }
   }
-  __syncthreads();
+  G.sync();
   for (uint32_t i = 0; i < sr; ++i)
     if (misc->hot[i] == 0) return;  // a row without hot registers: no tuple (short_sketch.py:360-361)
 
   // bucket starts: exclusive scan of counts stored at [1 .. 2^nk]
-  const uint32_t warp = threadIdx.x >> 5;
-  for (uint32_t i = warp; i < sr; i += blockDim.x >> 5) {
+  for (uint32_t i = G.warp; i < sr; i += G.nwarps) {
     uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
     warp_exclusive_scan(bs + 1, 1u << P.nk[i]);
   }
-  __syncthreads();
+  G.sync();
   // scatter hot columns into their buckets; bs[key+1] advances to the end
   // of bucket key, leaving bs[key] = start of bucket key for every key.
   for (uint32_t i = 0; i < sr; ++i) {
     uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
     uint16_t* cols = reinterpret_cast<uint16_t*>(sm + P.off_cols[i]);
     const uint8_t* regs = sm + P.off_regs[i];
-    for (uint32_t c = threadIdx.x; c < P.sc[i]; c += blockDim.x) {
+    for (uint32_t c = G.tid; c < P.sc[i]; c += G.size) {
       if (__popcll(load_reg(regs, c, P.reg_bytes)) >= 3) {
         const uint32_t pos = atomicAdd(&bs[pext32(c, P.keymask[i]) + 1], 1u);
         cols[pos] = (uint16_t)c;
       }
     }
   }
-  __syncthreads();
+  G.sync();
 
   // flatten rows 0 x 1: pref0[j] = number of row-1 partners of row-0 entry j
   {
@@ -265,29 +277,55 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
     const uint16_t* cols0 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[0]);
     const uint32_t* b1 = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[1]);
     const uint32_t h0 = misc->hot[0];
-    for (uint32_t j = threadIdx.x; j < h0; j += blockDim.x) {
+    for (uint32_t j = G.tid; j < h0; j += G.size) {
       const uint64_t v0 = scatter_col(cols0[j], P.isb[0], P.ibn[0], P.w);
       const uint32_t key = pext32(index_of(v0, P.isb[1], P.ibn[1], P.w) & P.keymask[1], P.keymask[1]);
       pref0[j] = b1[key + 1] - b1[key];
     }
-    __syncthreads();
-    if (warp == 0) {
+    G.sync();
+    if (G.warp == 0) {
       const uint32_t total = warp_exclusive_scan(pref0, h0);
-      if (threadIdx.x == 0) {
+      if (G.tid == 0) {
         pref0[h0] = total;
         misc->pairs = total;
       }
     }
-    __syncthreads();
+    G.sync();
   }
 
-  restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count);
-  __syncthreads();
+  restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
+  G.sync();
   if (misc->total > cap) {
-    if (threadIdx.x == 0) overflow[blockIdx.x] = 1;
+    if (G.tid == 0) overflow[slot] = 1;
     return;
   }
-  restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count);
+  restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
+}
+
+// one SEA per warp, 4 warps per CTA, each warp with its own smem slice
+__global__ void __launch_bounds__(128) restore_warp_kernel(const uint8_t* __restrict__ seav,
+                                                           const __grid_constant__ RestorePlan P, uint32_t rp_begin,
+                                                           uint32_t rp_count, uint64_t cap, uint32_t* out_ip,
+                                                           uint32_t* out_aux, uint64_t out_capacity,
+                                                           unsigned long long* out_count, uint8_t* overflow) {
+  extern __shared__ __align__(16) uint8_t smw[];
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (slot >= rp_count) return;
+  const Group<true> G{threadIdx.x & 31u, 32u, 0u, 1u};
+  restore_sea_group<true>(seav, P, smw + (size_t)warp * P.smem_bytes, rp_begin + slot, slot, cap, out_ip, out_aux,
+                          out_capacity, out_count, overflow, G);
+}
+
+__global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict__ seav,
+                                                      const __grid_constant__ RestorePlan P, uint32_t rp_begin,
+                                                      uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
+                                                      uint64_t out_capacity, unsigned long long* out_count,
+                                                      uint8_t* overflow) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const Group<false> G{threadIdx.x, blockDim.x, threadIdx.x >> 5, blockDim.x >> 5};
+  restore_sea_group<false>(seav, P, sm, rp_begin + blockIdx.x, blockIdx.x, cap, out_ip, out_aux, out_capacity,
+                           out_count, overflow, G);
 }
 
 // ------------------------------------------------------------------ filter
@@ -350,17 +388,47 @@ __global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr uint32_t kVec = 16 / sizeof(T);  // stamps per 16-byte load
   for (uint64_t j = warp; j < n; j += nwarps) {
     const uint32_t ip = ips[j];
+    // lane i (and i+32) hashes row i once; cell bases are broadcast by shuffle
+    const uint64_t base_a =
+        lane < p.lr ? p.slot_ldca_base + ((uint64_t)lane * p.lc + hash_range(ip, p.seed_lh[lane], p.div_lc)) * p.k : 0;
+    const uint64_t base_b =
+        lane + 32 < p.lr
+            ? p.slot_ldca_base + ((uint64_t)(lane + 32) * p.lc + hash_range(ip, p.seed_lh[lane + 32], p.div_lc)) * p.k
+            : 0;
     uint32_t pop = 0;
-    for (uint32_t s = lane; s < p.k; s += 32) {
-      bool all = true;
-      for (uint32_t i = 0; i < p.lr && all; ++i) {
-        const uint64_t c = hash_range(ip, p.seed_lh[i], p.div_lc);
-        const T ts = pool[p.slot_ldca_base + ((uint64_t)i * p.lc + c) * p.k + s];
-        all = (uint64_t)(T)(now - ts) < window;
+    bool vec = (p.k % (32 * kVec)) == 0;
+    for (uint32_t i = 0; i < p.lr && vec; ++i)
+      vec = ((__shfl_sync(0xFFFFFFFFu, i < 32 ? base_a : base_b, i & 31) * sizeof(T)) & 15u) == 0;
+    if (vec) {
+      // each lane ANDs kVec consecutive stamps of every row with one 16-B load per row
+      for (uint32_t s0 = lane * kVec; s0 < p.k; s0 += 32 * kVec) {
+        uint32_t live = (1u << kVec) - 1u;
+        for (uint32_t i = 0; i < p.lr; ++i) {
+          const uint64_t base = __shfl_sync(0xFFFFFFFFu, i < 32 ? base_a : base_b, i & 31);
+          union {
+            uint4 v;
+            T t[kVec];
+          } u;
+          u.v = __ldg(reinterpret_cast<const uint4*>(pool + base + s0));
+#pragma unroll
+          for (uint32_t e = 0; e < kVec; ++e)
+            if ((uint64_t)(T)(now - u.t[e]) >= window) live &= ~(1u << e);
+        }
+        pop += __popc(live);
       }
-      pop += all ? 1u : 0u;
+    } else {
+      for (uint32_t s0 = 0; s0 < p.k; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        bool all = s < p.k;
+        for (uint32_t i = 0; i < p.lr; ++i) {
+          const uint64_t base = __shfl_sync(0xFFFFFFFFu, i < 32 ? base_a : base_b, i & 31);
+          if (all) all = (uint64_t)(T)(now - pool[base + s]) < window;
+        }
+        pop += all ? 1u : 0u;
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
@@ -520,9 +588,17 @@ extern "C" int sspd_restore(const uint8_t* seav, const sspd_params* p, uint32_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if ((int)P.smem_bytes > max_smem) return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t regs = 0;
+  for (uint32_t i = 0; i < p->sr; ++i) regs += p->sc[i];
+  if (regs <= 512 && 4 * P.smem_bytes <= 48 * 1024) {  // small arrays: one warp per SEA
+    const uint32_t blocks = (rp_count + 3) / 4;
+    restore_warp_kernel<<<blocks, 128, 4 * P.smem_bytes, st>>>(seav, P, rp_begin, rp_count, cap, out_ip, out_aux,
+                                                               out_capacity, out_count, overflow);
+    return check_launch();
+  }
   if (P.smem_bytes > 48 * 1024)
     cudaFuncSetAttribute(restore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   restore_kernel<<<rp_count, 128, P.smem_bytes, st>>>(seav, P, rp_begin, cap, out_ip, out_aux, out_capacity,
                                                       out_count, overflow);
   return check_launch();

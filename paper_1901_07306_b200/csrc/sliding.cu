@@ -47,8 +47,22 @@ __global__ void __launch_bounds__(256) materialize_seav_kernel(const T* __restri
     }
     const T* slots = pool + p.slot_row_base[i] + local * p.g;
     uint64_t reg = 0;
-    for (uint32_t b = 0; b < p.g; ++b)
-      if (active<T>(slots[b], now, window)) reg |= 1ull << b;
+    constexpr uint32_t kVec = 16 / sizeof(T);
+    if ((p.g % kVec) == 0 && (reinterpret_cast<uintptr_t>(slots) & 15u) == 0) {
+      for (uint32_t b0 = 0; b0 < p.g; b0 += kVec) {  // 16-byte loads of kVec stamps
+        union {
+          uint4 v;
+          T t[kVec];
+        } u;
+        u.v = __ldg(reinterpret_cast<const uint4*>(slots + b0));
+#pragma unroll
+        for (uint32_t e = 0; e < kVec; ++e)
+          if (active<T>(u.t[e], now, window)) reg |= 1ull << (b0 + e);
+      }
+    } else {
+      for (uint32_t b = 0; b < p.g; ++b)
+        if (active<T>(slots[b], now, window)) reg |= 1ull << b;
+    }
     uint8_t* dst = out + p.seav_row_off[i] + local * p.reg_bytes;
     switch (p.reg_bytes) {
       case 1: *dst = (uint8_t)reg; break;
@@ -69,8 +83,18 @@ __global__ void __launch_bounds__(256) materialize_ldca_kernel(const T* __restri
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nbytes; q += stride) {
     const T* s = pool + base + q * 8;
     uint32_t v = 0;
+    if (sizeof(T) == 2 && (reinterpret_cast<uintptr_t>(s) & 15u) == 0) {  // 8 u16 stamps = one 16-B load
+      union {
+        uint4 v4;
+        T t[8];
+      } u;
+      u.v4 = __ldg(reinterpret_cast<const uint4*>(s));
 #pragma unroll
-    for (int b = 0; b < 8; ++b) v |= (active<T>(s[b], now, window) ? 1u : 0u) << b;
+      for (int b = 0; b < 8; ++b) v |= (active<T>(u.t[b], now, window) ? 1u : 0u) << b;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v |= (active<T>(s[b], now, window) ? 1u : 0u) << b;
+    }
     out[q] = (uint8_t)v;
   }
 }
@@ -117,7 +141,8 @@ extern "C" int sspd_materialize_seav(const void* pool, uint32_t ts_bytes, const 
   uint64_t regs = 0;
   for (uint32_t i = 0; i < p->sr; ++i) regs += ((uint64_t)p->sc[i]) << p->r;
   SSPD_TS_DISPATCH(ts_bytes, {
-    const int grid = grid_for(materialize_seav_kernel<T>, 256, regs);
+    // one register per thread: a full grid keeps every load independent
+    const int grid = (int)((regs + 255) / 256 < 0x7FFFFFFFull ? (regs + 255) / 256 : 0x7FFFFFFF);
     materialize_seav_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, *p, (T)now_wrapped, window_slices, seav_out);
   })
   return check_launch();
@@ -132,7 +157,7 @@ extern "C" int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes, const 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t nbytes = p->ldca_bytes;
   SSPD_TS_DISPATCH(ts_bytes, {
-    const int grid = grid_for(materialize_ldca_kernel<T>, 256, nbytes);
+    const int grid = (int)((nbytes + 255) / 256 < 0x7FFFFFFFull ? (nbytes + 255) / 256 : 0x7FFFFFFF);
     materialize_ldca_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, p->slot_ldca_base, nbytes, (T)now_wrapped,
                                                      window_slices, ldca_out);
   })

@@ -77,6 +77,13 @@ class TimestampPool:
     def device_buffer(self):
         return self._buf
 
+    def reset(self):
+        """Back to the constructor state (slice 0, every slot just expired)."""
+        self.now = 0
+        self._since_sweep = 0
+        self.sweep_count = 0
+        self._buf.fill_(_as_signed((-self.window_slices) & self._mask, self.ts_bytes))
+
     @property
     def ts(self) -> np.ndarray:
         return self._buf.cpu().numpy().view(self.dtype)
@@ -198,6 +205,10 @@ class SlidingDetector:
     def advance_slice(self):
         self.pool.advance_slice()
 
+    def reset(self):
+        self.pool.reset()
+        self.pair_count = 0
+
     def observe_batch(self, hips, oips):
         """K2: stamp every slot the discrete path would set (sliding.py:156-185)."""
         from ._device import call, ips_to_device, stream_ptr
@@ -262,12 +273,21 @@ class SlidingDetector:
         """Materialise (K4) -> restore (K5) -> filter on the pool (K6) (sliding.py:232-248)."""
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
-        seav = self.materialize_seav()
+        seav = getattr(self, "_view", None)  # reused across slides: K4 overwrites every register
+        if seav is None:
+            seav = self._view = self.materialize_seav()
+        else:
+            self._materialize_into(seav)
         pool = self.pool
         k = self.ldca_config.k
+        lview = getattr(self, "_ldca_view", None)
+        if lview is None:
+            from ._device import zeros_bytes
+
+            lview = self._ldca_view = zeros_bytes(self._params.ldca_bytes)
         ips, z0s = filter_candidates(
             seav, None, self._params, k, cutoff,
-            sliding=(pool.device_buffer(), pool.ts_bytes, pool._wrapped_now(), pool.window_slices))
+            sliding=(pool.device_buffer(), pool.ts_bytes, pool._wrapped_now(), pool.window_slices, lview))
         return ReportList(ips, z0s, k, self.now, "sliding")
 
 

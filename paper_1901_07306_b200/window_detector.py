@@ -206,9 +206,20 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
         call("sspd_filter", ldca_buf.data_ptr(), params_block, ip.data_ptr(), n, table.data_ptr(),
              z0.data_ptr(), keep.data_ptr(), stream_ptr())
     else:
-        pool, ts_bytes, now_w, window = sliding
-        call("sspd_filter_sliding", pool.data_ptr(), ts_bytes, params_block, now_w, window,
-             ip.data_ptr(), n, table.data_ptr(), z0.data_ptr(), keep.data_ptr(), stream_ptr())
+        pool, ts_bytes, now_w, window = sliding[:4]
+        view = sliding[4] if len(sliding) > 4 else None
+        if view is not None and n > params_block.lc:
+            # many candidates re-read the same LDCA cells: materialize the
+            # active-bit view once (K4, one pass over the LDCA stamps) and
+            # filter on packed bits; few candidates read their cells' stamps
+            # directly (K6 sliding)
+            call("sspd_materialize_ldca", pool.data_ptr(), ts_bytes, params_block, now_w, window,
+                 view.data_ptr(), stream_ptr())
+            call("sspd_filter", view.data_ptr(), params_block, ip.data_ptr(), n, table.data_ptr(),
+                 z0.data_ptr(), keep.data_ptr(), stream_ptr())
+        else:
+            call("sspd_filter_sliding", pool.data_ptr(), ts_bytes, params_block, now_w, window,
+                 ip.data_ptr(), n, table.data_ptr(), z0.data_ptr(), keep.data_ptr(), stream_ptr())
     ip_out = torch.empty(n, dtype=torch.int32, device=dev)
     z0_out = torch.empty(n, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)

@@ -201,11 +201,13 @@ def cardinalities(spec: StreamSpec) -> np.ndarray:
 
 
 # -------------------------------------------------------------- generator
-def generate(spec: StreamSpec, backend: str = "numpy", device=None):
+def generate(spec: StreamSpec, backend: str = "numpy", device=None, timing=None):
     """(hips, oips, supers): exactly spec.n_packets pairs.
 
     numpy backend -> uint32 arrays; torch backend -> int32 device tensors
     holding the uint32 bit patterns.  `supers` = sorted planted IPs (numpy).
+    With `timing` (config 4) a fourth array of non-decreasing millisecond
+    timestamps is returned and the stream is in arrival order.
     """
     xp = _NP() if backend == "numpy" else _Torch(device)
     seed = spec.seed
@@ -235,13 +237,61 @@ def generate(spec: StreamSpec, backend: str = "numpy", device=None):
         pad = xp.shr(xp.draw(T_PAD, seed, xp.arange(need - pool_n)), 1) % n_edges
         extra = xp.cat([extra_pool, pad])
     edges = xp.cat([eidx, extra])
-    order = xp.argsort(xp.shr(xp.draw(T_ORDER, seed, xp.arange(spec.n_packets)), 1))
+    ts_ms = None
+    if timing is None:
+        order = xp.argsort(xp.shr(xp.draw(T_ORDER, seed, xp.arange(spec.n_packets)), 1))
+    else:
+        # config 4: every packet gets an integer-microsecond arrival time --
+        # background uniform over the trace, planted supers uniform inside
+        # their own active interval -- and the stream is sorted by time
+        # (sorted uniform arrivals = a Poisson stream of the given rate).
+        span_us = int(round(spec.n_packets / timing.rate_pps * 1e6))
+        u = xp.shr(xp.draw(T_TIME, seed, xp.arange(spec.n_packets)), 11)
+        host = host_of[edges]
+        is_sup = host < spec.n_super
+        lo_h, len_h = super_intervals(spec, timing, span_us)
+        lo_t, len_t = xp.host(lo_h), xp.host(len_h)
+        hs = host * is_sup  # index 0 for background (masked below)
+        t_sup = lo_t[hs] + u % len_t[hs]
+        t_bg = u % span_us
+        t_us = t_sup * is_sup + t_bg * (1 - is_sup * 1)
+        order = xp.argsort(t_us * (1 << 24) + (xp.arange(spec.n_packets) & ((1 << 24) - 1)))
+        ts_ms = (t_us[order] // 1000)
     stream = edges[order]
     hips = src_ip[host_of[stream]]
     oips = dst[stream]
     supers = src_ip[: spec.n_super]
     if backend == "numpy":
-        return hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32))
+        out = (hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32)))
+        return out if ts_ms is None else out + (ts_ms.astype(np.uint32),)
     t = xp.t
     to32 = lambda x: t.where(x >= 2**31, x - 2**32, x).to(t.int32)  # noqa: E731
-    return to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32))
+    out = (to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32)))
+    return out if ts_ms is None else out + (ts_ms.to(t.int32),)
+
+
+@dataclass(frozen=True)
+class TimingSpec:
+    """Config 4: Poisson arrivals, planted supers active on sub-ranges."""
+
+    rate_pps: float = 1.8e6
+    active_s: tuple[int, int] = (60, 600)
+
+
+CONFIG4 = StreamSpec("config4", 1 << 29, 1_740_000, 256, (2048, 2048), 1.1, 200, 0.4, seed=4)
+CONFIG4_TIMING = TimingSpec()
+
+
+def super_intervals(spec: StreamSpec, timing: TimingSpec, span_us: int):
+    """[lo, lo+len) activity interval (microseconds) of every planted super,
+    lengths U[active_s] clipped to the trace span (BASELINE configs[3])."""
+    key = mix64_int(((spec.seed & 0xFFFFFFFF) << 8) | T_SPLIT)
+    lo = np.zeros(max(1, spec.n_super), dtype=np.int64)
+    ln = np.ones(max(1, spec.n_super), dtype=np.int64)
+    a, b = timing.active_s
+    for s in range(spec.n_super):
+        d1, d2 = mix64_int(2 * s ^ key), mix64_int((2 * s + 1) ^ key)
+        length = min(span_us, (a + d1 % (b - a + 1)) * 1_000_000)
+        start = d2 % max(1, span_us - length + 1)
+        lo[s], ln[s] = start, max(1, length)
+    return lo, ln
