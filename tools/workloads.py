@@ -295,3 +295,109 @@ def super_intervals(spec: StreamSpec, timing: TimingSpec, span_us: int):
         start = d2 % max(1, span_us - length + 1)
         lo[s], ln[s] = start, max(1, length)
     return lo, ln
+
+
+# ----------------------------------------------------- config 3 (sharded)
+@dataclass(frozen=True)
+class ShardedSpec:
+    """Config 3: n_shards routers over one global source population; every
+    planted super's peers are split evenly over 2..8 distinct routers so no
+    router sees more than 1,023 of them (BASELINE configs[2])."""
+
+    name: str = "config3"
+    n_shards: int = 8
+    packets_per_shard: int = 1 << 27
+    n_sources: int = 33_554_432
+    n_super: int = 1024
+    routers: tuple[int, int] = (2, 8)
+    zipf_s: float = 1.05
+    zipf_max: int = 1000
+    dup_p: float = 0.3
+    seed: int = 3
+
+
+CONFIG3 = ShardedSpec()
+T_SHARD = 11
+
+
+def sharded_scaled(spec: ShardedSpec, factor: int) -> ShardedSpec:
+    return replace(spec, name=f"{spec.name}/{factor}", packets_per_shard=spec.packets_per_shard // factor,
+                   n_sources=max(spec.n_super + 1, spec.n_sources // factor),
+                   n_super=max(1, spec.n_super // factor))
+
+
+def super_routing(spec: ShardedSpec):
+    """(cardinality, router list) of every planted super (host-side tables)."""
+    key = mix64_int(((spec.seed & 0xFFFFFFFF) << 8) | T_SHARD)
+    a, b = spec.routers
+    cards, routers = [], []
+    for s in range(spec.n_super):
+        d = [mix64_int((8 * s + t) ^ key) for t in range(3)]
+        m = min(spec.n_shards, a + d[0] % (b - a + 1))
+        c = 1024 + d[1] % (1023 * m - 1024 + 1)  # c ~ U[1024, 1023 m]: >= theta globally, <= 1023 per router
+        perm = sorted(range(spec.n_shards), key=lambda r: mix64_int((d[2] << 4) ^ r))
+        cards.append(c)
+        routers.append(perm[:m])
+    return np.array(cards, dtype=np.int64), routers
+
+
+def generate_shard(spec: ShardedSpec, shard: int, backend: str = "numpy", device=None):
+    """(hips, oips, supers) of one router's shard: exactly packets_per_shard pairs.
+
+    Background pairs of the global population go to router hash(pair) % n;
+    super s's j-th peer goes to routers_s[j % m_s]."""
+    xp = _NP() if backend == "numpy" else _Torch(device)
+    seed = spec.seed
+    sup_cards, routers = super_routing(spec)
+    total = spec.n_shards * spec.packets_per_shard
+    budget = int(total * spec.dup_p) - int(sup_cards.sum())
+    n_bg = spec.n_sources - spec.n_super
+    cards_h = np.concatenate([sup_cards, zipf_rank_size(n_bg, spec.zipf_s, spec.zipf_max, budget)])
+    n_src = spec.n_sources
+    src_ip = xp.perm32(xp.arange(n_src), mix64_int(seed ^ (T_SRC << 40)))
+    cards = xp.host(cards_h)
+    host_of = xp.repeat(xp.arange(n_src), cards)
+    starts = xp.cumsum(cards) - cards
+    n_edges = int(cards_h.sum())
+    eidx = xp.arange(n_edges)
+    rank = eidx - starts[host_of]
+    off = xp.draw(T_OFF, seed, host_of) & 0xFFFFFFFF
+    dst = xp.perm32((off + rank) & 0xFFFFFFFF, mix64_int(seed ^ (T_DST << 40)))
+    # router of every edge
+    m_h = np.array([len(r) for r in routers] + [1], dtype=np.int64)
+    tab_h = np.full((spec.n_super + 1, spec.n_shards), -1, dtype=np.int64)
+    for s, rs in enumerate(routers):
+        tab_h[s, : len(rs)] = rs
+    is_sup = host_of < spec.n_super
+    hs = host_of * is_sup + spec.n_super * (1 - is_sup * 1)  # row n_super = background
+    m = xp.host(m_h)[hs]
+    tab = xp.host(tab_h.reshape(-1))
+    sup_router = tab[hs * spec.n_shards + rank % m]
+    bg_router = xp.shr(xp.draw(T_SHARD, seed, eidx), 1) % spec.n_shards
+    router = sup_router * is_sup + bg_router * (1 - is_sup * 1)
+    mine = eidx[router == shard]
+    n_mine = int(mine.shape[0])
+    if n_mine > spec.packets_per_shard:
+        raise ValueError(f"{spec.name}: shard {shard} has {n_mine} pairs > {spec.packets_per_shard} packets")
+    sseed = seed * 131 + shard + 1
+    table = xp.host(geometric_table(spec.dup_p))
+    counts = 1 + xp.searchsorted_left(table, -xp.shr(xp.draw(T_DUP, sseed, mine), 11))
+    extra_pool = xp.repeat(mine, counts - 1)
+    need = spec.packets_per_shard - n_mine
+    pool_n = int(extra_pool.shape[0])
+    if pool_n >= need:
+        extra = extra_pool[xp.argsort(xp.shr(xp.draw(T_PICK, sseed, xp.arange(pool_n)), 1))[:need]]
+    else:
+        pad = mine[xp.shr(xp.draw(T_PAD, sseed, xp.arange(need - pool_n)), 1) % n_mine]
+        extra = xp.cat([extra_pool, pad])
+    edges = xp.cat([mine, extra])
+    order = xp.argsort(xp.shr(xp.draw(T_ORDER, sseed, xp.arange(spec.packets_per_shard)), 1))
+    stream = edges[order]
+    hips = src_ip[host_of[stream]]
+    oips = dst[stream]
+    supers = src_ip[: spec.n_super]
+    if backend == "numpy":
+        return hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32))
+    t = xp.t
+    to32 = lambda x: t.where(x >= 2**31, x - 2**32, x).to(t.int32)  # noqa: E731
+    return to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32))
