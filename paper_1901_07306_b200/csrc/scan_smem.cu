@@ -52,6 +52,18 @@ __device__ __forceinline__ uint64_t div_fast(uint64_t x, const sspd_divisor& dv)
   return (t + ((x - t) >> dv.sh1)) >> dv.sh2;
 }
 
+// Staging overflow (rare, skewed streams): re-apply every LDCA row of the
+// packet as a direct L2 red (exact: OR is idempotent).  Out of line so the
+// hot loop keeps its registers.
+__device__ __noinline__ void reapply_direct(const sspd_params& p, uint32_t lc_mask, uint32_t log2k, uint32_t hip,
+                                            uint32_t bb, uint32_t* ldca) {
+  for (uint32_t i = 0; i < p.lr; ++i) {
+    const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & lc_mask;
+    const uint32_t bit = ((i * p.lc + c) << log2k) | bb;
+    red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
+  }
+}
+
 constexpr uint32_t kThreads = 1024;
 constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile
 constexpr uint32_t kTile = kThreads * kPktPerThread;
@@ -72,7 +84,7 @@ struct PartPlan {
   uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w
 };
 
-// Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor]
+// Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor | sink]
 template <bool kSeav, bool kFast>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_partitioned_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
@@ -83,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* stage = smem + P.part_words;
   uint32_t* cnt = stage + (size_t)P.nparts * P.stage_slots;
   uint32_t* cursor = cnt + P.nparts;
+  uint32_t* sink = cursor + P.nparts;  // dummy target for overflowing staging writes
   cg::grid_group grid = cg::this_grid();
   const uint32_t self = blockIdx.x;
   const uint32_t tid = threadIdx.x;
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // of the low hash word and all index math is 32-bit.
               const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
               uint32_t cellbase = 0;
-              uint64_t ovf = 0;  // rows whose staging slot overflowed (rare)
+              bool ovf = false;  // some staging area was full (rare)
 #pragma unroll 8
               for (uint32_t i = 0; i < p.lr; ++i) {
                 const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
@@ -181,17 +194,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t local = w - q * P.part_words;
                 const uint32_t slot = atomicAdd(&cnt[q], 1u);
                 const bool fits = slot < P.stage_slots;
-                if (fits) stage[q * P.stage_slots + slot] = (local << 5) | (bit & 31u);
-                ovf |= (uint64_t)(!fits) << i;
+                ovf |= !fits;
+                // branch-free: an overflowing update is parked in a dummy word
+                *(fits ? &stage[q * P.stage_slots + slot] : sink) = (local << 5) | (bit & 31u);
                 cellbase += p.lc;
               }
-              while (ovf) {  // staging full: apply those rows directly (exact)
-                const uint32_t i = __ffsll((long long)ovf) - 1;
-                ovf &= ovf - 1;
-                const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
-                const uint32_t bit = ((i * p.lc + c) << P.log2k) | bb;
-                red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
-              }
+              if (ovf) reapply_direct(p, P.lc_mask, P.log2k, hip, bb, ldca);
             } else {
               const uint64_t bb = hash_range(oip, p.seed_h3, p.div_k);
               uint64_t cell = 0;
@@ -226,13 +234,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         // flush: one warp per destination; each run goes to this CTA's own
         // region of the destination bucket (no global atomics)
         for (uint32_t q = warp; q < np; q += nwarps) {
-          const uint32_t m = min(cnt[q], P.stage_slots);
-          if (m == 0) continue;
-          const uint32_t pos = cursor[q];
+          const uint32_t m0 = min(cnt[q], P.stage_slots);
+          if (m0 == 0) continue;
+          uint32_t* src = stage + q * P.stage_slots;
+          // pad the run to a multiple of 4 with copies of its last update
+          // (idempotent OR) so every copy below is an aligned 16-B store
+          const uint32_t m = (m0 + 3u) & ~3u;
+          if (lane < m - m0) src[m0 + lane] = src[m0 - 1];
+          __syncwarp();
+          const uint32_t pos = cursor[q];  // multiple of 4; region_cap multiple of 32
           const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
-          const uint32_t* src = stage + q * P.stage_slots;
-          uint32_t* dst = P.buckets + (((size_t)b * np + q) * np + self) * P.region_cap + pos;
-          for (uint32_t s = lane; s < fit; s += 32) __stcg(dst + s, src[s]);
+          uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (((size_t)b * np + q) * np + self) * P.region_cap + pos);
+          const uint4* src4 = reinterpret_cast<const uint4*>(src);
+          for (uint32_t s = lane; s < (fit >> 2); s += 32) __stcg(dst4 + s, src4[s]);
           for (uint32_t s = fit + lane; s < m; s += 32) {  // region full: direct (exact)
             const uint32_t u = src[s];
             red_or_g(ldca + (uint64_t)q * P.part_words + (u >> 5), 1u << (u & 31));
@@ -273,8 +287,8 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   P.part_words = (uint32_t)(((P.total_words + P.nparts - 1) / P.nparts + 3) & ~3ull);
   // staging: expected kTile*lr/nparts per destination per tile, + 6 sigma
   const double mean = (double)kTile * p->lr / P.nparts;
-  P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
-  smem = 4ull * (P.part_words + (uint64_t)P.nparts * P.stage_slots + 2ull * P.nparts);
+  P.stage_slots = ((uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0) + 3u) & ~3u;  // 16-B aligned rows
+  smem = 4ull * (P.part_words + (uint64_t)P.nparts * P.stage_slots + 2ull * P.nparts + 4);
   if ((int64_t)smem > max_smem || P.part_words >= (1u << 27)) return false;
   const uint64_t d = P.part_words;
   P.div_part.d = d;
