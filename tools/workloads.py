@@ -314,9 +314,16 @@ class ShardedSpec:
     zipf_max: int = 1000
     dup_p: float = 0.3
     seed: int = 3
+    super_log_range: tuple[int, int] | None = None
 
 
 CONFIG3 = ShardedSpec()
+# Config 5, one 300 s window: 8 routers x one 2^26-packet batch each; the
+# 4,096 supers are spread over the 8 windows (512 per window, log-uniform
+# cardinality 1,024 .. 2^20); 67,108,864 sources / 8 windows per window.
+CONFIG5_WINDOW = ShardedSpec(name="config5-window", n_shards=8, packets_per_shard=1 << 26, n_sources=8_388_608,
+                             n_super=512, routers=(1, 8), zipf_s=1.05, zipf_max=1000, dup_p=0.3, seed=5,
+                             super_log_range=(1024, 1 << 20))
 T_SHARD = 11
 
 
@@ -334,7 +341,12 @@ def super_routing(spec: ShardedSpec):
     for s in range(spec.n_super):
         d = [mix64_int((8 * s + t) ^ key) for t in range(3)]
         m = min(spec.n_shards, a + d[0] % (b - a + 1))
-        c = 1024 + d[1] % (1023 * m - 1024 + 1)  # c ~ U[1024, 1023 m]: >= theta globally, <= 1023 per router
+        if spec.super_log_range:  # config 5: log-uniform cardinality, any split
+            lo, hi = spec.super_log_range
+            u = (d[1] >> 11) / float(1 << 53)
+            c = int(min(hi, max(lo, math.floor(math.exp(math.log(lo) + u * (math.log(hi + 1) - math.log(lo)))))))
+        else:
+            c = 1024 + d[1] % (1023 * m - 1024 + 1)  # c ~ U[1024, 1023 m]: >= theta globally, <= 1023 per router
         perm = sorted(range(spec.n_shards), key=lambda r: mix64_int((d[2] << 4) ^ r))
         cards.append(c)
         routers.append(perm[:m])
