@@ -64,8 +64,11 @@ __device__ __noinline__ void reapply_direct(const sspd_params& p, uint32_t lc_ma
   }
 }
 
-constexpr uint32_t kThreads = 1024;
-constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile
+#ifndef SSPD_PART_THREADS
+#define SSPD_PART_THREADS 1024
+#endif
+constexpr uint32_t kThreads = SSPD_PART_THREADS;
+constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile (= one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPktPerThread;
 
 struct PartPlan {
@@ -82,6 +85,7 @@ struct PartPlan {
   // 32-bit fast path (k, lc powers of two, < 2^32 LDCA bits)
   uint32_t k_mask, lc_mask, log2k;
   uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w
+  uint32_t vec_ok;         // hips/oips 16-byte aligned and chunk % 4 == 0
 };
 
 // Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor | sink]
@@ -151,31 +155,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = (uint32_t)(t & 1);
       const uint64_t c0 = t * P.chunk;
       const uint64_t c1 = min(P.n, c0 + P.chunk);
-      const uint64_t per = (c1 - c0 + gridDim.x - 1) / gridDim.x;
+      // slices are whole multiples of 4 packets so 16-byte loads stay aligned
+      const uint64_t per = (((c1 - c0 + gridDim.x - 1) / gridDim.x) + 3) & ~3ull;
       const uint64_t lo = min(c1, c0 + per * self);
       const uint64_t hi = min(c1, lo + per);
       // software pipeline: the next tile's (hip, oip) are loaded into
       // registers while the current tile is hashed and flushed
-      uint32_t nh[kPktPerThread], no[kPktPerThread];
+      // thread tid owns the kPktPerThread consecutive packets base + 4 tid + e,
+      // fetched with one 16-byte load per array when the slice is aligned
+      auto fetch = [&](uint64_t first, uint32_t* h, uint32_t* o) {
+        if (P.vec_ok && first + kPktPerThread <= hi) {
+          const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(hips + first));
+          const uint4 ov = __ldcs(reinterpret_cast<const uint4*>(oips + first));
+          h[0] = hv.x, h[1] = hv.y, h[2] = hv.z, h[3] = hv.w;
+          o[0] = ov.x, o[1] = ov.y, o[2] = ov.z, o[3] = ov.w;
+        } else {
 #pragma unroll
-      for (uint32_t e = 0; e < kPktPerThread; ++e) {
-        const uint64_t j = lo + e * kThreads + tid;
-        nh[e] = j < hi ? __ldcs(hips + j) : 0u;
-        no[e] = j < hi ? __ldcs(oips + j) : 0u;
-      }
+          for (uint32_t e = 0; e < kPktPerThread; ++e) {
+            h[e] = first + e < hi ? __ldcs(hips + first + e) : 0u;
+            o[e] = first + e < hi ? __ldcs(oips + first + e) : 0u;
+          }
+        }
+      };
+      uint32_t nh[kPktPerThread], no[kPktPerThread];
+      fetch(lo + (uint64_t)tid * kPktPerThread, nh, no);
       for (uint64_t base = lo; base < hi; base += kTile) {
         uint32_t ch[kPktPerThread], co[kPktPerThread];
 #pragma unroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
           ch[e] = nh[e];
           co[e] = no[e];
-          const uint64_t jn = base + kTile + e * kThreads + tid;
-          nh[e] = jn < hi ? __ldcs(hips + jn) : 0u;
-          no[e] = jn < hi ? __ldcs(oips + jn) : 0u;
         }
+        fetch(base + kTile + (uint64_t)tid * kPktPerThread, nh, no);
 #pragma unroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
-          const uint64_t j = base + e * kThreads + tid;
+          const uint64_t j = base + (uint64_t)tid * kPktPerThread + e;
           if (j < hi) {
             const uint32_t hip = ch[e], oip = co[e];
             if (kFast) {
@@ -351,6 +365,10 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
   if (!plan_partitioned(p, n, chunk, sms, max_smem, P, smem, need)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
   P.buckets = static_cast<uint32_t*>(scratch);
+  P.vec_ok = (((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) == 0 &&
+              (P.chunk & 3u) == 0)
+                 ? 1u
+                 : 0u;
   P.counts = P.buckets + 2ull * P.nparts * P.nparts * P.region_cap;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool fast = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0 && bits_fit32(p);
