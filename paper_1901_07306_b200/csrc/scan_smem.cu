@@ -67,7 +67,15 @@ __device__ __noinline__ void reapply_direct(const sspd_params& p, uint32_t lc_ma
 #ifndef SSPD_PART_THREADS
 #define SSPD_PART_THREADS 1024
 #endif
+#ifndef SSPD_E_UNROLL  // packets of a thread's quad processed per unrolled body
+#define SSPD_E_UNROLL 4
+#endif
+#ifndef SSPD_ROW_UNROLL  // LDCA rows per unrolled body
+#define SSPD_ROW_UNROLL 8
+#endif
 constexpr uint32_t kThreads = SSPD_PART_THREADS;
+constexpr int kEUnroll = SSPD_E_UNROLL;
+constexpr int kRowUnroll = SSPD_ROW_UNROLL;
 constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile (= one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPktPerThread;
 
@@ -187,18 +195,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           co[e] = no[e];
         }
         fetch(base + kTile + (uint64_t)tid * kPktPerThread, nh, no);
-#pragma unroll
+#pragma unroll kEUnroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
           const uint64_t j = base + (uint64_t)tid * kPktPerThread + e;
+          const uint32_t hip = ch[e], oip = co[e];
           if (j < hi) {
-            const uint32_t hip = ch[e], oip = co[e];
             if (kFast) {
               // k, lc powers of two and < 2^32 LDCA bits: the modulo is a mask
               // of the low hash word and all index math is 32-bit.
               const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
               uint32_t cellbase = 0;
               bool ovf = false;  // some staging area was full (rare)
-#pragma unroll 8
+#pragma unroll kRowUnroll
               for (uint32_t i = 0; i < p.lr; ++i) {
                 const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
                 const uint32_t bit = ((cellbase + c) << P.log2k) | bb;
