@@ -33,6 +33,7 @@
 // of the LDCA, c_i = LH_i(hip) % lc, b = H3(oip) % k (long_sketch.py:125-135),
 // and the SEAV update of short_sketch.py:300-318.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "sspd_common.cuh"
 #include "launch.cuh"
@@ -64,40 +65,52 @@ __device__ __noinline__ void reapply_direct(const sspd_params& p, uint32_t lc_ma
   }
 }
 
+
 #ifndef SSPD_PART_THREADS
 #define SSPD_PART_THREADS 1024
 #endif
-#ifndef SSPD_E_UNROLL  // packets of a thread's quad processed per unrolled body
-#define SSPD_E_UNROLL 4
-#endif
-#ifndef SSPD_ROW_UNROLL  // LDCA rows per unrolled body
-#define SSPD_ROW_UNROLL 8
-#endif
 constexpr uint32_t kThreads = SSPD_PART_THREADS;
-constexpr int kEUnroll = SSPD_E_UNROLL;
-constexpr int kRowUnroll = SSPD_ROW_UNROLL;
 constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile (= one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPktPerThread;
 
+// Producer routing modes, chosen per launch by the host plan:
+//   kGeneric  64-bit index math, any k / lc (exact 64-bit modulo)
+//   kFast32   k, lc powers of two, < 2^32 LDCA bits; partition = magic division
+//   kPow2     kFast32 + power-of-two partitions + LR = 8 unrolled with static
+//             seeds: q = bit >> pshift, staged entry = bit & pmask
+enum : int { kGeneric = 0, kFast32 = 1, kPow2 = 2 };
+
 struct PartPlan {
-  uint32_t nparts;        // = gridDim.x (producers == consumers)
+  uint32_t nparts;        // consumers = partitions (CTAs 0 .. nparts-1)
+  uint32_t nsrc;          // producers = gridDim.x (>= nparts)
   uint32_t part_words;    // words per partition (last one may be shorter)
-  uint64_t total_words;   // LDCA words (ceil(bits / 32))
-  sspd_divisor div_part;  // divisor by part_words
   uint32_t stage_slots;   // staging slots per destination per tile
+  uint64_t total_words;   // LDCA words (ceil(bits / 32))
+  sspd_divisor div_part;  // divisor by part_words (generic mode)
   uint32_t region_cap;    // entries per (src, dst) region per chunk
+  uint32_t w_owner, w_other;  // producer slice weights (consumers vs pure producers)
   uint64_t chunk;         // packets per chunk
   uint64_t n;             // packets
   uint32_t* buckets;      // [2][dst][src][region_cap]
   uint32_t* counts;       // [2][dst][src]
-  // 32-bit fast path (k, lc powers of two, < 2^32 LDCA bits)
   uint32_t k_mask, lc_mask, log2k;
-  uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w
+  uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w (fast mode)
+  uint32_t pshift, pmask;  // pow2 mode: partition of a bit index / its local bit
   uint32_t vec_ok;         // hips/oips 16-byte aligned and chunk % 4 == 0
 };
 
+// Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
+// take w_other/w_owner as much as consumer CTAs; boundaries are 4-aligned.
+__device__ __forceinline__ uint64_t slice_start(const PartPlan& P, uint64_t c0, uint64_t c1, uint32_t s) {
+  if (s >= P.nsrc) return c1;
+  const uint64_t tw = (uint64_t)P.nparts * P.w_owner + (uint64_t)(P.nsrc - P.nparts) * P.w_other;
+  const uint64_t cw = (uint64_t)min(s, P.nparts) * P.w_owner + (uint64_t)(s > P.nparts ? s - P.nparts : 0) * P.w_other;
+  const uint64_t off = (((c1 - c0) * cw) / tw) & ~3ull;
+  return min(c1, c0 + off);
+}
+
 // Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor | sink]
-template <bool kSeav, bool kFast>
+template <bool kSeav, int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_partitioned_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
                             const __grid_constant__ sspd_params p, const __grid_constant__ PartPlan P,
@@ -113,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = kThreads >> 5;
   const uint32_t tmask = tau_mask(p.tau);
-  const uint32_t np = P.nparts;
+  const uint32_t np = P.nparts, ns = P.nsrc;
+  const bool owner = self < np;
 
   for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
   for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = cursor[i] = 0;
@@ -123,11 +137,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint64_t k = p.k;
   for (uint64_t t = 0; t <= nchunks; ++t) {
     // ---------------- consume chunk t-1 into the shared partition --------
-    if (t >= 1) {
+    if (t >= 1 && owner) {
       const uint32_t b = (uint32_t)((t - 1) & 1);
-      const uint32_t* cnts = P.counts + ((size_t)b * np + self) * np;
-      const uint32_t* regions = P.buckets + ((size_t)b * np + self) * (size_t)np * P.region_cap;
-      for (uint32_t src = warp; src < np; src += nwarps) {
+      const uint32_t* cnts = P.counts + ((size_t)b * np + self) * ns;
+      const uint32_t* regions = P.buckets + ((size_t)b * np + self) * (size_t)ns * P.region_cap;
+      for (uint32_t src = warp; src < ns; src += nwarps) {
         const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
         const uint32_t* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
         const uint32_t m4 = m >> 2;
@@ -163,14 +177,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = (uint32_t)(t & 1);
       const uint64_t c0 = t * P.chunk;
       const uint64_t c1 = min(P.n, c0 + P.chunk);
-      // slices are whole multiples of 4 packets so 16-byte loads stay aligned
-      const uint64_t per = (((c1 - c0 + gridDim.x - 1) / gridDim.x) + 3) & ~3ull;
-      const uint64_t lo = min(c1, c0 + per * self);
-      const uint64_t hi = min(c1, lo + per);
-      // software pipeline: the next tile's (hip, oip) are loaded into
-      // registers while the current tile is hashed and flushed
-      // thread tid owns the kPktPerThread consecutive packets base + 4 tid + e,
-      // fetched with one 16-byte load per array when the slice is aligned
+      const uint64_t lo = slice_start(P, c0, c1, self);
+      const uint64_t hi = slice_start(P, c0, c1, self + 1);
+      // software pipeline: thread tid owns the kPktPerThread consecutive
+      // packets base + 4 tid + e, fetched one tile ahead with one 16-byte
+      // load per array when the slice is aligned
       auto fetch = [&](uint64_t first, uint32_t* h, uint32_t* o) {
         if (P.vec_ok && first + kPktPerThread <= hi) {
           const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(hips + first));
@@ -195,18 +206,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           co[e] = no[e];
         }
         fetch(base + kTile + (uint64_t)tid * kPktPerThread, nh, no);
-#pragma unroll kEUnroll
+#pragma unroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
           const uint64_t j = base + (uint64_t)tid * kPktPerThread + e;
           const uint32_t hip = ch[e], oip = co[e];
           if (j < hi) {
-            if (kFast) {
+            if (kMode == kPow2) {
+              // LR = 8, k and lc powers of two, partitions of 2^pshift bits:
+              // the staged entry is the bit index inside its partition
+              const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
+              bool ovf = false;
+#pragma unroll
+              for (uint32_t i = 0; i < 8; ++i) {
+                const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
+                const uint32_t bit = ((i * p.lc + c) << P.log2k) | bb;
+                const uint32_t q = bit >> P.pshift;
+                const uint32_t slot = atomicAdd(&cnt[q], 1u);
+                const bool fits = slot < P.stage_slots;
+                ovf |= !fits;
+                *(fits ? &stage[q * P.stage_slots + slot] : sink) = bit & P.pmask;
+              }
+              if (ovf) reapply_direct(p, P.lc_mask, P.log2k, hip, bb, ldca);
+            } else if (kMode == kFast32) {
               // k, lc powers of two and < 2^32 LDCA bits: the modulo is a mask
               // of the low hash word and all index math is 32-bit.
               const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
               uint32_t cellbase = 0;
               bool ovf = false;  // some staging area was full (rare)
-#pragma unroll kRowUnroll
+#pragma unroll 8
               for (uint32_t i = 0; i < p.lr; ++i) {
                 const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
                 const uint32_t bit = ((cellbase + c) << P.log2k) | bb;
@@ -266,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           const uint32_t pos = cursor[q];  // multiple of 4; region_cap multiple of 32
           const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
-          uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (((size_t)b * np + q) * np + self) * P.region_cap + pos);
+          uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (((size_t)b * np + q) * ns + self) * P.region_cap + pos);
           const uint4* src4 = reinterpret_cast<const uint4*>(src);
           for (uint32_t s = lane; s < (fit >> 2); s += 32) __stcg(dst4 + s, src4[s]);
           for (uint32_t s = fit + lane; s < m; s += 32) {  // region full: direct (exact)
@@ -283,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // publish this CTA's run lengths for chunk t and reset the cursors
       for (uint32_t q = tid; q < np; q += kThreads) {
-        __stcg(P.counts + ((size_t)b * np + q) * np + self, cursor[q]);
+        __stcg(P.counts + ((size_t)b * np + q) * ns + self, cursor[q]);
         cursor[q] = 0;
       }
     }
@@ -291,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // fold the shared partition into the global LDCA (after the last barrier
   // no direct reds are in flight, so plain read-modify-write is exact)
+  if (!owner) return;
   __syncthreads();
   const uint64_t w0 = (uint64_t)self * P.part_words;
   for (uint32_t i = tid; i < P.part_words; i += kThreads) {
@@ -301,17 +329,56 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 static bool bits_fit32(const sspd_params* p) { return (uint64_t)p->lr * p->lc * p->k <= 0xFFFFFFFFull; }
 
+static uint32_t ilog2_ceil(uint64_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  return l;
+}
+
 static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int max_smem,
-                             PartPlan& P, uint64_t& smem, uint64_t& scratch) {
+                             PartPlan& P, uint64_t& smem, uint64_t& scratch, int& mode) {
   const uint64_t bits = (uint64_t)p->lr * p->lc * p->k;
-  P.nparts = (uint32_t)sms;
+  const bool pow2_kl = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0 && bits_fit32(p);
   P.total_words = (bits + 31) / 32;
-  P.part_words = (uint32_t)(((P.total_words + P.nparts - 1) / P.nparts + 3) & ~3ull);
-  // staging: expected kTile*lr/nparts per destination per tile, + 6 sigma
-  const double mean = (double)kTile * p->lr / P.nparts;
-  P.stage_slots = ((uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0) + 3u) & ~3u;  // 16-B aligned rows
-  smem = 4ull * (P.part_words + (uint64_t)P.nparts * P.stage_slots + 2ull * P.nparts + 4);
-  if ((int64_t)smem > max_smem || P.part_words >= (1u << 27)) return false;
+  P.nsrc = (uint32_t)sms;
+  auto staging = [&](uint32_t nparts) {
+    // expected kTile*lr/nparts per destination per tile + 3-4 sigma, 16-B rows
+    const double mean = (double)kTile * p->lr / nparts;
+    const double sig = nparts < (uint32_t)sms ? 3.0 : 4.0;
+    return ((uint32_t)(mean + sig * __builtin_sqrt(mean) + 8.0) + 3u) & ~3u;
+  };
+  auto fits = [&](uint32_t nparts, uint32_t pw, uint32_t slots) {
+    smem = 4ull * (pw + (uint64_t)nparts * slots + 2ull * nparts + 4);
+    return (int64_t)smem <= max_smem && pw < (1u << 27);
+  };
+  mode = pow2_kl ? kFast32 : kGeneric;
+  // power-of-two partitions when the LDCA word count is a power of two
+  // and the largest power-of-two partition count <= SMs fits in smem
+  const uint64_t tw = P.total_words;
+  if (pow2_kl && p->lr == 8 && (tw & (tw - 1)) == 0 && getenv("SSPD_PART_NOPOW2") == nullptr) {
+    uint32_t np2 = 1;
+    while ((uint64_t)np2 * 2 <= (uint64_t)sms) np2 *= 2;
+    if (tw >= np2) {
+      const uint32_t pw = (uint32_t)(tw / np2);
+      const uint32_t slots = staging(np2);
+      if (fits(np2, pw, slots)) {
+        mode = kPow2;
+        P.nparts = np2;
+        P.part_words = pw;
+        P.stage_slots = slots;
+        P.pshift = ilog2_ceil(pw) + 5;
+        P.pmask = (uint32_t)((uint64_t)pw * 32 - 1);
+      }
+    }
+  }
+  if (mode != kPow2) {
+    P.nparts = (uint32_t)sms;
+    P.part_words = (uint32_t)(((tw + P.nparts - 1) / P.nparts + 3) & ~3ull);
+    P.stage_slots = staging(P.nparts);
+    if (!fits(P.nparts, P.part_words, P.stage_slots)) return false;
+    P.pshift = 0;
+    P.pmask = 0;
+  }
   const uint64_t d = P.part_words;
   P.div_part.d = d;
   P.div_part.pad_ = 0;
@@ -320,32 +387,34 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
     P.div_part.magic = 0;
     P.div_part.sh1 = P.div_part.sh2 = 0;
   } else {
-    uint32_t l = 0;
-    while ((1ull << l) < d) ++l;
+    const uint32_t l = ilog2_ceil(d);
     const unsigned __int128 num = ((unsigned __int128)1 << 64) * (((unsigned __int128)1 << l) - d);
     P.div_part.magic = (uint64_t)(num / d) + 1;
     P.div_part.sh1 = 1;
     P.div_part.sh2 = l - 1;
     P.div_part.pow2 = 0;
   }
-  // default chunk: 4 full tiles per CTA, so every producer slice is whole tiles
-  P.chunk = chunk ? chunk : (uint64_t)P.nparts * kTile * 4;
-  const double rmean = (double)P.chunk * p->lr / ((double)P.nparts * P.nparts);
-  P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
-  P.region_cap = (P.region_cap + 31u) & ~31u;
-  P.n = n;
-  scratch = 4ull * (2ull * P.nparts * P.nparts * P.region_cap + 2ull * P.nparts * P.nparts);
-  // 32-bit division by part_words (Granlund-Montgomery, N = 32)
-  {
-    uint32_t l = 0;
-    while ((1ull << l) < d) ++l;
+  {  // 32-bit division by part_words (Granlund-Montgomery, N = 32)
+    const uint32_t l = ilog2_ceil(d);
     P.magic32 = (d & (d - 1)) == 0 ? 0u : (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
     P.sh32 = l - 1;
   }
+  // pure producers (no partition) take a larger slice: consumers also drain
+  // their buckets.  Weight ratio (x64) tunable with SSPD_PART_WEIGHT.
+  P.w_owner = 64;
+  P.w_other = 76;
+  if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
+  // default chunk: 4 tiles per producer, so slices are (nearly) whole tiles
+  P.chunk = chunk ? chunk : (uint64_t)P.nsrc * kTile * 4;
+  const double share = (double)P.w_other / ((double)P.nparts * P.w_owner + (double)(P.nsrc - P.nparts) * P.w_other);
+  const double rmean = (double)P.chunk * p->lr * share / P.nparts;  // largest producer -> one destination
+  P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
+  P.region_cap = (P.region_cap + 31u) & ~31u;
+  P.n = n;
+  scratch = 4ull * (2ull * P.nparts * P.nsrc * P.region_cap + 2ull * P.nparts * P.nsrc);
   P.k_mask = p->k - 1;
   P.lc_mask = p->lc - 1;
-  P.log2k = 0;
-  while ((1u << P.log2k) < p->k) ++P.log2k;
+  P.log2k = ilog2_ceil(p->k);
   return true;
 }
 
@@ -370,18 +439,25 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
   if (!coop) return SSPD_ERR_CONFIG;
   PartPlan P;
   uint64_t smem = 0, need = 0;
-  if (!plan_partitioned(p, n, chunk, sms, max_smem, P, smem, need)) return SSPD_ERR_CONFIG;
+  int mode = kGeneric;
+  if (!plan_partitioned(p, n, chunk, sms, max_smem, P, smem, need, mode)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
   P.buckets = static_cast<uint32_t*>(scratch);
+  P.counts = P.buckets + 2ull * P.nparts * P.nsrc * P.region_cap;
   P.vec_ok = (((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) == 0 &&
               (P.chunk & 3u) == 0)
                  ? 1u
                  : 0u;
-  P.counts = P.buckets + 2ull * P.nparts * P.nparts * P.region_cap;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool fast = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0 && bits_fit32(p);
-  void* kern = seav ? (fast ? (void*)scan_partitioned_kernel<true, true> : (void*)scan_partitioned_kernel<true, false>)
-                    : (fast ? (void*)scan_partitioned_kernel<false, true> : (void*)scan_partitioned_kernel<false, false>);
+  void* kern = nullptr;
+  if (seav)
+    kern = mode == kPow2 ? (void*)scan_partitioned_kernel<true, kPow2>
+                         : (mode == kFast32 ? (void*)scan_partitioned_kernel<true, kFast32>
+                                            : (void*)scan_partitioned_kernel<true, kGeneric>);
+  else
+    kern = mode == kPow2 ? (void*)scan_partitioned_kernel<false, kPow2>
+                         : (mode == kFast32 ? (void*)scan_partitioned_kernel<false, kFast32>
+                                            : (void*)scan_partitioned_kernel<false, kGeneric>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
@@ -392,7 +468,7 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
   uint32_t* sv = reinterpret_cast<uint32_t*>(seav);
   uint32_t* lv = reinterpret_cast<uint32_t*>(ldca);
   void* args[] = {(void*)&h, (void*)&o, (void*)&pv, (void*)&P, (void*)&sv, (void*)&lv};
-  if (cudaLaunchCooperativeKernel(kern, dim3(P.nparts), dim3(kThreads), args, smem, st) != cudaSuccess) {
+  if (cudaLaunchCooperativeKernel(kern, dim3(P.nsrc), dim3(kThreads), args, smem, st) != cudaSuccess) {
     cudaGetLastError();
     return SSPD_ERR_CUDA;
   }
@@ -413,6 +489,7 @@ extern "C" uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t
   }
   PartPlan P;
   uint64_t smem = 0, need = 0;
-  if (!plan_partitioned(p, 1, chunk, sms, max_smem, P, smem, need)) return 0;
+  int mode = 0;
+  if (!plan_partitioned(p, 1, chunk, sms, max_smem, P, smem, need, mode)) return 0;
   return need;
 }
