@@ -240,6 +240,18 @@ SSPD_API int sspd_ipc_open(const uint8_t* handle /* 64 B */, void** ptr);
 SSPD_API int sspd_ipc_close(void* ptr);
 SSPD_API int sspd_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 
+/* ---- ingest and frames ---------------------------------
+ * sspd_unpack_records: the reference trace format, n little-endian 12-byte
+ * records (slice u32, hip u32, oip u32) (evaluation.py:21, read_trace
+ * :235-254), into SoA device arrays; slices may be NULL.
+ * sspd_crc32: zlib.crc32 of a device buffer (the frame checksum of
+ * serialize/parse_frame, distributed.py:81-126); scratch NULL queries
+ * *scratch_bytes; *out (device uint32) receives the CRC. */
+SSPD_API int sspd_unpack_records(const uint8_t* records, uint64_t n, uint32_t* slices,
+                                 uint32_t* hips, uint32_t* oips, void* stream);
+SSPD_API int sspd_crc32(const uint8_t* data, uint64_t n, uint32_t* out, void* scratch,
+                        uint64_t* scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

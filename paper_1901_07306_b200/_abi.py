@@ -122,6 +122,8 @@ _SIGS = {
     "sspd_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(_VP)]),
     "sspd_ipc_close": (C.c_int, [_VP]),
     "sspd_copy_async": (C.c_int, [_VP, _VP, _U64, _VP]),
+    "sspd_unpack_records": (C.c_int, [_VP, _U64, _VP, _VP, _VP, _VP]),
+    "sspd_crc32": (C.c_int, [_VP, _U64, _VP, _VP, C.POINTER(_U64), _VP]),
 }
 
 _lib = None
