@@ -252,6 +252,19 @@ SSPD_API int sspd_unpack_records(const uint8_t* records, uint64_t n, uint32_t* s
 SSPD_API int sspd_crc32(const uint8_t* data, uint64_t n, uint32_t* out, void* scratch,
                         uint64_t* scratch_bytes, void* stream);
 
+/* ---- exact oracle --------------------------------
+ * Replaces ExactOracle.__init__ (evaluation.py:35-40): sort-unique of the
+ * keys (hip << 32 | oip), then distinct keys counted per host.  Writes the
+ * hosts ascending to hosts_out and their distinct-peer counts to
+ * counts_out (both sized n by the caller: at most n hosts), and the host
+ * count to *n_hosts_out (device).  scratch NULL queries *scratch_bytes
+ * (about 24 B per packet).  n < 2^31.  Evaluation infrastructure, not on
+ * the scan path. */
+SSPD_API int sspd_exact_cardinalities(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                      uint32_t* hosts_out, uint32_t* counts_out,
+                                      unsigned long long* n_hosts_out, void* scratch,
+                                      size_t* scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

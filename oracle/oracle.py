@@ -160,3 +160,13 @@ def cpu_threads() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def exact_cardinalities(hips, oips) -> tuple[np.ndarray, np.ndarray]:
+    """ExactOracle.__init__ (evaluation.py:35-40) restated with numpy:
+    sort-unique of (hip << 32 | oip), then distinct keys per host.
+    Returns (hosts uint32 ascending, counts int64)."""
+    key = (_u32(hips).astype(np.uint64) << np.uint64(32)) | _u32(oips).astype(np.uint64)
+    distinct = np.unique(key)
+    hosts, counts = np.unique(distinct >> np.uint64(32), return_counts=True)
+    return hosts.astype(np.uint32), counts.astype(np.int64)

@@ -342,6 +342,55 @@ def frames_case():
             "sim_ldca_sha": sha(sim.global_ldca.payload_bytes())}
 
 
+def exact_case():
+    """ExactOracle / metrics (evaluation.py:32-97) on a small skewed stream
+    (raw arrays) and on the config-1 stream (hashes + truth + metrics)."""
+    from sspd.evaluation import ExactOracle, metrics_report
+
+    rng = np.random.default_rng(9)
+    pool_h = rng.integers(0, 2**32, size=300, dtype=np.uint64)
+    hips = pool_h[rng.integers(0, 300, size=20000)]
+    oips = rng.integers(0, 5000, size=20000, dtype=np.uint64) * np.uint64(7919)
+    hips[:4000] = pool_h[0]                      # one heavy host
+    hips[4000:4100] = 0xFFFFFFFF                 # extreme keys
+    oips[4000:4100] = np.arange(100) % 37
+    hips[4100:4150] = 0
+    oips[4100:4150] = 0xFFFFFFFF
+    ex = ExactOracle(hips, oips)
+    small = {"hips": put("exact/hips", hips.astype(np.uint32)), "oips": put("exact/oips", oips.astype(np.uint32)),
+             "hosts": put("exact/hosts", ex.hosts), "counts": put("exact/counts", ex.counts),
+             "super_64": ex.superpoints(64)}
+    c_hips, c_oips, supers = generate(CONFIG1)
+    ex1 = ExactOracle(c_hips, c_oips)
+    st = DetectorState.create(DetectorParams())
+    for lo in range(0, len(c_hips), 1 << 16):
+        st.process_batch(c_hips[lo:lo + (1 << 16)], c_oips[lo:lo + (1 << 16)])
+    det = [r.ip for r in st.finalize_window()]
+    truth = ex1.superpoints(1024)
+    cfg1 = {"n_hosts": int(len(ex1.hosts)), "hosts_sha": sha(ex1.hosts.astype(np.uint32).tobytes()),
+            "counts_sha": sha(ex1.counts.astype(np.int64).tobytes()), "truth_1024": truth,
+            "max_count": int(ex1.counts.max()), "total_distinct": int(ex1.counts.sum()),
+            "metrics": {k: repr(v) for k, v in metrics_report(det, truth).items()}}
+    kats = []
+    for det_k, truth_k in (([1, 2, 3], [2, 3, 4, 5]), ([], [7]), ([9, 9, 8], [8]), ([1], [1])):
+        kats.append([det_k, truth_k, {k: repr(v) for k, v in metrics_report(det_k, truth_k).items()}])
+    return {"small": small, "config1": cfg1, "metric_kats": kats}
+
+
+def update(keys):
+    """Recompute only the named cases into the existing fixtures."""
+    golden = json.loads((HERE / "golden.json").read_text())
+    ARR.update(dict(np.load(HERE / "golden.npz")))
+    for key in keys:
+        golden[key] = CASES[key]()
+    (HERE / "golden.json").write_text(json.dumps(golden, indent=None, separators=(",", ":")))
+    np.savez_compressed(HERE / "golden.npz", **ARR)
+    print("updated", keys)
+
+
+CASES = {}
+
+
 def main():
     golden = {
         "generator": "tests/golden/make_golden.py (reference sspd 0.1.0 from /root/reference/pkg/src)",
@@ -355,6 +404,7 @@ def main():
         "merge_pools": merge_pools_case(),
         "route": route_case(),
         "frames": frames_case(),
+        "exact": exact_case(),
     }
     (HERE / "golden.json").write_text(json.dumps(golden, indent=None, separators=(",", ":")))
     np.savez_compressed(HERE / "golden.npz", **ARR)
@@ -362,5 +412,10 @@ def main():
           HERE / "golden.npz", (HERE / "golden.npz").stat().st_size, "bytes")
 
 
+CASES.update(exact=exact_case, frames=frames_case, route=route_case)
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[1] == "--update":
+        update(sys.argv[2:])
+    else:
+        main()

@@ -170,3 +170,32 @@ def test_route_hash(oracle, golden, garr):
     for n_wp in (1, 3, 7, 8, 16):
         lanes = oracle.route_hash(garr[g["hips"]], garr[g["oips"]], SeedFamily().route.value, n_wp)
         assert (lanes == garr[g[f"hash_{n_wp}"]]).all()
+
+
+def test_exact_cardinalities_oracle(oracle, golden, garr):
+    """Numpy ExactOracle restatement vs the reference's (evaluation.py:32-58)."""
+    from tools.workloads import CONFIG1, generate
+
+    g = golden["exact"]
+    hosts, counts = oracle.exact_cardinalities(garr["exact/hips"], garr["exact/oips"])
+    assert (hosts == garr["exact/hosts"]).all() and (counts == garr["exact/counts"]).all()
+    assert [int(h) for h in hosts[counts >= 64]] == g["small"]["super_64"]
+    hips, oips, _ = generate(CONFIG1)
+    hosts, counts = oracle.exact_cardinalities(hips, oips)
+    c = g["config1"]
+    assert len(hosts) == c["n_hosts"] and sha(hosts.tobytes()) == c["hosts_sha"]
+    assert sha(counts.astype(np.int64).tobytes()) == c["counts_sha"]
+    assert [int(h) for h in hosts[counts >= 1024]] == c["truth_1024"]
+
+
+def test_metrics_host_logic(golden):
+    """FPR/FNR/FTR normalised by |truth| (evaluation.py:73-97): the host
+    arithmetic of the drop-in module against the reference's values."""
+    from paper_1901_07306_b200 import UndefinedMetricError, metrics, metrics_report
+
+    for det, truth, want in golden["exact"]["metric_kats"]:
+        got = metrics_report(det, truth)
+        assert {k: repr(v) for k, v in got.items()} == want
+        assert metrics(det, truth) == (got["fpr"], got["fnr"], got["ftr"])
+    with pytest.raises(UndefinedMetricError):
+        metrics([1, 2], [])
