@@ -97,6 +97,8 @@ struct PartPlan {
   uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w (fast mode)
   uint32_t pshift, pmask;  // pow2 mode: partition of a bit index / its local bit
   uint32_t vec_ok;         // hips/oips 16-byte aligned and chunk % 4 == 0
+  uint32_t qstride;        // ns * region_cap: bucket elements per destination
+  uint32_t gshift;         // log2 of the flush group size (threads per destination)
 };
 
 // Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
@@ -141,8 +143,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = (uint32_t)((t - 1) & 1);
       const uint32_t* cnts = P.counts + ((size_t)b * np + self) * ns;
       const uint32_t* regions = P.buckets + ((size_t)b * np + self) * (size_t)ns * P.region_cap;
-      for (uint32_t src = warp; src < ns; src += nwarps) {
-        const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
+      // warp w drains sources w, w+32, ...: fetch all of its run lengths at
+      // once (lane j holds source w+32j) so no region waits on its count
+      const uint32_t my_src = warp + 32u * lane;
+      const uint32_t my_cnt = my_src < ns ? min(__ldcg(cnts + my_src), P.region_cap) : 0u;
+      for (uint32_t src = warp, j = 0; src < ns; src += nwarps, ++j) {
+        const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
         const uint32_t* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
         const uint32_t m4 = m >> 2;
         const uint4* r4 = reinterpret_cast<const uint4*>(reg);
@@ -161,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        for (uint32_t j = (m4 << 2) + lane; j < m; j += 32) {
-          const uint32_t u = __ldcg(reg + j);
+        for (uint32_t jj = (m4 << 2) + lane; jj < m; jj += 32) {
+          const uint32_t u = __ldcg(reg + jj);
           atomicOr(&part[u >> 5], 1u << (u & 31));
         }
         // the region is dead once read: drop its L2 lines without write-back
@@ -280,30 +286,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncthreads();
-        // flush: one warp per destination; each run goes to this CTA's own
-        // region of the destination bucket (no global atomics)
-        for (uint32_t q = warp; q < np; q += nwarps) {
-          const uint32_t m0 = min(cnt[q], P.stage_slots);
-          if (m0 == 0) continue;
-          uint32_t* src = stage + q * P.stage_slots;
-          // pad the run to a multiple of 4 with copies of its last update
-          // (idempotent OR) so every copy below is an aligned 16-B store
-          const uint32_t m = (m0 + 3u) & ~3u;
-          if (lane < m - m0) src[m0 + lane] = src[m0 - 1];
-          __syncwarp();
-          const uint32_t pos = cursor[q];  // multiple of 4; region_cap multiple of 32
-          const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
-          uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (((size_t)b * np + q) * ns + self) * P.region_cap + pos);
-          const uint4* src4 = reinterpret_cast<const uint4*>(src);
-          for (uint32_t s = lane; s < (fit >> 2); s += 32) __stcg(dst4 + s, src4[s]);
-          for (uint32_t s = fit + lane; s < m; s += 32) {  // region full: direct (exact)
-            const uint32_t u = src[s];
-            red_or_g(ldca + (uint64_t)q * P.part_words + (u >> 5), 1u << (u & 31));
-          }
-          __syncwarp();
-          if (lane == 0) {
-            cursor[q] = pos + fit;
-            cnt[q] = 0;
+        // flush: a group of G = 2^gshift threads per destination (8 when
+        // there are 128 destinations) copies the run as aligned 16-B stores
+        // into this CTA's own region of the destination bucket (no global
+        // atomics).  The loop is warp-uniform so __syncwarp is safe.
+        {
+          const uint32_t gs = P.gshift, G = 1u << gs, gl = tid & (G - 1u);
+          const uint32_t boff = (uint32_t)b * np * P.qstride + self * P.region_cap;
+          for (uint32_t q0 = 0; q0 < np; q0 += (kThreads >> gs)) {
+            const uint32_t q = q0 + (tid >> gs);
+            const bool act = q < np;
+            const uint32_t m0 = act ? min(cnt[q], P.stage_slots) : 0u;
+            uint32_t* src = stage + (act ? q : 0u) * P.stage_slots;
+            // pad the run to a multiple of 4 with copies of its last update
+            // (idempotent OR) so every copy below is an aligned 16-B store
+            const uint32_t m = (m0 + 3u) & ~3u;
+            if (gl < m - m0) src[m0 + gl] = src[m0 - 1];
+            __syncwarp();
+            if (m0) {
+              const uint32_t pos = cursor[q];  // multiple of 4; region_cap multiple of 32
+              const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
+              uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (boff + q * P.qstride + pos));
+              const uint4* src4 = reinterpret_cast<const uint4*>(src);
+              for (uint32_t s = gl; s < (fit >> 2); s += G) __stcg(dst4 + s, src4[s]);
+              for (uint32_t s = fit + gl; s < m; s += G) {  // region full: direct (exact)
+                const uint32_t u = src[s];
+                red_or_g(ldca + (uint64_t)q * P.part_words + (u >> 5), 1u << (u & 31));
+              }
+              if (gl == 0) {
+                cursor[q] = pos + fit;
+                cnt[q] = 0;
+              }
+            }
           }
         }
         __syncthreads();
@@ -410,6 +424,12 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   const double rmean = (double)P.chunk * p->lr * share / P.nparts;  // largest producer -> one destination
   P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
   P.region_cap = (P.region_cap + 31u) & ~31u;
+  // bucket offsets are 32-bit element indexes
+  if (2ull * P.nparts * P.nsrc * P.region_cap >= (1ull << 32)) return false;
+  P.qstride = P.nsrc * P.region_cap;
+  P.gshift = 0;
+  while ((2u << P.gshift) <= 32u && ((kThreads >> (P.gshift + 1)) >= P.nparts)) ++P.gshift;
+  if (P.gshift < 2) return false;  // the flush pads runs with up to 3 lanes of a group
   P.n = n;
   scratch = 4ull * (2ull * P.nparts * P.nsrc * P.region_cap + 2ull * P.nparts * P.nsrc);
   P.k_mask = p->k - 1;
