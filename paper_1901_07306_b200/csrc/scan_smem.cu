@@ -96,6 +96,7 @@ struct PartPlan {
   uint32_t k_mask, lc_mask, log2k;
   uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w (fast mode)
   uint32_t pshift, pmask;  // pow2 mode: partition of a bit index / its local bit
+  uint32_t qshift;         // pow2 mode: partition of a cell index (pshift - log2k)
   uint32_t vec_ok;         // hips/oips 16-byte aligned and chunk % 4 == 0
   uint32_t qstride;        // ns * region_cap: bucket elements per destination
   uint32_t gshift;         // log2 of the flush group size (threads per destination)
@@ -224,13 +225,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               bool ovf = false;
 #pragma unroll
               for (uint32_t i = 0; i < 8; ++i) {
+                // partitions hold whole cells and rows hold whole partitions
+                // (plan): q = cell >> qshift, entry = (cell << log2k | b) & pmask
                 const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
-                const uint32_t bit = ((i * p.lc + c) << P.log2k) | bb;
-                const uint32_t q = bit >> P.pshift;
+                const uint32_t q = (i * p.lc + c) >> P.qshift;
                 const uint32_t slot = atomicAdd(&cnt[q], 1u);
                 const bool fits = slot < P.stage_slots;
                 ovf |= !fits;
-                *(fits ? &stage[q * P.stage_slots + slot] : sink) = bit & P.pmask;
+                *(fits ? &stage[q * P.stage_slots + slot] : sink) = ((c << P.log2k) & P.pmask) | bb;
               }
               if (ovf) reapply_direct(p, P.lc_mask, P.log2k, hip, bb, ldca);
             } else if (kMode == kFast32) {
@@ -308,8 +310,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
               uint4* dst4 = reinterpret_cast<uint4*>(P.buckets + (boff + q * P.qstride + pos));
               const uint4* src4 = reinterpret_cast<const uint4*>(src);
-              for (uint32_t s = gl; s < (fit >> 2); s += G) __stcg(dst4 + s, src4[s]);
-              for (uint32_t s = fit + gl; s < m; s += G) {  // region full: direct (exact)
+              const uint32_t f4 = fit >> 2;
+              uint32_t s = gl;
+              for (; s + 3u * G < f4; s += 4u * G) {  // 4 shared loads in flight, then 4 stores
+                const uint4 a0 = src4[s], a1 = src4[s + G], a2 = src4[s + 2u * G], a3 = src4[s + 3u * G];
+                __stcg(dst4 + s, a0);
+                __stcg(dst4 + s + G, a1);
+                __stcg(dst4 + s + 2u * G, a2);
+                __stcg(dst4 + s + 3u * G, a3);
+              }
+              for (; s < f4; s += G) __stcg(dst4 + s, src4[s]);
+              for (s = fit + gl; s < m; s += G) {  // region full: direct (exact)
                 const uint32_t u = src[s];
                 red_or_g(ldca + (uint64_t)q * P.part_words + (u >> 5), 1u << (u & 31));
               }
@@ -435,6 +446,17 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   P.k_mask = p->k - 1;
   P.lc_mask = p->lc - 1;
   P.log2k = ilog2_ceil(p->k);
+  P.qshift = 0;
+  if (mode == kPow2) {
+    // the cell form of the routing needs whole cells per partition and
+    // whole partitions per row
+    const uint64_t pbits = 1ull << P.pshift;
+    if (P.pshift < P.log2k || ((uint64_t)p->lc << P.log2k) % pbits != 0) {
+      mode = kFast32;
+    } else {
+      P.qshift = P.pshift - P.log2k;
+    }
+  }
   return true;
 }
 
