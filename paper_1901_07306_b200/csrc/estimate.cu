@@ -346,7 +346,22 @@ __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__
     const uint64_t off_b =
         lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, p.seed_lh[lane + 32], p.div_lc)) * cell_bytes : 0;
     uint32_t pop = 0;
-    if ((p.k & 31u) == 0) {
+    if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
+      // 16-byte loads: lane l ANDs words 4l..4l+3 of each 128-word stripe
+      const uint32_t vecs = (uint32_t)(cell_bytes >> 4);
+      for (uint32_t base = 0; base < vecs; base += 32) {
+        const uint32_t v = base + lane;
+        uint4 acc = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        for (uint32_t i = 0; i < p.lr; ++i) {
+          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+          if (v < vecs) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(ldca + off) + v);
+            acc.x &= w.x, acc.y &= w.y, acc.z &= w.z, acc.w &= w.w;
+          }
+        }
+        if (v < vecs) pop += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+      }
+    } else if ((p.k & 31u) == 0) {
       const uint32_t words = p.k >> 5;
       for (uint32_t base = 0; base < words; base += 32) {
         const uint32_t wd = base + lane;

@@ -19,6 +19,7 @@
 // and every sliding stamp is a plain store (all writers of one slice store
 // the same value, so no atomic is needed and none would be correct across
 // the wrap -- see DESIGN.md).
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "sspd_common.cuh"
 #include "launch.cuh"
@@ -162,6 +163,65 @@ __global__ void __launch_bounds__(256) scan_sliding_kernel(const uint32_t* __res
     packet_sliding<T>(hips[j], oips[j], p, s, tmask);
 }
 
+// K2 fast path: u16 stamps, k and lc powers of two, < 2^32 slots, 16-byte
+// aligned inputs (config 4).  Four packets per thread from one 16-byte load
+// per array, 32-bit slot math (the row modulo is a mask), and the LDCA stamp
+// stores carry an L2 evict_last policy for a fraction of the addresses:
+// the ~134 MB LDCA stamp region is the re-written working set (8 stores per
+// packet), while the input stream and the sparse SEAV stamps are not, so
+// keeping most of it L2-resident turns partial-sector misses into hits.
+__device__ __forceinline__ void st_u16_hint(uint16_t* addr, uint16_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(addr), "h"(v), "l"(pol) : "memory");
+}
+
+__global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32_t* __restrict__ hips,
+                                                                    const uint32_t* __restrict__ oips, uint64_t n,
+                                                                    const __grid_constant__ sspd_params p,
+                                                                    uint16_t* pool, uint16_t now, float l2_frac) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(l2_frac));
+  const uint32_t tmask = tau_mask(p.tau);
+  const uint32_t k_mask = p.k - 1, lc_mask = p.lc - 1;
+  const uint32_t log2k = 31 - __clz(p.k);
+  uint16_t* const lpool = pool + p.slot_ldca_base;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // hips/oips share their misalignment (host check): peel the scalar head
+  const uint64_t head = min(n, (uint64_t)((16u - (reinterpret_cast<uintptr_t>(hips) & 15u)) & 15u) >> 2);
+  const uint64_t nq = (n - head) >> 2;
+  const uint4* hq = reinterpret_cast<const uint4*>(hips + head);
+  const uint4* oq = reinterpret_cast<const uint4*>(oips + head);
+  auto one = [&](uint32_t hip, uint32_t oip) {
+    if (sampled(oip, p.seed_h1, tmask)) {
+      const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+      const uint64_t rp = hip & ((1u << p.r) - 1u);
+      const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+      for (uint32_t i = 0; i < p.sr; ++i) {
+        const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+        pool[p.slot_row_base[i] + (rp * p.sc[i] + col) * p.g + bit] = now;
+      }
+    }
+    const uint32_t b = (uint32_t)mix64(oip ^ p.seed_h3) & k_mask;
+    uint32_t cell = 0;
+#pragma unroll 8
+    for (uint32_t i = 0; i < p.lr; ++i) {
+      const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & lc_mask;
+      st_u16_hint(lpool + (((cell + c) << log2k) | b), now, pol);
+      cell += p.lc;
+    }
+  };
+  for (uint64_t q = tid; q < nq; q += stride) {
+    const uint4 h = ld_stream(hq + q);
+    const uint4 o = ld_stream(oq + q);
+    one(h.x, o.x);
+    one(h.y, o.y);
+    one(h.z, o.z);
+    one(h.w, o.w);
+  }
+  if (tid < head) one(hips[tid], oips[tid]);
+  for (uint64_t j = head + (nq << 2) + tid; j < n; j += stride) one(hips[j], oips[j]);
+}
+
 template <bool S, bool L>
 static int launch_discrete(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params& p,
                            uint8_t* seav, uint8_t* ldca, cudaStream_t st) {
@@ -209,6 +269,18 @@ extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uin
       break;
     }
     case 2: {
+      const bool pow2 = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0;
+      const bool aligned = ((reinterpret_cast<uintptr_t>(hips) ^ reinterpret_cast<uintptr_t>(oips)) & 15u) == 0 &&
+                           (reinterpret_cast<uintptr_t>(hips) & 3u) == 0;
+      if (pow2 && aligned && p->slot_total < (1ull << 32) && getenv("SSPD_SLIDE_GENERIC") == nullptr) {
+        float frac = 0.85f;
+        if (const char* e = getenv("SSPD_SLIDE_L2_FRAC")) frac = (float)atof(e);
+        frac = frac < 0.f ? 0.f : (frac > 1.f ? 1.f : frac);
+        const int grid = grid_for(scan_sliding_u16_fast_kernel, 256, (n + 3) / 4);
+        scan_sliding_u16_fast_kernel<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool,
+                                                            (uint16_t)now_wrapped, frac);
+        break;
+      }
       const int grid = grid_for(scan_sliding_kernel<uint16_t>, 256, n);
       scan_sliding_kernel<uint16_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped);
       break;

@@ -73,6 +73,44 @@ __global__ void __launch_bounds__(256) materialize_seav_kernel(const T* __restri
   }
 }
 
+// Fast path of materialize_seav for the common layout (g = 8 one-byte
+// registers, u16 stamps): a thread builds FOUR consecutive registers of one
+// row from four independent 16-byte streaming loads (8 stamps each) and
+// writes them as one u32, so the pass runs at HBM speed instead of being
+// instruction-bound (one register per thread).  `quads` = registers / 4.
+__device__ __forceinline__ uint32_t active8_u16(uint4 v, uint16_t now, uint32_t window) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t lo = (uint16_t)(now - (uint16_t)(w[e] & 0xFFFFu));
+    const uint32_t hi = (uint16_t)(now - (uint16_t)(w[e] >> 16));
+    bits |= (lo < window ? 1u : 0u) << (2 * e);
+    bits |= (hi < window ? 1u : 0u) << (2 * e + 1);
+  }
+  return bits;
+}
+
+__global__ void __launch_bounds__(256) materialize_seav_g8u16_kernel(const uint16_t* __restrict__ pool,
+                                                                     const __grid_constant__ sspd_params p,
+                                                                     uint16_t now, uint32_t window, uint64_t quads,
+                                                                     uint8_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += stride) {
+    uint32_t i = 0;
+    uint64_t local = q;
+    while (local >= (((uint64_t)p.sc[i] << p.r) >> 2)) {
+      local -= ((uint64_t)p.sc[i] << p.r) >> 2;
+      ++i;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(pool + p.slot_row_base[i]) + local * 4;
+    const uint4 v0 = __ldcs(src), v1 = __ldcs(src + 1), v2 = __ldcs(src + 2), v3 = __ldcs(src + 3);
+    const uint32_t word = active8_u16(v0, now, window) | (active8_u16(v1, now, window) << 8) |
+                          (active8_u16(v2, now, window) << 16) | (active8_u16(v3, now, window) << 24);
+    *reinterpret_cast<uint32_t*>(out + p.seav_row_off[i] + local * 4) = word;
+  }
+}
+
 // materialize_ldca (sliding.py:215-220): byte q of the packed array holds
 // the activity of slots ldca_base + 8q .. 8q+7, little bit order.
 template <typename T>
@@ -140,12 +178,37 @@ extern "C" int sspd_materialize_seav(const void* pool, uint32_t ts_bytes, const 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint64_t regs = 0;
   for (uint32_t i = 0; i < p->sr; ++i) regs += ((uint64_t)p->sc[i]) << p->r;
+  bool fast = ts_bytes == 2 && p->g == 8 && p->reg_bytes == 1 &&
+              (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 && (reinterpret_cast<uintptr_t>(seav_out) & 3u) == 0;
+  for (uint32_t i = 0; i < p->sr && fast; ++i)
+    fast = ((((uint64_t)p->sc[i]) << p->r) & 3u) == 0 && (p->slot_row_base[i] & 7u) == 0 && (p->seav_row_off[i] & 3u) == 0;
+  if (fast) {
+    const uint64_t quads = regs >> 2;
+    const int grid = grid_for(materialize_seav_g8u16_kernel, 256, quads);
+    materialize_seav_g8u16_kernel<<<grid, 256, 0, st>>>((const uint16_t*)pool, *p, (uint16_t)now_wrapped,
+                                                        (uint32_t)window_slices, quads, seav_out);
+    return check_launch();
+  }
   SSPD_TS_DISPATCH(ts_bytes, {
     // one register per thread: a full grid keeps every load independent
     const int grid = (int)((regs + 255) / 256 < 0x7FFFFFFFull ? (regs + 255) / 256 : 0x7FFFFFFF);
     materialize_seav_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, *p, (T)now_wrapped, window_slices, seav_out);
   })
   return check_launch();
+}
+
+// materialize_ldca fast path (u16 stamps): four output bytes per thread
+// from four independent 16-byte streaming loads, one u32 store.
+__global__ void __launch_bounds__(256) materialize_ldca_u16x4_kernel(const uint16_t* __restrict__ pool, uint64_t base,
+                                                                     uint64_t nwords, uint16_t now, uint32_t window,
+                                                                     uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) {
+    const uint4* src = reinterpret_cast<const uint4*>(pool + base) + q * 4;
+    const uint4 v0 = __ldcs(src), v1 = __ldcs(src + 1), v2 = __ldcs(src + 2), v3 = __ldcs(src + 3);
+    out[q] = active8_u16(v0, now, window) | (active8_u16(v1, now, window) << 8) |
+             (active8_u16(v2, now, window) << 16) | (active8_u16(v3, now, window) << 24);
+  }
 }
 
 extern "C" int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes, const sspd_params* p,
@@ -156,6 +219,15 @@ extern "C" int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes, const 
   if (!pool || !ldca_out) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t nbytes = p->ldca_bytes;
+  if (ts_bytes == 2 && (nbytes & 3u) == 0 && (p->slot_ldca_base & 7u) == 0 &&
+      (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca_out) & 3u) == 0) {
+    const uint64_t nwords = nbytes >> 2;
+    const int grid = grid_for(materialize_ldca_u16x4_kernel, 256, nwords);
+    materialize_ldca_u16x4_kernel<<<grid, 256, 0, st>>>((const uint16_t*)pool, p->slot_ldca_base, nwords,
+                                                        (uint16_t)now_wrapped, (uint32_t)window_slices,
+                                                        reinterpret_cast<uint32_t*>(ldca_out));
+    return check_launch();
+  }
   SSPD_TS_DISPATCH(ts_bytes, {
     const int grid = (int)((nbytes + 255) / 256 < 0x7FFFFFFFull ? (nbytes + 255) / 256 : 0x7FFFFFFF);
     materialize_ldca_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, p->slot_ldca_base, nbytes, (T)now_wrapped,

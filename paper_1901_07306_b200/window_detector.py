@@ -190,13 +190,16 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
 
     ip, aux, overflow = seav._restore_device(0, 1 << seav.config.r)
     n = ip.numel()
-    flagged = np.nonzero(overflow.cpu().numpy())[0].tolist()
-    for rp in flagged:
-        err = SeaOverflowError(rp, seav.restore_cap)
-        if on_overflow != "warn":
-            raise err
-        warnings.warn(str(err), RuntimeWarning, stacklevel=3)
+
+    def check_overflow(flags: np.ndarray):
+        for rp in np.nonzero(flags)[0].tolist():
+            err = SeaOverflowError(rp, seav.restore_cap)
+            if on_overflow != "warn":
+                raise err
+            warnings.warn(str(err), RuntimeWarning, stacklevel=4)
+
     if n == 0:
+        check_overflow(overflow.cpu().numpy())
         return np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32)
     dev = ip.device
     table = device_keep_table(k, cutoff)
@@ -220,18 +223,27 @@ def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: 
         else:
             call("sspd_filter_sliding", pool.data_ptr(), ts_bytes, params_block, now_w, window,
                  ip.data_ptr(), n, table.data_ptr(), z0.data_ptr(), keep.data_ptr(), stream_ptr())
-    ip_out = torch.empty(n, dtype=torch.int32, device=dev)
-    z0_out = torch.empty(n, dtype=torch.int32, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    out = torch.empty(2 * n + 2, dtype=torch.int32, device=dev)  # [ip_out | z0_out | count (i64)]
+    ip_out, z0_out = out[:n], out[n:2 * n]
+    cnt = out[2 * n:].view(torch.int64)
     need = ctypes.c_size_t(0)
     call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
          z0_out.data_ptr(), cnt.data_ptr(), None, ctypes.byref(need), stream_ptr())
     scratch = torch.empty(max(16, need.value), dtype=torch.uint8, device=dev)
     call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
          z0_out.data_ptr(), cnt.data_ptr(), scratch.data_ptr(), ctypes.byref(need), stream_ptr())
-    m = int(cnt.item())
-    both = torch.stack((ip_out[:m], z0_out[:m])).cpu().numpy().view(np.uint32)
-    return both[0], both[1]
+    # ONE device->host round trip for the results, their count and the
+    # restore overflow flags (pinned staging, asynchronous copies)
+    host = torch.empty(out.numel(), dtype=torch.int32, pin_memory=True)
+    host_ovf = torch.empty(overflow.numel(), dtype=torch.uint8, pin_memory=True)
+    host.copy_(out, non_blocking=True)
+    host_ovf.copy_(overflow, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    check_overflow(host_ovf.numpy())
+    h = host.numpy()
+    m = int(h[2 * n:].view(np.int64)[0])
+    both = h[:2 * n].view(np.uint32)
+    return both[:m].copy(), both[n:n + m].copy()
 
 
 @dataclass

@@ -178,3 +178,31 @@ def test_partition_invariance(cuda, route, n_wp):
     assert res.global_seav.payload_bytes() == ref.global_seav.payload_bytes()
     assert res.global_ldca.payload_bytes() == ref.global_ldca.payload_bytes()
     assert res.reports == ref.reports and len(res.reports) >= 1
+
+
+@pytest.mark.parametrize("off", [0, 1, 2, 3, 7])
+def test_sliding_observe_device_slices_vs_oracle(cuda, oracle, off):
+    """K2 fast path (u16 stamps, pow2 geometry) on device slices at every
+    16-byte misalignment: pool bytes equal the oracle's, slide by slide."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=1024, k=8192, lr=8, lc=256, design_n=1e5)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(params, window_slices=300)
+    rng = np.random.default_rng(100 + off)
+    n = 60_013
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    hips[:5000] = 0x0A000001
+    h = torch.from_numpy(hips.view(np.int32)).cuda()
+    o = torch.from_numpy(oips.view(np.int32)).cuda()
+    pool = det.pool.ts.copy()
+    cuts = [off, off + 1, off + 4098, off + 20_001, n - 3, n]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        det.observe_batch(h[lo:hi], o[lo:hi])
+        oracle.observe(det._params, hips[lo:hi], oips[lo:hi], pool, det.pool._wrapped_now())
+        assert (det.pool.ts == pool).all(), (lo, hi)
+        det.advance_slice()
