@@ -203,6 +203,10 @@ struct Group {
     else
       __syncthreads();
   }
+  __device__ __forceinline__ bool any(bool v) const {
+    if (kWarp) return __any_sync(0xFFFFFFFFu, v);
+    return __syncthreads_or(v) != 0;
+  }
 };
 
 template <bool kWarp>
@@ -212,6 +216,17 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
                                   const Group<kWarp> G) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t sr = P.sr;
+
+  // fast reject straight from global memory: a row without a hot register
+  // admits no complete tuple (short_sketch.py:360-361), so the SEA has no
+  // candidates and no survivors (it cannot overflow either).  Most SEAs of
+  // a large, sparse SEAV end here without touching shared memory.
+  for (uint32_t i = 0; i < sr; ++i) {
+    const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * P.sc[i] * P.reg_bytes;
+    bool hot = false;
+    for (uint32_t c = G.tid; c < P.sc[i]; c += G.size) hot |= __popcll(load_reg(src, c, P.reg_bytes)) >= 3;
+    if (!G.any(hot)) return;
+  }
 
   // stage the SEA's registers and clear the bucket tables
   for (uint32_t i = 0; i < sr; ++i) {

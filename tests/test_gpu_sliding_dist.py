@@ -206,3 +206,34 @@ def test_sliding_observe_device_slices_vs_oracle(cuda, oracle, off):
         oracle.observe(det._params, hips[lo:hi], oips[lo:hi], pool, det.pool._wrapped_now())
         assert (det.pool.ts == pool).all(), (lo, hi)
         det.advance_slice()
+
+
+@pytest.mark.parametrize("r", [4, 8, 16])
+def test_views_fast_paths_vs_oracle(cuda, oracle, r):
+    """K4 fast paths (4 SEAV registers / 4 LDCA bytes per thread, u16
+    stamps) on a random pool whose ages straddle the window edge, at every
+    wrapped `now`, vs the oracle's materialize_* (sliding.py:191-220)."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=1024, r=r, k=4096, lr=4, lc=64, design_n=1e5)
+    w = 300
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(params, window_slices=w)
+    rng = np.random.default_rng(r)
+    n = det.pool.n_slots
+    for now in (0, 299, 300, 65535, 40000):
+        edge = rng.integers(w - 3, w + 3, size=n)          # around the window edge
+        ages = np.where(rng.random(n) < 0.5, rng.integers(0, 2 * w + 2, size=n), edge)
+        pool = ((now - ages) & 0xFFFF).astype(np.uint16)
+        det.pool.ts = pool
+        det.pool.now = now
+        got_s = det.materialize_seav().payload_bytes()
+        got_l = det.materialize_ldca().tobytes()
+        want_s = oracle.materialize_seav(det._params, pool, now & 0xFFFF, w)
+        want_l = oracle.materialize_ldca(det._params, pool, now & 0xFFFF, w)
+        assert got_s == want_s.tobytes(), now
+        assert got_l == want_l.tobytes(), now
+        torch.cuda.synchronize()
