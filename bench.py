@@ -397,7 +397,7 @@ def run_gpu(args) -> dict | None:
     achieved_gbs = 8 * n / (scan_ms * 1e-3) / 1e9
     roof_pps = min(hbm_gbs * 1e9 / 8, red_per_s / reds_per_pkt)
     kernel = getattr(st, "last_scan", "direct")
-    kname = ("scan_partitioned_kernel<true,true> (K1p, LDCA in shared memory)" if kernel == "partitioned"
+    kname = ("scan_partitioned_kernel<true, kPow2> (K1p, LDCA in shared memory)" if kernel == "partitioned"
              else "scan_discrete_kernel<true,true> (K1, L2 red.or)")
     # per-kernel ncu evidence committed under profiles/ (bytes and issue slots per packet)
     prof = {}
@@ -429,11 +429,17 @@ def run_gpu(args) -> dict | None:
                    "l2": "inputs (2 GiB/window) exceed the 126 MB L2; no flush needed",
                    "seav_r": dp.r, "ldca": "LR=8 LC=1024 k=8192 (8 MiB)"},
         "e2e": e2e,
-        "gpu_launches": args.steps * (5 + (1 if merger else 0)),
+        # per step: K1p scan, K5 restore, CUB sort (histogram, exclusive sum,
+        # 4 onesweep passes), K6 filter, compaction (count + scatter) = 11
+        # launches of libsspd_b200.so (+ the merge kernels at N > 1)
+        "gpu_launches": args.steps * (11 + (2 if merger else 0)),
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": hbm_gbs, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback",
-                     "kernel": kname, "algorithmic_bytes_per_packet": 8},
+                     "kernel": kname, "algorithmic_bytes_per_packet": 8,
+                     "note": ("the packet stream is 8 B/pkt, so HBM is far from binding; the scan is bound by "
+                              "SM instruction issue (ten SplitMix64 hashes per packet on the ALU pipe) -- "
+                              "see issue_roofline, and scan_roofline for the SURVEY's L2-atomic roofline")},
         "scan_roofline": {"bound": "l2_red", "l2_red_ops_per_s": round(red_per_s / 1e9, 2),
                           "reds_per_packet": round(reds_per_pkt, 4), "roofline_gpps": round(roof_pps / 1e9, 3),
                           "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / roof_pps, 4),

@@ -18,8 +18,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --clock-control none -k regex:scan_partitioned -c 2 --csv --log-file "$OUT/ncu_metrics_partitioned.csv" \
   python tools/sweep_k1p.py --reps 1 "" > /dev/null 2>&1; echo "ncu_metrics=$?"
 # launch list of the default bench step (every kernel of the step)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file "$OUT/launches_config2.csv" \
-  python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo "launches=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:sspd::|CUB_' -c 66 --csv \
+  --log-file "$OUT/launches_config2.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+echo "launches=$?"
 # full capture of the dominant kernel
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_partitioned -c 1 -f -o "$OUT/k1p_full" \
   python tools/sweep_k1p.py --reps 1 "" > /dev/null 2>&1; echo "ncu_full=$?"
