@@ -79,3 +79,46 @@ def test_exact_full_size_config2_properties(cuda):
     planted = cardinalities(CONFIG2)[:CONFIG2.n_super]  # distinct by construction
     assert sorted(ex.cardinality(int(s)) for s in supers) == sorted(planted.tolist())
     assert len(ex.hosts) == CONFIG2.n_sources
+
+
+# --- the reference's oracle tests (test_evaluation.py:27-60) re-stated -------
+
+def test_empty_trace_oracle(cuda):  # :27-29
+    from paper_1901_07306_b200 import ExactOracle
+
+    oracle = ExactOracle(np.array([], dtype=np.uint64), np.array([], dtype=np.uint64))
+    assert oracle.superpoints(1) == []
+
+
+def test_oracle_counts_distinct_only(cuda):  # :32-40
+    from paper_1901_07306_b200 import ExactOracle
+
+    oracle = ExactOracle(np.array([1, 1, 1, 2, 2], dtype=np.uint64), np.array([9, 9, 8, 7, 7], dtype=np.uint64))
+    assert oracle.cardinality(1) == 2 and oracle.cardinality(2) == 1 and oracle.cardinality(3) == 0
+    assert oracle.superpoints(2) == [1]
+    assert oracle.superpoints(1) == [1, 2]
+
+
+def test_boundary_inclusion(cuda):  # :43-47
+    from paper_1901_07306_b200 import ExactOracle, oracle_superpoints
+
+    oracle = ExactOracle(np.repeat(np.uint64(5), 10), np.arange(10, dtype=np.uint64))
+    assert oracle_superpoints(oracle, 10) == [5]
+    assert oracle_superpoints(oracle, 11) == []
+
+
+def test_oracle_implementations_agree(cuda):  # :50-60 (seeded instead of hypothesis)
+    from paper_1901_07306_b200 import ExactOracle
+
+    rng = np.random.default_rng(60)
+    for _ in range(50):
+        m = int(rng.integers(0, 301))
+        pairs = rng.integers(0, 51, size=(m, 2))
+        fast = ExactOracle(pairs[:, 0].astype(np.uint64), pairs[:, 1].astype(np.uint64))
+        slow: dict[int, set] = {}
+        for h, o in pairs.tolist():
+            slow.setdefault(h, set()).add(o)
+        slow_c = {h: len(v) for h, v in slow.items()}
+        assert {int(h): int(c) for h, c in zip(fast.hosts, fast.counts)} == slow_c
+        for theta in (1, 2, 5):
+            assert fast.superpoints(theta) == sorted(h for h, c in slow_c.items() if c >= theta)

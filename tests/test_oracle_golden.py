@@ -199,3 +199,18 @@ def test_metrics_host_logic(golden):
         assert metrics(det, truth) == (got["fpr"], got["fnr"], got["ftr"])
     with pytest.raises(UndefinedMetricError):
         metrics([1, 2], [])
+
+
+def test_metric_rates_reference_cases():
+    """test_evaluation.py:65-100 re-stated on the drop-in metric functions."""
+    from paper_1901_07306_b200 import metrics, metrics_report
+
+    truth = list(range(50))
+    assert metrics(truth, truth) == (0.0, 0.0, 0.0)
+    fpr, fnr, ftr = metrics(truth + [999], truth)
+    assert fpr == pytest.approx(0.02) and fnr == 0.0 and ftr == pytest.approx(0.02)
+    fpr, fnr, _ = metrics(truth[:-2], truth)
+    assert fnr == pytest.approx(0.04) and fpr == 0.0
+    assert metrics(list(range(100, 110)), list(range(5)))[0] == pytest.approx(2.0)
+    rep = metrics_report([1, 2, 3, 99], [1, 2, 3, 4])
+    assert rep["precision_nonpaper"] == pytest.approx(3 / 4) and rep["detected"] == 4 and rep["truth"] == 4

@@ -358,6 +358,13 @@ def generate_shard(spec: ShardedSpec, shard: int, backend: str = "numpy", device
 
     Background pairs of the global population go to router hash(pair) % n;
     super s's j-th peer goes to routers_s[j % m_s]."""
+    return generate_shards(spec, [shard], backend, device)[0]
+
+
+def generate_shards(spec: ShardedSpec, shards, backend: str = "numpy", device=None):
+    """[(hips, oips, supers)] for several routers of one population: the
+    global edge set and its routing are built once (bit-identical to
+    calling generate_shard per router)."""
     xp = _NP() if backend == "numpy" else _Torch(device)
     seed = spec.seed
     sup_cards, routers = super_routing(spec)
@@ -387,29 +394,37 @@ def generate_shard(spec: ShardedSpec, shard: int, backend: str = "numpy", device
     sup_router = tab[hs * spec.n_shards + rank % m]
     bg_router = xp.shr(xp.draw(T_SHARD, seed, eidx), 1) % spec.n_shards
     router = sup_router * is_sup + bg_router * (1 - is_sup * 1)
-    mine = eidx[router == shard]
-    n_mine = int(mine.shape[0])
-    if n_mine > spec.packets_per_shard:
-        raise ValueError(f"{spec.name}: shard {shard} has {n_mine} pairs > {spec.packets_per_shard} packets")
-    sseed = seed * 131 + shard + 1
-    table = xp.host(geometric_table(spec.dup_p))
-    counts = 1 + xp.searchsorted_left(table, -xp.shr(xp.draw(T_DUP, sseed, mine), 11))
-    extra_pool = xp.repeat(mine, counts - 1)
-    need = spec.packets_per_shard - n_mine
-    pool_n = int(extra_pool.shape[0])
-    if pool_n >= need:
-        extra = extra_pool[xp.argsort(xp.shr(xp.draw(T_PICK, sseed, xp.arange(pool_n)), 1))[:need]]
-    else:
-        pad = mine[xp.shr(xp.draw(T_PAD, sseed, xp.arange(need - pool_n)), 1) % n_mine]
-        extra = xp.cat([extra_pool, pad])
-    edges = xp.cat([mine, extra])
-    order = xp.argsort(xp.shr(xp.draw(T_ORDER, sseed, xp.arange(spec.packets_per_shard)), 1))
-    stream = edges[order]
-    hips = src_ip[host_of[stream]]
-    oips = dst[stream]
+    del rank, off, m, sup_router, bg_router, hs, is_sup
     supers = src_ip[: spec.n_super]
-    if backend == "numpy":
-        return hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32))
-    t = xp.t
-    to32 = lambda x: t.where(x >= 2**31, x - 2**32, x).to(t.int32)  # noqa: E731
-    return to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32))
+    table = xp.host(geometric_table(spec.dup_p))
+    out = []
+    for shard in shards:
+        mine = eidx[router == shard]
+        n_mine = int(mine.shape[0])
+        if n_mine > spec.packets_per_shard:
+            raise ValueError(f"{spec.name}: shard {shard} has {n_mine} pairs > {spec.packets_per_shard} packets")
+        sseed = seed * 131 + shard + 1
+        counts = 1 + xp.searchsorted_left(table, -xp.shr(xp.draw(T_DUP, sseed, mine), 11))
+        extra_pool = xp.repeat(mine, counts - 1)
+        need = spec.packets_per_shard - n_mine
+        pool_n = int(extra_pool.shape[0])
+        if pool_n >= need:
+            extra = extra_pool[xp.argsort(xp.shr(xp.draw(T_PICK, sseed, xp.arange(pool_n)), 1))[:need]]
+        else:
+            pad = mine[xp.shr(xp.draw(T_PAD, sseed, xp.arange(need - pool_n)), 1) % n_mine]
+            extra = xp.cat([extra_pool, pad])
+        edges = xp.cat([mine, extra])
+        del mine, counts, extra_pool, extra
+        order = xp.argsort(xp.shr(xp.draw(T_ORDER, sseed, xp.arange(spec.packets_per_shard)), 1))
+        stream = edges[order]
+        del edges, order
+        hips = src_ip[host_of[stream]]
+        oips = dst[stream]
+        del stream
+        if backend == "numpy":
+            out.append((hips.astype(np.uint32), oips.astype(np.uint32), np.sort(supers.astype(np.uint32))))
+        else:
+            t = xp.t
+            to32 = lambda x: t.where(x >= 2**31, x - 2**32, x).to(t.int32)  # noqa: E731
+            out.append((to32(hips), to32(oips), np.sort(supers.cpu().numpy().astype(np.uint32))))
+    return out
