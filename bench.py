@@ -352,7 +352,9 @@ def run_gpu(args) -> dict | None:
             if merger is not None:
                 merger.merge_to_root()
             reps = st.finalize_window() if rank == 0 else []
-            d2h[0] = 8 * len(reps) + 16  # (ip, z0) pairs + counts read back
+            if rank == 0 and len(reps):
+                reps.ips  # the super-point list itself comes back to the host (lazy otherwise)
+            d2h[0] = 8 * len(reps) + 16 + (1 << dp.r)  # (ip, z0) pairs + counts + overflow flags
             st.reset()
 
         for _ in range(max(1, args.warmup // 2)):
@@ -493,13 +495,16 @@ def run_sliding(args) -> dict:
 
     def step(record=None):
         det.reset()
-        total = 0
+        pending = []
         for s in range(n_sl):
             lo, hi = bounds[s], bounds[s + 1]
             if hi > lo:
                 det.observe_batch(hips[lo:hi], oips[lo:hi])
-            total += len(det.detect())
+            # every slide's super-point list is computed inside the step; the
+            # async form overlaps restore/filter of slide s with the scan of s+1
+            pending.append(det.detect() if args.sync_detect else det.detect_async())
             det.advance_slice()
+        total = sum(len(r) for r in pending)  # all lists resolved before the step ends
         if record is not None:
             record.append(total)
 
@@ -528,6 +533,8 @@ def run_sliding(args) -> dict:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 keys / u16 stamps",
         "data": "synthetic (seeded, tools/workloads.py CONFIG4)",
         "config": {"workload": f"config4: {n} pkts, {n_sl} slices, w=300, r=16, LDCA 8x1024x8192, detect every slide",
+                   "detect": "synchronous detect()" if args.sync_detect else
+                             "detect_async(): K5/K6 of slide s on a side stream, overlapping K2 of slide s+1",
                    "pool_bytes": det.pool.memory_bytes(), "l2": "pool 403 MB exceeds L2; inputs 4 GiB"},
         "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
@@ -749,6 +756,7 @@ def main():
     ap.add_argument("--part-chunk", type=int, default=0, help="partitioned-scan chunk (packets); 0 = default")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
+    ap.add_argument("--sync-detect", action="store_true", help="config 4: synchronous detect() per slide")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="2 = headline discrete window; 3 = 8 router shards OR-merged (strong scaling); "
                          "4 = sliding window, detect every slide; 5 = 2^32 pkts streamed from host")

@@ -125,6 +125,12 @@ SSPD_API uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t c
 SSPD_API int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                       const sspd_params* p, void* pool, uint32_t ts_bytes,
                       uint64_t now_wrapped, void* stream);
+/* The same with the scan's grid capped at max_blocks_per_sm resident blocks
+ * per SM (0 = no cap), leaving room for kernels of another stream -- the
+ * pipelined detect of SlidingDetector.detect_async. */
+SSPD_API int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                      const sspd_params* p, void* pool, uint32_t ts_bytes,
+                                      uint64_t now_wrapped, uint32_t max_blocks_per_sm, void* stream);
 
 /* ---- K3 sweep: TimestampPool._sweep (sliding.py:88-94) ---------------- */
 SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
@@ -196,6 +202,21 @@ SSPD_API int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0,
                          const uint8_t* keep, uint64_t n, uint32_t* ip_out,
                          uint32_t* z0_out, unsigned long long* out_count,
                          void* scratch, size_t* scratch_bytes, void* stream);
+
+/* ---- fused finalize (K5 + sort + K6 + compaction, no host round trip) ----
+ * DetectorState.finalize_window (window_detector.py:105-125) /
+ * SlidingDetector.detect on a materialised LDCA view (sliding.py:232-248):
+ * restore with cap `restore_cap` into `capacity` candidate slots, sort by
+ * ip, filter against `ldca` with the host-built keep table, stable
+ * compaction into out_ip/out_z0 (capacity entries each).  counts (device,
+ * 2 x u64): [0] candidates found -- if it exceeds `capacity` the outputs
+ * are incomplete and the caller re-runs with a larger capacity -- and [1]
+ * reports kept.  overflow (device, 2^r bytes): 1 for every register array
+ * dropped by the cap.  scratch NULL queries *scratch_bytes. */
+SSPD_API int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p,
+                           uint64_t restore_cap, const uint8_t* keep_table, uint64_t capacity,
+                           uint32_t* out_ip, uint32_t* out_z0, unsigned long long* counts,
+                           uint8_t* overflow, void* scratch, size_t* scratch_bytes, void* stream);
 
 /* ---- K7 merge ----------------------------------------------------------
  * Bytewise OR of n_src equal-length buffers into dst (dst may alias

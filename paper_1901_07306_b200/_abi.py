@@ -103,6 +103,7 @@ _SIGS = {
     "sspd_scan_partitioned": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "sspd_scan_partitioned_scratch": (_U64, [_PP, _U64]),
     "sspd_scan_sliding": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _VP]),
+    "sspd_scan_sliding_capped": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP]),
     "sspd_sweep": (C.c_int, [_VP, _U64, _U32, _U64, _U64, _U64, _VP]),
     "sspd_materialize_seav": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP]),
     "sspd_materialize_ldca": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP]),
@@ -124,6 +125,8 @@ _SIGS = {
     "sspd_copy_async": (C.c_int, [_VP, _VP, _U64, _VP]),
     "sspd_unpack_records": (C.c_int, [_VP, _U64, _VP, _VP, _VP, _VP]),
     "sspd_crc32": (C.c_int, [_VP, _U64, _VP, _VP, C.POINTER(_U64), _VP]),
+    "sspd_finalize": (C.c_int, [_VP, _VP, _PP, _U64, _VP, _U64, _VP, _VP, _VP, _VP, _VP, C.POINTER(C.c_size_t),
+                                _VP]),
     "sspd_exact_cardinalities": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _VP, _VP, C.POINTER(C.c_size_t), _VP]),
 }
 

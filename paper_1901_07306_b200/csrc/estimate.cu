@@ -345,16 +345,23 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
 
 // ------------------------------------------------------------------ filter
 // One warp per candidate: AND of the LR row cells, popcount, z0 = k - pop.
+// n_dev (optional): the live count lives in device memory (<= n); entries
+// at or beyond it get keep = 0 so a fixed-capacity compaction skips them.
 __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__ ldca,
                                                      const __grid_constant__ sspd_params p,
                                                      const uint32_t* __restrict__ ips, uint64_t n,
                                                      const uint8_t* __restrict__ keep_table, uint32_t* z0_out,
-                                                     uint8_t* keep_out) {
+                                                     uint8_t* keep_out, const unsigned long long* n_dev) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t cell_bytes = p.k >> 3;
+  const uint64_t live = n_dev ? min(n, (uint64_t)*n_dev) : n;
   for (uint64_t j = warp; j < n; j += nwarps) {
+    if (j >= live) {
+      if (lane == 0 && keep_out) keep_out[j] = 0;
+      continue;
+    }
     const uint32_t ip = ips[j];
     // lane i (and i+32) hashes row i once; cells are broadcast by shuffle
     const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, p.seed_lh[lane], p.div_lc)) * cell_bytes : 0;
@@ -671,7 +678,7 @@ extern "C" int sspd_filter(const uint8_t* ldca, const sspd_params* p, const uint
   if (!ldca || !ips || !z0_out) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = grid_for(filter_kernel, 256, n * 32);
-  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, ips, n, keep_table, z0_out, keep_out);
+  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, ips, n, keep_table, z0_out, keep_out, nullptr);
   return check_launch();
 }
 
@@ -723,5 +730,66 @@ extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, cons
   uint32_t* seg_counts = static_cast<uint32_t*>(scratch);
   compact_count_kernel<<<(unsigned)segs, 1024, 0, st>>>(keep, n, seg_counts);
   compact_scatter_kernel<<<(unsigned)segs, 1024, 0, st>>>(ip, z0, keep, n, seg_counts, ip_out, z0_out, out_count);
+  return check_launch();
+}
+
+// One finalize without host round trips (restore -> sort -> filter ->
+// compaction), every count kept on the device.  The candidate buffers have a
+// fixed capacity C: the key buffer is pre-filled with 0xFFFFFFFF so the
+// radix sort of all C slots leaves the live candidates first (stable on
+// equal keys), the filter marks slots past the live count as not kept, and
+// the compaction runs over C.  counts[0] = candidates found (may exceed C:
+// the outputs are then incomplete and the caller retries with a larger C),
+// counts[1] = reports kept.
+extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p, uint64_t restore_cap,
+                             const uint8_t* keep_table, uint64_t capacity, uint32_t* out_ip, uint32_t* out_z0,
+                             unsigned long long* counts, uint8_t* overflow, void* scratch, size_t* scratch_bytes,
+                             void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!scratch_bytes || capacity == 0 || capacity >= (1ull << 31)) return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t C = (size_t)capacity;
+  const size_t vec = ((C * 4 + 255) / 256) * 256;
+  size_t sort_tmp = 0;
+  {
+    cub::DoubleBuffer<uint32_t> k0(nullptr, nullptr), v0(nullptr, nullptr);
+    if (cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, k0, v0, (int)C, 0, 32, st) != cudaSuccess)
+      return SSPD_ERR_CUDA;
+  }
+  const size_t segs = (C + kSeg - 1) / kSeg;
+  // [ip | aux | ip_alt | aux_alt | z0 | keep | sort temp | compaction segs]
+  const size_t o_aux = vec, o_ipa = 2 * vec, o_auxa = 3 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;
+  const size_t o_tmp = o_keep + ((C + 255) / 256) * 256;
+  const size_t o_seg = o_tmp + ((sort_tmp + 255) / 256) * 256;
+  const size_t need = o_seg + 4 * segs + 256;
+  if (!scratch) {
+    *scratch_bytes = need;
+    return SSPD_OK;
+  }
+  if (*scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  if (!seav || !ldca || !out_ip || !out_z0 || !counts || !overflow) return SSPD_ERR_DATA;
+  uint8_t* s8 = static_cast<uint8_t*>(scratch);
+  uint32_t* ip = reinterpret_cast<uint32_t*>(s8);
+  uint32_t* aux = reinterpret_cast<uint32_t*>(s8 + o_aux);
+  uint32_t* ipa = reinterpret_cast<uint32_t*>(s8 + o_ipa);
+  uint32_t* auxa = reinterpret_cast<uint32_t*>(s8 + o_auxa);
+  uint32_t* z0 = reinterpret_cast<uint32_t*>(s8 + o_z0);
+  uint8_t* keep = s8 + o_keep;
+  const uint32_t rp_count = 1u << p->r;
+  if (cudaMemsetAsync(ip, 0xFF, C * 4, st) != cudaSuccess || cudaMemsetAsync(counts, 0, 16, st) != cudaSuccess ||
+      cudaMemsetAsync(overflow, 0, rp_count, st) != cudaSuccess)
+    return SSPD_ERR_CUDA;
+  rc = sspd_restore(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, stream);
+  if (rc) return rc;
+  size_t tb = sort_tmp;
+  cub::DoubleBuffer<uint32_t> kb(ip, ipa), vb(aux, auxa);
+  if (cub::DeviceRadixSort::SortPairs(s8 + o_tmp, tb, kb, vb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
+  const uint32_t* sorted = kb.Current();
+  const int grid = grid_for(filter_kernel, 256, C * 32);
+  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);
+  size_t cb = 4 * segs;
+  rc = sspd_compact_reports(sorted, z0, keep, C, out_ip, out_z0, counts + 1, s8 + o_seg, &cb, stream);
+  if (rc) return rc;
   return check_launch();
 }

@@ -255,8 +255,18 @@ extern "C" int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, ui
   return launch_discrete<false, true>(hips, oips, n, *p, seav, ldca, st);
 }
 
+extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                        const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                        uint32_t max_blocks_per_sm, void* stream);
+
 extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                                  void* pool, uint32_t ts_bytes, uint64_t now_wrapped, void* stream) {
+  return sspd_scan_sliding_capped(hips, oips, n, p, pool, ts_bytes, now_wrapped, 0, stream);
+}
+
+extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                        const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                        uint32_t max_blocks_per_sm, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
   if (n == 0) return SSPD_OK;
@@ -276,7 +286,18 @@ extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uin
         float frac = 0.85f;
         if (const char* e = getenv("SSPD_SLIDE_L2_FRAC")) frac = (float)atof(e);
         frac = frac < 0.f ? 0.f : (frac > 1.f ? 1.f : frac);
-        const int grid = grid_for(scan_sliding_u16_fast_kernel, 256, (n + 3) / 4);
+        int grid = grid_for(scan_sliding_u16_fast_kernel, 256, (n + 3) / 4);
+        // optional cap (blocks per SM) so kernels on other streams (the
+        // pipelined detect) stay co-resident with this store-bound scan
+        uint32_t cap_bps = max_blocks_per_sm;
+        if (const char* e = getenv("SSPD_SLIDE_BLOCKS_PER_SM")) cap_bps = (uint32_t)atoi(e);
+        if (cap_bps) {
+          int dev = 0, sms = 148;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          const int cap = (int)cap_bps * sms;
+          if (grid > cap) grid = cap;
+        }
         scan_sliding_u16_fast_kernel<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool,
                                                             (uint16_t)now_wrapped, frac);
         break;

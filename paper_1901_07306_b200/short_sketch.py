@@ -242,6 +242,16 @@ class SeavSketch:
         self._params = build_params(config, _ldca_config or LdcaConfig(lr=1, lc=1, k=8), seeds)
         self._buf = zeros_bytes(config.memory_bytes())
         self._cand_cap = 1 << 14
+        self._scratch_buf = None
+
+    def _scratch(self, nbytes: int):
+        """Device work space of the fused finalize, kept across windows
+        (stream-ordered reuse); grows on demand."""
+        import torch
+
+        if self._scratch_buf is None or self._scratch_buf.numel() < nbytes:
+            self._scratch_buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self._buf.device)
+        return self._scratch_buf
 
     # -- state access ------------------------------------------------------
     @property

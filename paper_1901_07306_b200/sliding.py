@@ -13,6 +13,7 @@ view (K4), restores (K5) and filters straight from the pool (K6 sliding).
 
 from __future__ import annotations
 
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -20,7 +21,7 @@ import numpy as np
 from .errors import ConfigError
 from .long_sketch import ldc_estimate
 from .short_sketch import SeavSketch
-from .window_detector import DetectionReport, DetectorParams, ReportList, filter_candidates
+from .window_detector import DetectionReport, DetectorParams, DeviceFinalize, ReportList
 
 _UNSIGNED = ((1, np.uint8), (2, np.uint16), (4, np.uint32), (8, np.uint64))
 
@@ -182,6 +183,8 @@ class _SlotLayout:
 class SlidingDetector:
     """Sliding-window pipeline over one device timestamp pool (sliding.py:128-248)."""
 
+    pipelined_scan_blocks_per_sm = 2  # K2 grid cap while detect_async runs (measured best on B200)
+
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
         from ._abi import build_params
@@ -218,8 +221,11 @@ class SlidingDetector:
         if h.numel() != o.numel():
             raise ConfigError("hips and oips differ in length")
         pool = self.pool
-        call("sspd_scan_sliding", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
-             pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), stream_ptr())
+        # once detection is pipelined (detect_async), the scan leaves SM room
+        # for the finalize kernels running on the side stream
+        cap = self.pipelined_scan_blocks_per_sm if getattr(self, "_async", None) else 0
+        call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+             pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
         self.pair_count += int(h.numel())
 
     def observe(self, hip: int, oip: int):
@@ -270,7 +276,11 @@ class SlidingDetector:
         return ldc_estimate(int(z0.item()) & 0xFFFFFFFF, self.ldca_config.k)
 
     def detect(self, beta: float | None = None) -> list[DetectionReport]:
-        """Materialise (K4) -> restore (K5) -> filter on the pool (K6) (sliding.py:232-248)."""
+        """Materialise (K4: SEAV registers + packed LDCA) -> fused finalize
+        (K5 restore, sort, K6 filter, compaction; one host round trip)
+        (sliding.py:232-248)."""
+        from ._device import call, stream_ptr, zeros_bytes
+
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
         seav = getattr(self, "_view", None)  # reused across slides: K4 overwrites every register
@@ -278,17 +288,101 @@ class SlidingDetector:
             seav = self._view = self.materialize_seav()
         else:
             self._materialize_into(seav)
-        pool = self.pool
-        k = self.ldca_config.k
         lview = getattr(self, "_ldca_view", None)
         if lview is None:
-            from ._device import zeros_bytes
-
             lview = self._ldca_view = zeros_bytes(self._params.ldca_bytes)
-        ips, z0s = filter_candidates(
-            seav, None, self._params, k, cutoff,
-            sliding=(pool.device_buffer(), pool.ts_bytes, pool._wrapped_now(), pool.window_slices, lview))
-        return ReportList(ips, z0s, k, self.now, "sliding")
+        pool = self.pool
+        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
+        fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff)
+        return fin.reports(self.now, "sliding")
+
+    def detect_async(self, beta: float | None = None) -> PendingReports:
+        """`detect()` pipelined with the caller's next slices.
+
+        The active-bit views (K4: SEAV registers + packed LDCA) are built on
+        the caller's stream, so the next `observe_batch` -- which rewrites
+        stamps -- is ordered after them; the fused finalize (K5 restore,
+        sort, K6 filter on the LDCA view, compaction) is enqueued on a side
+        stream, with no host round trip, and overlaps the next slices' scans
+        (K2 is bound by random-store traffic, K5 by issue slots).  Two view
+        sets alternate; a set is reused only after the finalize that read it
+        has been resolved.  The list resolves on first access; same reports
+        as `detect()` (window_id = the slice of this call)."""
+        import torch
+
+        from ._device import call, stream_ptr, zeros_bytes
+
+        beta = self.params.beta if beta is None else beta
+        cutoff = beta * self.params.theta
+        st = _async_state(self)
+        i = st["n"] % 2
+        st["n"] += 1
+        vset = st["sets"][i]
+        if vset is None:
+            vset = st["sets"][i] = [self.materialize_seav(), zeros_bytes(self._params.ldca_bytes), None]
+        elif vset[2] is not None:
+            vset[2].resolve()  # the finalize two calls ago is done with this view set
+        seav, lview = vset[0], vset[1]
+        pool = self.pool
+        self._materialize_into(seav)
+        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
+        views_ready = torch.cuda.Event()
+        views_ready.record(torch.cuda.current_stream())
+        side = st["side"]
+        side.wait_event(views_ready)
+        fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff, stream=side)
+        vset[2] = fin
+        now = self.now
+        return PendingReports(lambda: fin.reports(now, "sliding"))
+
+
+class PendingReports(Sequence):
+    """Report list of `SlidingDetector.detect_async`: the device pipeline
+    runs on a side stream; the first access waits for it, then this
+    behaves exactly like the ReportList `detect()` returns."""
+
+    __slots__ = ("_resolve", "_value")
+
+    def __init__(self, resolve):
+        self._resolve = resolve
+        self._value = None
+
+    def result(self) -> ReportList:
+        if self._value is None:
+            self._value = self._resolve()
+            self._resolve = None
+        return self._value
+
+    def done(self) -> bool:
+        return self._value is not None
+
+    def __len__(self) -> int:
+        return len(self.result())
+
+    def __getitem__(self, i):
+        return self.result()[i]
+
+    def __iter__(self):
+        return iter(self.result())
+
+    def __eq__(self, other) -> bool:
+        return self.result() == (other.result() if isinstance(other, PendingReports) else other)
+
+    def __repr__(self) -> str:
+        return f"PendingReports({self.result()!r})" if self.done() else "PendingReports(<running>)"
+
+
+def _async_state(det):
+    """Side stream and two view sets (double buffering)."""
+    st = getattr(det, "_async", None)
+    if st is None:
+        import torch
+
+        st = det._async = {"side": torch.cuda.Stream(device=torch.cuda.current_device()), "sets": [None, None],
+                           "n": 0}
+    return st
 
 
 def detect_sliding(detector: SlidingDetector, theta: int | None = None, beta: float | None = None):

@@ -66,20 +66,38 @@ class ReportList(Sequence):
     Behaves like the reference's list[DetectionReport] (len, iteration,
     indexing, ==, `list += reports`); objects are only created when touched,
     so a window with tens of thousands of saturated candidates does not pay
-    Python object construction unless the caller asks for them."""
+    Python object construction unless the caller asks for them.  A list
+    made by the fused device finalize knows its length from the device
+    counts and copies the (ip, z0) arrays to the host on first access."""
 
-    __slots__ = ("ips", "z0s", "k", "window_id", "source", "_est")
+    __slots__ = ("_ips", "_z0s", "k", "window_id", "source", "_est", "_n", "_fetch")
 
-    def __init__(self, ips: np.ndarray, z0s: np.ndarray, k: int, window_id: int, source: str):
-        self.ips = ips
-        self.z0s = z0s
+    def __init__(self, ips, z0s, k: int, window_id: int, source: str, n: int | None = None, fetch=None):
+        self._ips = ips
+        self._z0s = z0s
+        self._n = n
+        self._fetch = fetch
         self.k = k
         self.window_id = window_id
         self.source = source
         self._est = estimate_table(k)
 
+    def _arrays(self):
+        if self._ips is None:
+            self._ips, self._z0s = self._fetch()
+            self._fetch = None
+        return self._ips, self._z0s
+
+    @property
+    def ips(self) -> np.ndarray:
+        return self._arrays()[0]
+
+    @property
+    def z0s(self) -> np.ndarray:
+        return self._arrays()[1]
+
     def __len__(self) -> int:
-        return len(self.ips)
+        return self._n if self._n is not None else len(self.ips)
 
     def _make(self, i: int) -> DetectionReport:
         z0 = int(self.z0s[i])
@@ -173,77 +191,97 @@ def device_keep_table(k: int, cutoff: float):
     return t
 
 
-def filter_candidates(seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: float,
-                      on_overflow: str = "warn", sliding=None):
-    """Device restore -> sort -> z0 filter -> stable compaction.
+class DeviceFinalize:
+    """One fused finalize (`sspd_finalize`: K5 restore -> sort -> K6 filter ->
+    compaction) enqueued on a stream without any host round trip.
 
-    Returns host lists (ips, z0s) of the kept candidates, sorted by ip, and
-    warns (or raises) once per overflowed register array like
-    SeavSketch.restore(on_overflow) (short_sketch.py:392-408).
-    `sliding` = (pool, ts_bytes, now_wrapped, window) to read the LDCA from
-    a timestamp pool instead of a packed buffer.
-    """
-    import torch
+    The candidate capacity is the sketch's learned `_cand_cap`; the two
+    device counts and the overflow flags are copied asynchronously into
+    pinned memory.  `resolve()` waits for them (one synchronisation), re-runs
+    with a larger capacity in the rare case the candidates did not fit (the
+    inputs must still be intact: callers resolve before reusing them), and
+    emits the reference's overflow warnings (short_sketch.py:398-407).
+    `reports()` then returns a ReportList whose arrays are copied on first
+    access."""
 
-    from ._device import call, stream_ptr
-    from .errors import SeaOverflowError
+    def __init__(self, seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: float, stream=None,
+                 on_overflow: str = "warn"):
+        import torch
 
-    ip, aux, overflow = seav._restore_device(0, 1 << seav.config.r)
-    n = ip.numel()
+        self.seav, self.ldca, self.p, self.k, self.cutoff = seav, ldca_buf, params_block, k, cutoff
+        self.stream = stream or torch.cuda.current_stream()
+        self.on_overflow = on_overflow
+        self.m = None
+        self._launch(max(1024, seav._cand_cap))
 
-    def check_overflow(flags: np.ndarray):
-        for rp in np.nonzero(flags)[0].tolist():
-            err = SeaOverflowError(rp, seav.restore_cap)
-            if on_overflow != "warn":
+    def _launch(self, cap: int):
+        import torch
+
+        from ._device import call
+
+        seav = self.seav
+        self.cap = cap
+        with torch.cuda.stream(self.stream):
+            dev = seav._buf.device
+            table = device_keep_table(self.k, self.cutoff)
+            self.out = torch.empty(2 * cap + 4, dtype=torch.int32, device=dev)  # ip | z0 | counts (2 x u64)
+            ovf = torch.empty(1 << seav.config.r, dtype=torch.uint8, device=dev)
+            need = ctypes.c_size_t(0)
+            call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None,
+                 ctypes.byref(need), 0)
+            scratch = seav._scratch(need.value)
+            call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
+                 table.data_ptr(), cap, self.out.data_ptr(), self.out[cap:].data_ptr(),
+                 self.out[2 * cap:].data_ptr(), ovf.data_ptr(), scratch.data_ptr(), ctypes.byref(need),
+                 self.stream.cuda_stream)
+            self.h_counts = torch.empty(4, dtype=torch.int32, pin_memory=True)
+            self.h_ovf = torch.empty(ovf.numel(), dtype=torch.uint8, pin_memory=True)
+            self.h_counts.copy_(self.out[2 * cap:], non_blocking=True)
+            self.h_ovf.copy_(ovf, non_blocking=True)
+            self.event = torch.cuda.Event()
+            self.event.record(self.stream)
+
+    def resolve(self) -> int:
+        """Number of reports (waits for the device counts; idempotent)."""
+        if self.m is not None:
+            return self.m
+        from .errors import SeaOverflowError
+
+        self.event.synchronize()
+        found, kept = (int(x) for x in self.h_counts.numpy().view(np.int64))
+        if found > self.cap:  # candidates did not fit: learn the size, run again
+            self.seav._cand_cap = 1 << (found - 1).bit_length()
+            self._launch(self.seav._cand_cap)
+            self.event.synchronize()
+            found, kept = (int(x) for x in self.h_counts.numpy().view(np.int64))
+        for rp in np.nonzero(self.h_ovf.numpy())[0].tolist():
+            err = SeaOverflowError(rp, self.seav.restore_cap)
+            if self.on_overflow != "warn":
                 raise err
             warnings.warn(str(err), RuntimeWarning, stacklevel=4)
+        self.m = kept
+        return kept
 
-    if n == 0:
-        check_overflow(overflow.cpu().numpy())
-        return np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32)
-    dev = ip.device
-    table = device_keep_table(k, cutoff)
-    z0 = torch.empty(n, dtype=torch.int32, device=dev)
-    keep = torch.empty(n, dtype=torch.uint8, device=dev)
-    if sliding is None:
-        call("sspd_filter", ldca_buf.data_ptr(), params_block, ip.data_ptr(), n, table.data_ptr(),
-             z0.data_ptr(), keep.data_ptr(), stream_ptr())
-    else:
-        pool, ts_bytes, now_w, window = sliding[:4]
-        view = sliding[4] if len(sliding) > 4 else None
-        if view is not None and n > params_block.lc:
-            # many candidates re-read the same LDCA cells: materialize the
-            # active-bit view once (K4, one pass over the LDCA stamps) and
-            # filter on packed bits; few candidates read their cells' stamps
-            # directly (K6 sliding)
-            call("sspd_materialize_ldca", pool.data_ptr(), ts_bytes, params_block, now_w, window,
-                 view.data_ptr(), stream_ptr())
-            call("sspd_filter", view.data_ptr(), params_block, ip.data_ptr(), n, table.data_ptr(),
-                 z0.data_ptr(), keep.data_ptr(), stream_ptr())
-        else:
-            call("sspd_filter_sliding", pool.data_ptr(), ts_bytes, params_block, now_w, window,
-                 ip.data_ptr(), n, table.data_ptr(), z0.data_ptr(), keep.data_ptr(), stream_ptr())
-    out = torch.empty(2 * n + 2, dtype=torch.int32, device=dev)  # [ip_out | z0_out | count (i64)]
-    ip_out, z0_out = out[:n], out[n:2 * n]
-    cnt = out[2 * n:].view(torch.int64)
-    need = ctypes.c_size_t(0)
-    call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
-         z0_out.data_ptr(), cnt.data_ptr(), None, ctypes.byref(need), stream_ptr())
-    scratch = torch.empty(max(16, need.value), dtype=torch.uint8, device=dev)
-    call("sspd_compact_reports", ip.data_ptr(), z0.data_ptr(), keep.data_ptr(), n, ip_out.data_ptr(),
-         z0_out.data_ptr(), cnt.data_ptr(), scratch.data_ptr(), ctypes.byref(need), stream_ptr())
-    # ONE device->host round trip for the results, their count and the
-    # restore overflow flags (pinned staging, asynchronous copies)
-    host = torch.empty(out.numel(), dtype=torch.int32, pin_memory=True)
-    host_ovf = torch.empty(overflow.numel(), dtype=torch.uint8, pin_memory=True)
-    host.copy_(out, non_blocking=True)
-    host_ovf.copy_(overflow, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    check_overflow(host_ovf.numpy())
-    h = host.numpy()
-    m = int(h[2 * n:].view(np.int64)[0])
-    both = h[:2 * n].view(np.uint32)
-    return both[:m].copy(), both[n:n + m].copy()
+    def _fetch(self):
+        import torch
+
+        m, cap = self.m, self.cap
+        host = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            host[:m].copy_(self.out[:m], non_blocking=True)
+            host[m:].copy_(self.out[cap:cap + m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        ev.synchronize()
+        both = host.numpy().view(np.uint32)
+        self.out = None
+        return both[:m].copy(), both[m:].copy()
+
+    def reports(self, window_id: int, source: str) -> "ReportList":
+        m = self.resolve()
+        if m == 0:
+            return ReportList(np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32), self.k, window_id, source)
+        return ReportList(None, None, self.k, window_id, source, n=m, fetch=self._fetch)
 
 
 @dataclass
@@ -365,8 +403,8 @@ class DetectorState:
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.theta
         k = self.ldca.config.k
-        ips, z0s = filter_candidates(self.seav, self.ldca.device_buffer(), self.seav._params, k, cutoff)
-        return ReportList(ips, z0s, k, self.window_id, source)
+        fin = DeviceFinalize(self.seav, self.ldca.device_buffer(), self.seav._params, k, cutoff)
+        return fin.reports(self.window_id, source)
 
     def reset(self):
         self.seav.clear()

@@ -237,3 +237,34 @@ def test_views_fast_paths_vs_oracle(cuda, oracle, r):
         assert got_s == want_s.tobytes(), now
         assert got_l == want_l.tobytes(), now
         torch.cuda.synchronize()
+
+
+def test_detect_async_equals_detect(cuda):
+    """detect_async (views on the caller's stream, K5/K6 on a side stream,
+    two alternating view sets) returns exactly detect()'s lists, slide by
+    slide, while later slices keep rewriting the pool."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5)
+    w = 20
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=w)
+        b = SlidingDetector(params, window_slices=w)
+    rng = np.random.default_rng(2024)
+    heavy = rng.integers(0, 2**32, size=6, dtype=np.uint64)
+    pending, sync = [], []
+    for s in range(60):
+        n = int(rng.integers(1_000, 40_000))
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        hips[: n // 4] = heavy[(s // 10) % len(heavy)]  # heavy hosts come and go
+        a.observe_batch(hips, oips)
+        b.observe_batch(hips, oips)
+        pending.append(a.detect_async())
+        sync.append(rep_list(b.detect()))
+        a.advance_slice()
+        b.advance_slice()
+    got = [rep_list(p) for p in pending]
+    assert got == sync
+    assert sum(len(x) for x in sync) > 0
