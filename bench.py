@@ -490,6 +490,8 @@ def run_sliding(args) -> dict:
         warnings.simplefilter("ignore")
         det = SlidingDetector(DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=1024, design_n=2.15e8),
                               window_slices=300)
+    if os.environ.get("SSPD_PIPELINE_DEPTH"):
+        det.pipeline_depth = int(os.environ["SSPD_PIPELINE_DEPTH"])
     stream = torch.cuda.current_stream()
     counts = []
 

@@ -184,6 +184,7 @@ class SlidingDetector:
     """Sliding-window pipeline over one device timestamp pool (sliding.py:128-248)."""
 
     pipelined_scan_blocks_per_sm = 2  # K2 grid cap while detect_async runs (measured best on B200)
+    pipeline_depth = 2  # view sets of detect_async (detects in flight)
 
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
@@ -316,13 +317,18 @@ class SlidingDetector:
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
         st = _async_state(self)
-        i = st["n"] % 2
+        if len(st["sets"]) != self.pipeline_depth:
+            for vs in st["sets"]:
+                if vs is not None and vs[2] is not None:
+                    vs[2].resolve()
+            st["sets"] = [None] * max(1, self.pipeline_depth)
+        i = st["n"] % len(st["sets"])
         st["n"] += 1
         vset = st["sets"][i]
         if vset is None:
             vset = st["sets"][i] = [self.materialize_seav(), zeros_bytes(self._params.ldca_bytes), None]
         elif vset[2] is not None:
-            vset[2].resolve()  # the finalize two calls ago is done with this view set
+            vset[2].resolve()  # the finalize `pipeline_depth` calls ago is done with this view set
         seav, lview = vset[0], vset[1]
         pool = self.pool
         self._materialize_into(seav)
