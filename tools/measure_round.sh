@@ -9,10 +9,14 @@ OUT=gpurun_out/round
 mkdir -p "$OUT"
 export PATH=/usr/local/cuda/bin:$PATH
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
+timeout 900 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest=$?"
 timeout 600 python bench.py > "$OUT/bench_config2.json" 2> "$OUT/bench_config2.err"; echo "bench=$?"
 timeout 600 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"; echo "ref=$?"
 timeout 900 python bench.py --config 3 --steps 3 --warmup 1 > "$OUT/bench_config3.json" 2> "$OUT/bench_config3.err"; echo "c3=$?"
 timeout 600 python bench.py --config 4 --steps 3 --warmup 1 > "$OUT/bench_config4.json" 2> "$OUT/bench_config4.err"; echo "c4=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 2500 -c 150 --csv \
+  --log-file "$OUT/launches_config4.csv" python bench.py --config 4 --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1
+echo "launches4=$?"
 timeout 900 python bench.py --config 5 --steps 1 --warmup 1 > "$OUT/bench_config5.json" 2> "$OUT/bench_config5.err"; echo "c5=$?"
 # K1p metric dump on the config-2 window (duration, DRAM bytes, warp instructions)
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,lts__t_requests_srcunit_tex_op_red.sum \

@@ -48,6 +48,7 @@ def main():
     for setting in args.settings:
         st.scan_mode = "direct" if setting == "direct" else "partitioned"
         env = {} if setting == "direct" else dict(kv.split("=", 1) for kv in setting.split(",") if kv)
+        st.partitioned_chunk = int(env.pop("chunk", 0))  # packets per chunk (0 = library default)
         for k in [k for k in os.environ if k.startswith("SSPD_PART_")]:
             del os.environ[k]
         os.environ.update(env)
