@@ -23,7 +23,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --clock-control none -k regex:scan_partitioned -c 2 --csv --log-file "$OUT/ncu_metrics_partitioned.csv" \
   python tools/sweep_k1p.py --reps 1 "" > /dev/null 2>&1; echo "ncu_metrics=$?"
 # launch list of the default bench step (every kernel of the step)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:sspd::|CUB_' -c 66 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k 'regex:sspd::|CUB_200802' -c 66 --csv \
   --log-file "$OUT/launches_config2.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 echo "launches=$?"
 # full capture of the dominant kernel
