@@ -271,3 +271,45 @@ def test_compaction_is_stable(cuda, n):
         assert m == int(want.sum())
         assert (ip_o[:m].cpu().numpy() == ip.cpu().numpy()[want]).all()
         assert (z0_o[:m].cpu().numpy() == z0.cpu().numpy()[want]).all()
+
+
+@pytest.mark.slow
+def test_config2_full_window_bit_exact_vs_oracle(cuda, oracle):
+    """The bench workload itself (BASELINE configs[1]: 268,435,456 packets,
+    SEAV r=12, LDCA 8 MiB) through the default scan (K1p) and the fused
+    finalize: SEAV/LDCA bytes and the full report list (ips, estimates,
+    saturation) equal the CPU oracle's, bit for bit."""
+    import hashlib
+    import math
+
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams
+    from tools.workloads import CONFIG2, generate
+
+    dp = DetectorParams(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=80.5e6)
+    _, _, p = params_block(dp)
+    hips, oips, supers = generate(CONFIG2, "torch", cuda)
+    st = make_state(dp)
+    st.process_batch(hips, oips)
+    assert st.last_scan == "partitioned"
+    reps = st.finalize_window()
+    got = [(r.ip, r.estimated_cardinality, r.saturated) for r in reps]
+    h = hips.cpu().numpy().view(np.uint32)
+    o = oips.cpu().numpy().view(np.uint32)
+    del hips, oips
+    torch.cuda.empty_cache()
+    seav, ldca = oracle.scan(p, h, o, threads=oracle.cpu_threads())
+    sha = lambda b: hashlib.sha256(bytes(b)).hexdigest()  # noqa: E731
+    assert sha(st.seav.payload_bytes()) == sha(seav.tobytes())
+    assert sha(st.ldca.payload_bytes()) == sha(ldca.tobytes())
+    ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+    z0 = oracle.filter_z0(p, ldca, ips)
+    k = dp.k
+    want = []
+    for ip, z in zip(ips.tolist(), z0.tolist()):
+        est, sat = (k * math.log(k), True) if z == 0 else (-k * math.log(z / k), False)
+        if sat or est >= dp.beta * dp.theta:
+            want.append((int(ip), est, sat))
+    assert got == want
+    assert set(supers.tolist()) <= {r[0] for r in got}
