@@ -268,3 +268,64 @@ def test_detect_async_equals_detect(cuda):
     got = [rep_list(p) for p in pending]
     assert got == sync
     assert sum(len(x) for x in sync) > 0
+
+
+@pytest.mark.slow
+def test_config4_scaled_trace_vs_oracle(cuda, oracle):
+    """Config 4 at 1/8 scale (2^26 timestamped packets over ~298 one-second
+    slices, w = 300, r = 16, LDCA 8 MiB), driven exactly like the bench
+    (observe per slice, pipelined detect_async at EVERY slide): the pool
+    bytes at the end and the report lists at sampled slides equal the
+    oracle's (observe -> materialize -> restore -> filter), bit for bit."""
+    import hashlib
+    import math
+
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+    from tools.workloads import CONFIG4, CONFIG4_TIMING, TimingSpec, generate, scaled
+
+    spec = scaled(CONFIG4, 8)
+    timing = TimingSpec(rate_pps=spec.n_packets / (CONFIG4.n_packets / CONFIG4_TIMING.rate_pps))
+    hips, oips, supers, ts = generate(spec, "torch", cuda, timing=timing)
+    slices = (ts // 1000).cpu().numpy()
+    n_sl = int(slices[-1]) + 1
+    bounds = np.searchsorted(slices, np.arange(n_sl + 1))
+    dp = DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=1024, design_n=2.7e7)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(dp, window_slices=300)
+    p = det._params
+    h_np = hips.cpu().numpy().view(np.uint32)
+    o_np = oips.cpu().numpy().view(np.uint32)
+    pool = det.pool.ts.copy()
+    check = {n_sl // 4, n_sl // 2, n_sl - 1}
+    pending, want = {}, {}
+    for s in range(n_sl):
+        lo, hi = int(bounds[s]), int(bounds[s + 1])
+        if hi > lo:
+            det.observe_batch(hips[lo:hi], oips[lo:hi])
+            oracle.observe(p, h_np[lo:hi], o_np[lo:hi], pool, det.pool._wrapped_now())
+        pending[s] = det.detect_async()
+        if s in check:
+            now, w = det.pool._wrapped_now(), det.pool.window_slices
+            seav = oracle.materialize_seav(p, pool, now, w)
+            ldca = oracle.materialize_ldca(p, pool, now, w)
+            ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+            z0 = oracle.filter_z0(p, ldca, ips)
+            k = dp.k
+            rows = []
+            for ip, z in zip(ips.tolist(), z0.tolist()):
+                est, sat = (k * math.log(k), True) if z == 0 else (-k * math.log(z / k), False)
+                if sat or est >= dp.beta * dp.theta:
+                    rows.append((int(ip), est, sat))
+            want[s] = rows
+        det.advance_slice()
+    torch.cuda.synchronize()
+    sha = lambda b: hashlib.sha256(bytes(b)).hexdigest()  # noqa: E731
+    assert sha(det.pool.ts.tobytes()) == sha(pool.tobytes())
+    for s, rows in want.items():
+        got = [(r.ip, r.estimated_cardinality, r.saturated) for r in pending[s]]
+        assert got == rows, s
+        assert all(r.window_id == s for r in list(pending[s])[:3])
+    assert sum(len(pending[s]) for s in pending) > 0
