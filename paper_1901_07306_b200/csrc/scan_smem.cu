@@ -66,12 +66,31 @@ __device__ __noinline__ void reapply_direct(const sspd_params& p, uint32_t lc_ma
 }
 
 
+// SEAV update of one sampled packet (short_sketch.py:300-318): SR direct reds.
+__device__ __forceinline__ void seav_update(const sspd_params& p, uint32_t hip, uint32_t oip, uint32_t* seav) {
+  const uint32_t sbit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+  const uint64_t rp = hip & ((1u << p.r) - 1u);
+  const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+    const uint64_t abs_bit = (p.seav_row_off[i] + (rp * p.sc[i] + col) * p.reg_bytes) * 8 + sbit;
+    red_or_g(seav + (abs_bit >> 5), 1u << (abs_bit & 31));
+  }
+}
+__device__ __noinline__ void seav_update_ool(const sspd_params& p, uint32_t hip, uint32_t oip, uint32_t* seav) {
+  seav_update(p, hip, oip, seav);
+}
+
 #ifndef SSPD_PART_THREADS
 #define SSPD_PART_THREADS 1024
 #endif
 constexpr uint32_t kThreads = SSPD_PART_THREADS;
 constexpr uint32_t kPktPerThread = 4;  // packets per thread per tile (= one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPktPerThread;
+// sampled packets (0.78 % at tau = 7, ~32 per tile) are queued in shared
+// memory and their SEAV updates applied by all lanes after the tile, instead
+// of one divergent lane per warp inside the hashing loop
+constexpr uint32_t kSeavQueue = 128;  // per tile parity
 
 // Producer routing modes, chosen per launch by the host plan:
 //   kGeneric  64-bit index math, any k / lc (exact 64-bit modulo)
@@ -112,7 +131,8 @@ __device__ __forceinline__ uint64_t slice_start(const PartPlan& P, uint64_t c0, 
   return min(c1, c0 + off);
 }
 
-// Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor | sink]
+// Shared memory: [part_words | nparts*stage_slots staging | nparts cnt | nparts cursor | sink
+//                 | sampled-packet queue (count + kSeavQueue (hip, oip) pairs)]
 template <bool kSeav, int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_partitioned_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
@@ -124,6 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* cnt = stage + (size_t)P.nparts * P.stage_slots;
   uint32_t* cursor = cnt + P.nparts;
   uint32_t* sink = cursor + P.nparts;  // dummy target for overflowing staging writes
+  uint32_t* sq_cnt = sink + 4;         // [2] queue counts by tile parity (16-B aligned)
+  uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [2][kSeavQueue]
   cg::grid_group grid = cg::this_grid();
   const uint32_t self = blockIdx.x;
   const uint32_t tid = threadIdx.x;
@@ -134,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
   for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = cursor[i] = 0;
+  if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
   __syncthreads();
 
   const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
@@ -205,7 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       uint32_t nh[kPktPerThread], no[kPktPerThread];
       fetch(lo + (uint64_t)tid * kPktPerThread, nh, no);
-      for (uint64_t base = lo; base < hi; base += kTile) {
+      uint32_t par = 0;  // tile parity: selects the sampled-packet queue
+      for (uint64_t base = lo; base < hi; base += kTile, par ^= 1u) {
         uint32_t ch[kPktPerThread], co[kPktPerThread];
 #pragma unroll
         for (uint32_t e = 0; e < kPktPerThread; ++e) {
@@ -276,18 +300,22 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (kSeav && sampled(oip, p.seed_h1, tmask)) {
-              const uint32_t sbit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
-              const uint64_t rp = hip & ((1u << p.r) - 1u);
-              const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
-              for (uint32_t i = 0; i < p.sr; ++i) {
-                const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
-                const uint64_t abs_bit = (p.seav_row_off[i] + (rp * p.sc[i] + col) * p.reg_bytes) * 8 + sbit;
-                red_or_g(seav + (abs_bit >> 5), 1u << (abs_bit & 31));
-              }
+              const uint32_t qs = atomicAdd(sq_cnt + par, 1u);
+              if (qs < kSeavQueue)
+                sq_base[par * kSeavQueue + qs] = make_uint2(hip, oip);
+              else
+                seav_update_ool(p, hip, oip, seav);  // queue full (a skewed tile): apply now
             }
           }
         }
         __syncthreads();
+        if (kSeav) {  // the tile's sampled packets, all lanes busy
+          const uint32_t nq = min(sq_cnt[par], kSeavQueue);
+          const uint2* sq = sq_base + par * kSeavQueue;
+          for (uint32_t i = tid; i < nq; i += kThreads) seav_update(p, sq[i].x, sq[i].y, seav);
+          // the previous tile's queue was fully read before this barrier
+          if (tid == 0) sq_cnt[par ^ 1u] = 0;
+        }
         // flush: a group of G = 2^gshift threads per destination (8 when
         // there are 128 destinations) copies the run as aligned 16-B stores
         // into this CTA's own region of the destination bucket (no global
@@ -333,6 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncthreads();
       }
+      if (kSeav) {  // queues restart at parity 0 with the next chunk's slice
+        __syncthreads();
+        if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+      }
       // publish this CTA's run lengths for chunk t and reset the cursors
       for (uint32_t q = tid; q < np; q += kThreads) {
         __stcg(P.counts + ((size_t)b * np + q) * ns + self, cursor[q]);
@@ -373,7 +405,7 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
     return ((uint32_t)(mean + sig * __builtin_sqrt(mean) + 8.0) + 3u) & ~3u;
   };
   auto fits = [&](uint32_t nparts, uint32_t pw, uint32_t slots) {
-    smem = 4ull * (pw + (uint64_t)nparts * slots + 2ull * nparts + 4);
+    smem = 4ull * (pw + (uint64_t)nparts * slots + 2ull * nparts + 8 + 4ull * kSeavQueue);
     return (int64_t)smem <= max_smem && pw < (1u << 27);
   };
   mode = pow2_kl ? kFast32 : kGeneric;
