@@ -459,10 +459,11 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   // pure producers (no partition) take a larger slice: consumers also drain
   // their buckets.  Weight ratio (x64) tunable with SSPD_PART_WEIGHT.
   P.w_owner = 64;
-  P.w_other = 76;
+  P.w_other = 80;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
-  // default chunk: 4 tiles per producer, so slices are (nearly) whole tiles
-  P.chunk = chunk ? chunk : (uint64_t)P.nsrc * kTile * 4;
+  // default chunk: 8 tiles per producer (measured best together with w_other = 80),
+  // so slices are (nearly) whole tiles
+  P.chunk = chunk ? chunk : (uint64_t)P.nsrc * kTile * 8;
   const double share = (double)P.w_other / ((double)P.nparts * P.w_owner + (double)(P.nsrc - P.nparts) * P.w_other);
   const double rmean = (double)P.chunk * p->lr * share / P.nparts;  // largest producer -> one destination
   P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
