@@ -25,11 +25,15 @@
 // registers are all hot, so the count is order-independent: pass 1 counts
 // (stopping early once the shared total exceeds cap), pass 2 emits the
 // weight >= 3 tuples only for SEAs that did not overflow.
+#include <cooperative_groups.h>
+#include <cooperative_groups/details/partitioning.h>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 #include "sspd_common.cuh"
 #include "launch.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sspd {
 
@@ -131,8 +135,15 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
     auto leaf = [&](uint64_t lp, uint64_t acc_and) {
       if (kEmit) {
         const uint32_t wgt = (uint32_t)__popcll(acc_and);
+        // warp-aggregated slot reservation: the lanes that reach a leaf
+        // together take one global atomic (a single counter is shared by
+        // every SEA, so per-candidate atomics would serialise at L2)
+        cg::coalesced_group leaves = cg::coalesced_threads();
+        const cg::coalesced_group keep = cg::binary_partition(leaves, wgt >= 3);
         if (wgt >= 3) {
-          const unsigned long long slot = atomicAdd(out_count, 1ull);
+          unsigned long long base = 0;
+          if (keep.thread_rank() == 0) base = atomicAdd(out_count, (unsigned long long)keep.size());
+          const unsigned long long slot = keep.shfl(base, 0) + keep.thread_rank();
           if (slot < out_capacity) {
             out_ip[slot] = (uint32_t)((lp << P.r) | rp);
             out_aux[slot] = (rp << 8) | wgt;
