@@ -426,7 +426,8 @@ def run_gpu(args) -> dict | None:
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32 keys / u8 bit arrays (integer)",
         "data": "synthetic (seeded counter-based generator, tools/workloads.py; no CAIDA traces offline)",
-        "config": {"workload": WORKLOAD, "global_batch": world * n, "packets_per_gpu": n,
+        "config": {"workload": WORKLOAD if n == CONFIG2.n_packets else WORKLOAD.replace("268,435,456", f"{n:,}"),
+                   "global_batch": world * n, "packets_per_gpu": n,
                    "parallelism": f"dp{world} (one border router per GPU, OR-merge to rank 0)",
                    "l2": "inputs (2 GiB/window) exceed the 126 MB L2; no flush needed",
                    "seav_r": dp.r, "ldca": "LR=8 LC=1024 k=8192 (8 MiB)"},
