@@ -116,6 +116,7 @@ struct PartPlan {
   uint32_t magic32, sh32;  // floor(w / part_words) for 32-bit w (fast mode)
   uint32_t pshift, pmask;  // pow2 mode: partition of a bit index / its local bit
   uint32_t qshift;         // pow2 mode: partition of a cell index (pshift - log2k)
+  uint32_t s_lo[10], s_hg[10];  // split seeds (mix64_lo_split): H3, H1, LH0..7
   uint32_t vec_ok;         // hips/oips 16-byte aligned and chunk % 4 == 0
   uint32_t qstride;        // ns * region_cap: bucket elements per destination
   uint32_t gshift;         // log2 of the flush group size (threads per destination)
@@ -245,13 +246,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kMode == kPow2) {
               // LR = 8, k and lc powers of two, partitions of 2^pshift bits:
               // the staged entry is the bit index inside its partition
-              const uint32_t bb = (uint32_t)mix64(oip ^ p.seed_h3) & P.k_mask;
+              const uint32_t bb = mix64_lo_split(oip, P.s_lo[0], P.s_hg[0]) & P.k_mask;
               bool ovf = false;
 #pragma unroll
               for (uint32_t i = 0; i < 8; ++i) {
                 // partitions hold whole cells and rows hold whole partitions
                 // (plan): q = cell >> qshift, entry = (cell << log2k | b) & pmask
-                const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & P.lc_mask;
+                const uint32_t c = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
                 const uint32_t q = (i * p.lc + c) >> P.qshift;
                 const uint32_t slot = atomicAdd(&cnt[q], 1u);
                 const bool fits = slot < P.stage_slots;
@@ -299,7 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cell += p.lc;
               }
             }
-            if (kSeav && sampled(oip, p.seed_h1, tmask)) {
+            if (kSeav && (kMode == kPow2 ? (mix64_lo_split(oip, P.s_lo[1], P.s_hg[1]) & tmask) == 0u
+                                         : sampled(oip, p.seed_h1, tmask))) {
               const uint32_t qs = atomicAdd(sq_cnt + par, 1u);
               if (qs < kSeavQueue)
                 sq_base[par * kSeavQueue + qs] = make_uint2(hip, oip);
@@ -479,6 +481,14 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   P.k_mask = p->k - 1;
   P.lc_mask = p->lc - 1;
   P.log2k = ilog2_ceil(p->k);
+  {
+    const uint64_t seeds[10] = {p->seed_h3, p->seed_h1, p->seed_lh[0], p->seed_lh[1], p->seed_lh[2],
+                                p->seed_lh[3], p->seed_lh[4], p->seed_lh[5], p->seed_lh[6], p->seed_lh[7]};
+    for (int i = 0; i < 10; ++i) {
+      P.s_lo[i] = (uint32_t)seeds[i];
+      P.s_hg[i] = (uint32_t)(seeds[i] >> 32) + (uint32_t)(kGolden >> 32);
+    }
+  }
   P.qshift = 0;
   if (mode == kPow2) {
     // the cell form of the routing needs whole cells per partition and

@@ -27,6 +27,23 @@ SSPD_HD uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+#if defined(__CUDACC__)
+// Low 32 bits of mix64(key ^ seed) for a 32-bit key, with the seed split on
+// the host into s_lo (low word) and hg = s_hi + golden_hi: the first add of
+// SplitMix64 then reads both straight from the constant bank (no per-row
+// 64-bit seed load).  Same value as (uint32_t)mix64(key ^ seed).
+__device__ __forceinline__ uint32_t mix64_lo_split(uint32_t key, uint32_t s_lo, uint32_t hg) {
+  uint32_t zl, zh;
+  asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;"
+      : "=r"(zl), "=r"(zh)
+      : "r"(key ^ s_lo), "n"((uint32_t)(kGolden & 0xFFFFFFFFull)), "r"(hg));
+  uint64_t z = ((uint64_t)zh << 32) | zl;
+  z = (z ^ (z >> 30)) * kMixA;
+  z = (z ^ (z >> 27)) * kMixB;
+  return (uint32_t)(z ^ (z >> 31));
+}
+#endif
+
 SSPD_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #if defined(__CUDA_ARCH__)
   return __umul64hi(a, b);
