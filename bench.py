@@ -442,7 +442,9 @@ def run_gpu(args) -> dict | None:
                      "kernel": kname, "algorithmic_bytes_per_packet": 8,
                      "note": ("the packet stream is 8 B/pkt, so HBM is far from binding; the scan is bound by "
                               "SM instruction issue (ten SplitMix64 hashes per packet on the ALU pipe) -- "
-                              "see issue_roofline, and scan_roofline for the SURVEY's L2-atomic roofline")},
+                              "see issue_roofline, and scan_roofline for the SURVEY's L2-atomic roofline; `traffic` is "
+                              "the 8 B/pkt input plus the part of the 32 B/pkt shared-memory bucket exchange that "
+                              "spills from L2 with the default 8-tile chunks (DESIGN.md §3)")},
         "scan_roofline": {"bound": "l2_red", "l2_red_ops_per_s": round(red_per_s / 1e9, 2),
                           "reds_per_packet": round(reds_per_pkt, 4), "roofline_gpps": round(roof_pps / 1e9, 3),
                           "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / roof_pps, 4),
