@@ -27,6 +27,7 @@
 // weight >= 3 tuples only for SEAs that did not overflow.
 #include <cooperative_groups.h>
 #include <cooperative_groups/details/partitioning.h>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
@@ -639,7 +640,12 @@ extern "C" int sspd_restore(const uint8_t* seav, const sspd_params* p, uint32_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint32_t regs = 0;
   for (uint32_t i = 0; i < p->sr; ++i) regs += p->sc[i];
-  if (regs <= 512 && 4 * P.smem_bytes <= 48 * 1024) {  // small arrays: one warp per SEA
+  // arrays up to this many registers: one warp per SEA (r = 16 geometry,
+  // 65,536 small arrays); larger ones (r = 12: 512 registers) split each
+  // array's work list over a CTA -- measured 93 vs 213 us at config 2
+  uint32_t warp_regs = 256;
+  if (const char* e = getenv("SSPD_RESTORE_WARP_REGS")) warp_regs = (uint32_t)atoi(e);
+  if (regs <= warp_regs && 4 * P.smem_bytes <= 48 * 1024) {  // small arrays: one warp per SEA
     const uint32_t blocks = (rp_count + 3) / 4;
     restore_warp_kernel<<<blocks, 128, 4 * P.smem_bytes, st>>>(seav, P, rp_begin, rp_count, cap, out_ip, out_aux,
                                                                out_capacity, out_count, overflow);
