@@ -526,6 +526,34 @@ def run_sliding(args) -> dict:
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    # K2 alone over the same trace (observe + advance, same grid cap as in
+    # the timed run) against the measured random-u16-store rate at the LDCA
+    # stamp footprint: the store-bound roofline of the sliding scan
+    import ctypes
+
+    from paper_1901_07306_b200._abi import lib
+
+    det.reset()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for s in range(n_sl):
+        lo, hi = bounds[s], bounds[s + 1]
+        if hi > lo:
+            det.observe_batch(hips[lo:hi], oips[lo:hi])
+        det.advance_slice()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    scan_ms = s0.elapsed_time(s1)
+    lcfg = det.ldca_config
+    foot = 1 << max(1, (2 * lcfg.lr * lcfg.lc * lcfg.k - 1).bit_length())  # LDCA stamp bytes, pow2
+    sbuf = torch.empty(foot, dtype=torch.uint8, device=dev)
+    rate = ctypes.c_double(0.0)
+    lib().sspd_microbench_store16(sbuf.data_ptr(), foot, 8, 256, ctypes.byref(rate), stream.cuda_stream)
+    del sbuf
+    stores_pp = lcfg.lr + det.seav_config.sr / (1 << det.seav_config.tau)
+    scan_gpps = n / (scan_ms * 1e-3) / 1e9
+    store_roof = rate.value / stores_pp / 1e9
     # roofline of K2: 8 scattered 2-byte stores/packet into a 403 MB pool (> L2):
     # HBM sector read-modify-write bound (8 + 8.031 x 32 B)
     peaks = measured_peaks()
@@ -544,6 +572,14 @@ def run_sliding(args) -> dict:
         "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
                      "kernel": "whole trace (K2 + per-slide K4/K5/K6)", "bytes_per_packet_model": bytes_pp},
+        "scan_roofline": {"bound": "random_u16_store", "store_rate_gops": round(rate.value / 1e9, 2),
+                          "footprint_bytes": foot, "stores_per_packet": round(stores_pp, 4),
+                          "roofline_gpps": round(store_roof, 3), "achieved_gpps": round(scan_gpps, 3),
+                          "frac": round(scan_gpps / store_roof, 4), "scan_ms_per_trace": round(scan_ms, 3),
+                          "scan_share_of_step": round(scan_ms / ms, 4),
+                          "note": "K2 over the whole trace alone vs the live-measured random st.global.u16 rate at "
+                                  "the LDCA stamp footprint (the SURVEY's 265 B/pkt HBM model assumes peak "
+                                  "bandwidth for random 32 B sector writes)"},
         "clocks": clk, "detect": {"reports_total": counts[0] if counts else None, "slides": n_sl,
                                   "planted": len(supers)},
         "gen_s": round(t_gen, 2),

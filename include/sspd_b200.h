@@ -248,6 +248,10 @@ SSPD_API int sspd_route_pairs(const uint32_t* hips, const uint32_t* oips, uint64
  * bench.py for the L2-atomic term of the scan roofline. */
 SSPD_API int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
                         int iters, double* ops_per_s, void* stream);
+/* Random st.global.u16 rate over a `bytes` (power of two) footprint -- the
+ * measured roofline term of the sliding scan K2. */
+SSPD_API int sspd_microbench_store16(void* buf, uint64_t bytes, int blocks_per_sm,
+                                     int iters, double* ops_per_s, void* stream);
 
 /* ---- multi-GPU plumbing (CUDA IPC) -------------------------------------
  * One cudaMalloc block per rank holds SEAV+LDCA; its 64-byte IPC handle is

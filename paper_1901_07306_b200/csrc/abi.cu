@@ -25,6 +25,17 @@ __global__ void __launch_bounds__(256) microbench_red_kernel(uint32_t* buf, uint
   }
 }
 
+// Random u16 stores with the sliding scan's instruction (st.global.u16) over
+// a `bytes` footprint: the roofline term of K2 (the pool is
+// not L2-resident, so every stamp store is a partial-sector write).
+__global__ void __launch_bounds__(256) microbench_store16_kernel(uint16_t* buf, uint32_t elems_mask, int iters) {
+  uint32_t s = 0x2545F491u ^ ((blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u);
+  for (int i = 0; i < iters; ++i) {
+    const uint32_t r = xorshift(s);
+    asm volatile("st.global.u16 [%0], %1;" ::"l"(buf + (r & elems_mask)), "h"((unsigned short)(r >> 16)) : "memory");
+  }
+}
+
 }  // namespace sspd
 
 using namespace sspd;
@@ -66,6 +77,36 @@ extern "C" int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
   for (int rep = 0; rep < 5; ++rep) {
     cudaEventRecord(a, st);
     microbench_red_kernel<<<grid, 256, 0, st>>>(static_cast<uint32_t*>(buf), mask, iters);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ops_per_s = (double)grid * 256.0 * iters / (best * 1e-3);
+  return check_launch();
+}
+
+extern "C" int sspd_microbench_store16(void* buf, uint64_t bytes, int blocks_per_sm, int iters, double* ops_per_s,
+                                       void* stream) {
+  if (!buf || !ops_per_s || bytes < 2 || (bytes & (bytes - 1))) return SSPD_ERR_CONFIG;
+  if (bytes / 2 - 1 > 0xFFFFFFFFull) return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = sms * (blocks_per_sm > 0 ? blocks_per_sm : 8);
+  const uint32_t mask = (uint32_t)(bytes / 2 - 1);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  microbench_store16_kernel<<<grid, 256, 0, st>>>(static_cast<uint16_t*>(buf), mask, iters);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(a, st);
+    microbench_store16_kernel<<<grid, 256, 0, st>>>(static_cast<uint16_t*>(buf), mask, iters);
     cudaEventRecord(b, st);
     cudaEventSynchronize(b);
     float ms = 0.f;
