@@ -65,9 +65,5 @@ def ips_to_device(a, name: str = "ips"):
     return torch.from_numpy(arr.view(np.int32)).to(device(), non_blocking=False)
 
 
-def to_host_bytes(t, nbytes: int) -> bytes:
-    return t[:nbytes].cpu().numpy().tobytes()
-
-
 def call(name: str, *args):
     check(getattr(lib(), name)(*args), name)

@@ -119,6 +119,7 @@ def test_overflow_semantics(cuda, golden, garr):
     dict(theta=1024, r=12, k=8192, lr=8, lc=1024),
     dict(theta=256, r=16, k=4096, lr=2, lc=4096),
     dict(theta=8, r=4, addr_bits=16, k=256, lr=2, lc=16),
+    dict(theta=1024, r=16, k=8192, lr=8, lc=8192),  # config 5: 64 MiB LDCA
 ])
 def test_random_streams_vs_oracle(cuda, oracle, geom):
     """Geometries beyond the golden set, checked against the pinned oracle."""
@@ -313,3 +314,43 @@ def test_config2_full_window_bit_exact_vs_oracle(cuda, oracle):
             want.append((int(ip), est, sat))
     assert got == want
     assert set(supers.tolist()) <= {r[0] for r in got}
+
+
+def test_config5_geometry_host_stream_windows_vs_oracle(cuda, oracle):
+    """Config-5 geometry (LDCA 64 MiB: LR=8, LC=8192, k=8192 -- too big for
+    shared memory, so the L2-red scan K1 runs; SEAV r=16) streamed from
+    pinned host memory in 2^22-pair chunks over two windows with a reset
+    between: each window's sketches and report list equal the oracle's."""
+    import math
+
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=8192, design_n=5e7)
+    _, _, p = params_block(dp)
+    st = make_state(dp)
+    rng = np.random.default_rng(55)
+    for window in range(2):
+        n = (1 << 23) + 12345
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        heavy = rng.integers(0, 2**32, size=16, dtype=np.uint64).astype(np.uint32)
+        for i, h in enumerate(heavy):
+            hips[i * 20_000:(i + 1) * 20_000 - i * 700] = h
+        h_t = torch.from_numpy(hips.view(np.int32)).pin_memory()
+        o_t = torch.from_numpy(oips.view(np.int32)).pin_memory()
+        assert st.process_host_stream(h_t, o_t, chunk_pairs=1 << 22) == 8 * n
+        reps = st.finalize_window()
+        seav, ldca = oracle.scan(p, hips, oips, threads=oracle.cpu_threads())
+        assert st.seav.payload_bytes() == seav.tobytes()
+        assert st.ldca.payload_bytes() == ldca.tobytes()
+        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+        z0 = oracle.filter_z0(p, ldca, ips)
+        k = dp.k
+        want = [int(ip) for ip, z in zip(ips.tolist(), z0.tolist())
+                if z == 0 or -k * math.log(z / k) >= dp.beta * dp.theta]
+        assert [r.ip for r in reps] == want
+        assert set(heavy.tolist()) <= set(want)
+        assert all(r.window_id == window for r in list(reps)[:3])
+        st.reset()
