@@ -30,6 +30,8 @@ from __future__ import annotations
 
 import ctypes
 
+from .trace import traced
+
 
 def stripes(nbytes: int, world: int, align: int = 16) -> list[tuple[int, int]]:
     """[lo, hi) byte stripe per rank, 16-byte aligned, covering [0, nbytes)."""
@@ -147,6 +149,7 @@ class OrMerger:
             raise RuntimeError("CUDA IPC peer mapping failed on some rank")
         self.stripes = stripes(self.nbytes, self.world)
 
+    @traced("merge")
     def merge_to_root(self):
         """After every rank finished scanning: rank 0's block = OR of all blocks."""
         if self.transport == "nccl":

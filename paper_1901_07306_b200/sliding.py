@@ -22,6 +22,7 @@ from .errors import ConfigError
 from .long_sketch import ldc_estimate
 from .short_sketch import SeavSketch
 from .window_detector import DetectionReport, DetectorParams, DeviceFinalize, ReportList
+from .trace import traced
 
 _UNSIGNED = ((1, np.uint8), (2, np.uint16), (4, np.uint32), (8, np.uint64))
 
@@ -213,6 +214,7 @@ class SlidingDetector:
         self.pool.reset()
         self.pair_count = 0
 
+    @traced("observe")
     def observe_batch(self, hips, oips):
         """K2: stamp every slot the discrete path would set (sliding.py:156-185)."""
         from ._device import call, ips_to_device, stream_ptr
@@ -276,6 +278,7 @@ class SlidingDetector:
              stream_ptr())
         return ldc_estimate(int(z0.item()) & 0xFFFFFFFF, self.ldca_config.k)
 
+    @traced("detect")
     def detect(self, beta: float | None = None) -> list[DetectionReport]:
         """Materialise (K4: SEAV registers + packed LDCA) -> fused finalize
         (K5 restore, sort, K6 filter, compaction; one host round trip)
@@ -298,6 +301,7 @@ class SlidingDetector:
         fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff)
         return fin.reports(self.now, "sliding")
 
+    @traced("detect_async")
     def detect_async(self, beta: float | None = None) -> PendingReports:
         """`detect()` pipelined with the caller's next slices.
 

@@ -33,6 +33,7 @@ from .long_sketch import (
     plan_rows,
 )
 from .short_sketch import DEFAULT_RESTORE_CAP, SeavConfig, SeavSketch, sort_candidates
+from .trace import traced
 
 DEFAULT_BETA = 0.8
 
@@ -312,6 +313,7 @@ class DetectorState:
     def process_pair(self, hip: int, oip: int):
         self.process_batch(np.array([hip], dtype=np.uint64), np.array([oip], dtype=np.uint64))
 
+    @traced("scan")
     def process_batch(self, hips, oips):
         """K1: one fused pass updating both sketches (window_detector.py:100-103)."""
         from ._device import call, ips_to_device, stream_ptr
@@ -354,6 +356,7 @@ class DetectorState:
         call("sspd_scan_discrete", h_ptr, o_ptr, n, self.seav._params, seav_p, ldca_p, stream_ptr())
         self.last_scan = "direct"
 
+    @traced("host_stream")
     def process_host_stream(self, hips, oips, chunk_pairs: int = 1 << 23):
         """Stream HOST arrays through two device staging buffers: the H2D copy
         of chunk i+1 (copy stream) overlaps the K1 scan of chunk i (compute
@@ -399,6 +402,7 @@ class DetectorState:
         self.pair_count += n
         return 8 * n
 
+    @traced("finalize")
     def finalize_window(self, beta: float | None = None, source: str = "discrete") -> "ReportList":
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.theta
