@@ -132,6 +132,35 @@ SSPD_API int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips
                                       const sspd_params* p, void* pool, uint32_t ts_bytes,
                                       uint64_t now_wrapped, uint32_t max_blocks_per_sm, void* stream);
 
+/* ---- incremental SEAV view of a sliding pool (u16 stamps) ---------------
+ * Instead of re-reading the whole SEAV stamp region at every detect
+ * (materialize_seav, sliding.py:191-203), SlidingDetector keeps the active
+ * SEAV bits up to date:
+ *   sspd_scan_sliding_tracked  = sspd_scan_sliding_capped that also ORs
+ *       every SEAV stamp's bit into `seav_view` and appends the slot to the
+ *       ring `log` (log_entries, a power of two; *log_head counts appends);
+ *   sspd_seav_advance          = before TimestampPool.advance_slice
+ *       (sliding.py:81-86): records the log head of slice now_abs in
+ *       meta[4 + now_abs % nseg] and clears the view bit of every slot of
+ *       slice now_abs + 1 - window whose stamp was not renewed (the bits
+ *       that turn inactive); sets meta[1] if the ring overwrote live entries;
+ *   sspd_materialize_seav_if   = full materialization into seav_view only
+ *       when *flag (meta[1]) is set -- the invalidated view stays exact.
+ * meta (u64): [0] log head, [1] invalid flag, [4 + s % nseg] segment ends;
+ * nseg >= window + 2. */
+SSPD_API int sspd_scan_sliding_tracked(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                       const sspd_params* p, void* pool, uint32_t ts_bytes,
+                                       uint64_t now_wrapped, uint32_t max_blocks_per_sm,
+                                       uint8_t* seav_view, uint32_t* log, uint64_t log_entries,
+                                       unsigned long long* log_head, void* stream);
+SSPD_API int sspd_seav_advance(const void* pool, uint32_t ts_bytes, const sspd_params* p,
+                               uint8_t* seav_view, const uint32_t* log, uint64_t log_entries,
+                               unsigned long long* meta, uint32_t nseg, uint64_t now_abs,
+                               uint64_t window_slices, void* stream);
+SSPD_API int sspd_materialize_seav_if(const void* pool, uint32_t ts_bytes, const sspd_params* p,
+                                      uint64_t now_wrapped, uint64_t window_slices, uint8_t* seav_out,
+                                      const unsigned long long* flag, void* stream);
+
 /* ---- K3 sweep: TimestampPool._sweep (sliding.py:88-94) ---------------- */
 SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
                uint64_t now_wrapped, uint64_t window_slices,

@@ -19,10 +19,13 @@
 // and every sliding stamp is a plain store (all writers of one slice store
 // the same value, so no atomic is needed and none would be correct across
 // the wrap -- see DESIGN.md).
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include "sspd_common.cuh"
 #include "launch.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sspd {
 
@@ -174,10 +177,24 @@ __device__ __forceinline__ void st_u16_hint(uint16_t* addr, uint16_t v, uint64_t
   asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(addr), "h"(v), "l"(pol) : "memory");
 }
 
+// Incremental SEAV view (optional, `tr.view != nullptr`): every SEAV stamp
+// also sets its bit in the maintained active-bit view and appends the slot
+// to a ring log, so advance_slice can clear exactly the bits whose slice
+// expires (sspd_seav_advance) instead of re-reading the 268 MB SEAV stamp
+// region at every detect.
+struct SeavTracker {
+  uint32_t* view;                // SEAV view as words (seav payload layout)
+  uint32_t* log;                 // ring of SEAV slot indexes
+  unsigned long long* log_head;  // entries ever appended
+  uint32_t log_mask;             // ring size - 1
+};
+
+template <bool kTrack>
 __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32_t* __restrict__ hips,
                                                                     const uint32_t* __restrict__ oips, uint64_t n,
                                                                     const __grid_constant__ sspd_params p,
-                                                                    uint16_t* pool, uint16_t now, float l2_frac) {
+                                                                    uint16_t* pool, uint16_t now, float l2_frac,
+                                                                    SeavTracker tr) {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(l2_frac));
   const uint32_t tmask = tau_mask(p.tau);
@@ -196,9 +213,23 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
       const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
       const uint64_t rp = hip & ((1u << p.r) - 1u);
       const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+      unsigned long long pos = 0;
+      if (kTrack) {  // one log reservation per group of lanes sampling together (one shared counter)
+        cg::coalesced_group g = cg::coalesced_threads();
+        unsigned long long base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(tr.log_head, (unsigned long long)g.size() * p.sr);
+        pos = g.shfl(base, 0) + (unsigned long long)g.thread_rank() * p.sr;
+      }
       for (uint32_t i = 0; i < p.sr; ++i) {
         const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
-        pool[p.slot_row_base[i] + (rp * p.sc[i] + col) * p.g + bit] = now;
+        const uint64_t reg = rp * p.sc[i] + col;
+        const uint64_t slot = p.slot_row_base[i] + reg * p.g + bit;
+        pool[slot] = now;
+        if (kTrack) {
+          const uint64_t vbit = (p.seav_row_off[i] + reg * p.reg_bytes) * 8 + bit;
+          atomicOr(tr.view + (vbit >> 5), 1u << (vbit & 31));
+          tr.log[(pos + i) & tr.log_mask] = (uint32_t)slot;
+        }
       }
     }
     const uint32_t b = (uint32_t)mix64(oip ^ p.seed_h3) & k_mask;
@@ -255,20 +286,41 @@ extern "C" int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, ui
   return launch_discrete<false, true>(hips, oips, n, *p, seav, ldca, st);
 }
 
+static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                             void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
+                             SeavTracker tracker, void* stream);
+
 extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                         const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
-                                        uint32_t max_blocks_per_sm, void* stream);
+                                        uint32_t max_blocks_per_sm, void* stream) {
+  return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm,
+                           SeavTracker{nullptr, nullptr, nullptr, 0u}, stream);
+}
+
+extern "C" int sspd_scan_sliding_tracked(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                         const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                         uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
+                                         uint64_t log_entries, unsigned long long* log_head, void* stream) {
+  if (!seav_view || !log || !log_head || log_entries == 0 || (log_entries & (log_entries - 1)) ||
+      log_entries > (1ull << 32) || (reinterpret_cast<uintptr_t>(seav_view) & 3u))
+    return SSPD_ERR_DATA;
+  return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm,
+                           SeavTracker{reinterpret_cast<uint32_t*>(seav_view), log, log_head,
+                                       (uint32_t)(log_entries - 1)},
+                           stream);
+}
 
 extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                                  void* pool, uint32_t ts_bytes, uint64_t now_wrapped, void* stream) {
   return sspd_scan_sliding_capped(hips, oips, n, p, pool, ts_bytes, now_wrapped, 0, stream);
 }
 
-extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
-                                        const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
-                                        uint32_t max_blocks_per_sm, void* stream) {
+static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                             void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
+                             SeavTracker tracker, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
+  if (tracker.view && ts_bytes != 2) return SSPD_ERR_CONFIG;  // tracking exists only on the u16 fast path
   if (n == 0) return SSPD_OK;
   if (!hips || !oips || !pool) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -286,7 +338,8 @@ extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oi
         float frac = 0.85f;
         if (const char* e = getenv("SSPD_SLIDE_L2_FRAC")) frac = (float)atof(e);
         frac = frac < 0.f ? 0.f : (frac > 1.f ? 1.f : frac);
-        int grid = grid_for(scan_sliding_u16_fast_kernel, 256, (n + 3) / 4);
+        auto kern = tracker.view ? scan_sliding_u16_fast_kernel<true> : scan_sliding_u16_fast_kernel<false>;
+        int grid = grid_for(kern, 256, (n + 3) / 4);
         // optional cap (blocks per SM) so kernels on other streams (the
         // pipelined detect) stay co-resident with this store-bound scan
         uint32_t cap_bps = max_blocks_per_sm;
@@ -298,10 +351,10 @@ extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oi
           const int cap = (int)cap_bps * sms;
           if (grid > cap) grid = cap;
         }
-        scan_sliding_u16_fast_kernel<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool,
-                                                            (uint16_t)now_wrapped, frac);
+        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker);
         break;
       }
+      if (tracker.view) return SSPD_ERR_CONFIG;  // tracking exists only on the fast path
       const int grid = grid_for(scan_sliding_kernel<uint16_t>, 256, n);
       scan_sliding_kernel<uint16_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped);
       break;

@@ -111,6 +111,63 @@ __global__ void __launch_bounds__(256) materialize_seav_g8u16_kernel(const uint1
   }
 }
 
+// ---- incremental SEAV view (SlidingDetector, u16 stamps) -----------------
+// meta (u64): [0] log head (entries ever appended by the tracked scan),
+// [1] "view invalid" flag (sticky: full materialization at every detect),
+// [4 + s % nseg] = log head at the end of slice s.
+__global__ void seav_record_kernel(unsigned long long* meta, uint32_t seg_slot) {
+  meta[4 + seg_slot] = meta[0];
+}
+
+// Clear the view bit of every SEAV slot logged during slice e whose stamp is
+// still e (not re-touched since): those are exactly the bits that turn
+// inactive when `now` reaches e + window (sliding.py:96-102).
+__global__ void __launch_bounds__(256) seav_expire_kernel(const uint16_t* __restrict__ pool,
+                                                          const __grid_constant__ sspd_params p, uint32_t* view,
+                                                          const uint32_t* __restrict__ log, uint64_t log_entries,
+                                                          unsigned long long* meta, int32_t start_slot,
+                                                          uint32_t end_slot, uint16_t expired) {
+  const unsigned long long start = start_slot < 0 ? 0ull : meta[4 + start_slot];
+  const unsigned long long end = meta[4 + end_slot];
+  if (meta[0] - start > log_entries) {  // the ring overwrote entries of slice e
+    if (blockIdx.x == 0 && threadIdx.x == 0) meta[1] = 1ull;
+    return;
+  }
+  const uint64_t mask = log_entries - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t pos = start + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < end; pos += stride) {
+    const uint32_t slot = log[pos & mask];
+    if (pool[slot] != expired) continue;
+    uint32_t i = 0;
+    while (i + 1 < p.sr && p.slot_row_base[i + 1] <= slot) ++i;
+    const uint64_t rel = slot - p.slot_row_base[i];
+    const uint64_t vbit = (p.seav_row_off[i] + (rel / p.g) * p.reg_bytes) * 8 + rel % p.g;
+    atomicAnd(view + (vbit >> 5), ~(1u << (vbit & 31)));
+  }
+}
+
+__global__ void __launch_bounds__(256) materialize_seav_g8u16_if_kernel(const uint16_t* __restrict__ pool,
+                                                                        const __grid_constant__ sspd_params p,
+                                                                        uint16_t now, uint32_t window, uint64_t quads,
+                                                                        uint8_t* out,
+                                                                        const unsigned long long* flag) {
+  if (*flag == 0ull) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += stride) {
+    uint32_t i = 0;
+    uint64_t local = q;
+    while (local >= (((uint64_t)p.sc[i] << p.r) >> 2)) {
+      local -= ((uint64_t)p.sc[i] << p.r) >> 2;
+      ++i;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(pool + p.slot_row_base[i]) + local * 4;
+    const uint4 v0 = __ldcs(src), v1 = __ldcs(src + 1), v2 = __ldcs(src + 2), v3 = __ldcs(src + 3);
+    *reinterpret_cast<uint32_t*>(out + p.seav_row_off[i] + local * 4) =
+        active8_u16(v0, now, window) | (active8_u16(v1, now, window) << 8) | (active8_u16(v2, now, window) << 16) |
+        (active8_u16(v3, now, window) << 24);
+  }
+}
+
 // materialize_ldca (sliding.py:215-220): byte q of the packed array holds
 // the activity of slots ldca_base + 8q .. 8q+7, little bit order.
 template <typename T>
@@ -233,6 +290,58 @@ extern "C" int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes, const 
     materialize_ldca_kernel<T><<<grid, 256, 0, st>>>((const T*)pool, p->slot_ldca_base, nbytes, (T)now_wrapped,
                                                      window_slices, ldca_out);
   })
+  return check_launch();
+}
+
+static bool seav_fast_layout(const void* pool, const sspd_params* p, const void* out) {
+  bool ok = p->g == 8 && p->reg_bytes == 1 && (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
+            (reinterpret_cast<uintptr_t>(out) & 3u) == 0;
+  for (uint32_t i = 0; i < p->sr && ok; ++i)
+    ok = ((((uint64_t)p->sc[i]) << p->r) & 3u) == 0 && (p->slot_row_base[i] & 7u) == 0 && (p->seav_row_off[i] & 3u) == 0;
+  return ok;
+}
+
+// advance_slice of an incrementally tracked pool (u16 stamps): record the
+// log head for slice `now_abs`, then clear the bits of slice now_abs+1-w.
+extern "C" int sspd_seav_advance(const void* pool, uint32_t ts_bytes, const sspd_params* p, uint8_t* seav_view,
+                                 const uint32_t* log, uint64_t log_entries, unsigned long long* meta, uint32_t nseg,
+                                 uint64_t now_abs, uint64_t window_slices, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (ts_bytes != 2 || nseg < window_slices + 2) return SSPD_ERR_CONFIG;
+  if (!pool || !seav_view || !log || !meta || log_entries == 0 || (log_entries & (log_entries - 1)))
+    return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  seav_record_kernel<<<1, 1, 0, st>>>(meta, (uint32_t)(now_abs % nseg));
+  if (now_abs + 1 >= window_slices) {
+    const uint64_t e = now_abs + 1 - window_slices;
+    const int32_t start_slot = e == 0 ? -1 : (int32_t)((e - 1) % nseg);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    seav_expire_kernel<<<sms * 2, 256, 0, st>>>((const uint16_t*)pool, *p, reinterpret_cast<uint32_t*>(seav_view),
+                                                log, log_entries, meta, start_slot, (uint32_t)(e % nseg),
+                                                (uint16_t)(e & 0xFFFFu));
+  }
+  return check_launch();
+}
+
+// The SEAV view materialized from the pool only when *flag != 0 (the
+// incremental view was invalidated); otherwise a no-op launch.
+extern "C" int sspd_materialize_seav_if(const void* pool, uint32_t ts_bytes, const sspd_params* p,
+                                        uint64_t now_wrapped, uint64_t window_slices, uint8_t* seav_out,
+                                        const unsigned long long* flag, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (ts_bytes != 2 || !seav_fast_layout(pool, p, seav_out)) return SSPD_ERR_CONFIG;
+  if (!flag) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t regs = 0;
+  for (uint32_t i = 0; i < p->sr; ++i) regs += ((uint64_t)p->sc[i]) << p->r;
+  const uint64_t quads = regs >> 2;
+  const int grid = grid_for(materialize_seav_g8u16_if_kernel, 256, quads);
+  materialize_seav_g8u16_if_kernel<<<grid, 256, 0, st>>>((const uint16_t*)pool, *p, (uint16_t)now_wrapped,
+                                                         (uint32_t)window_slices, quads, seav_out, flag);
   return check_launch();
 }
 

@@ -71,6 +71,7 @@ class TimestampPool:
         self._sweep_period = self._modulus - 2 * window_slices
         self._since_sweep = 0
         self.sweep_count = 0
+        self._version = 0  # bumped by every stamp write that bypasses SlidingDetector
         init = (-window_slices) & self._mask  # age == window: just expired
         self._buf = torch.full((n_slots,), _as_signed(init, self.ts_bytes),
                                dtype=_signed_torch(self.ts_bytes), device=device())
@@ -84,6 +85,7 @@ class TimestampPool:
         self.now = 0
         self._since_sweep = 0
         self.sweep_count = 0
+        self._version += 1
         self._buf.fill_(_as_signed((-self.window_slices) & self._mask, self.ts_bytes))
 
     @property
@@ -98,6 +100,7 @@ class TimestampPool:
         if arr.shape != (self.n_slots,):
             raise ConfigError("timestamp array shape mismatch")
         signed = arr.view(_signed_torch_np(self.ts_bytes))
+        self._version += 1
         self._buf.copy_(torch.from_numpy(signed))
 
     def memory_bytes(self) -> int:
@@ -118,12 +121,14 @@ class TimestampPool:
         current = int(self._buf[slot_index].item()) & self._mask
         existing_age = (self._wrapped_now() - current) & self._mask
         if candidate_age < existing_age:
+            self._version += 1
             self._buf[slot_index] = _as_signed(now & self._mask, self.ts_bytes)
 
     def touch_batch(self, slot_indexes):
         import torch
 
         idx = torch.as_tensor(np.asarray(slot_indexes, dtype=np.int64)).to(self._buf.device)
+        self._version += 1
         self._buf.index_fill_(0, idx, _as_signed(self._wrapped_now(), self.ts_bytes))
 
     def advance_slice(self):
@@ -186,6 +191,10 @@ class SlidingDetector:
 
     pipelined_scan_blocks_per_sm = 2  # K2 grid cap while detect_async runs (measured best on B200)
     pipeline_depth = 2  # view sets of detect_async (detects in flight)
+    # keep the SEAV active-bit view up to date (stamp-time set + expiry log)
+    # instead of re-reading the whole SEAV stamp region at every detect
+    incremental_seav = True
+    seav_log_entries = 1 << 25  # ring of logged SEAV stamps (4 B each)
 
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
@@ -208,11 +217,86 @@ class SlidingDetector:
         return self.pool.now
 
     def advance_slice(self):
+        iv = self._iv()
+        if iv is not None:
+            from ._device import call, stream_ptr
+
+            self._iv_check(iv)
+            pool = self.pool
+            call("sspd_seav_advance", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+                 iv["view"].device_buffer().data_ptr(), iv["log"].data_ptr(), iv["log"].numel(),
+                 iv["meta"].data_ptr(), iv["nseg"], pool.now, pool.window_slices, stream_ptr())
+            iv["now"] = pool.now + 1
         self.pool.advance_slice()
 
     def reset(self):
         self.pool.reset()
         self.pair_count = 0
+        iv = getattr(self, "_iv_state", None)
+        if iv:
+            iv["view"].clear()
+            iv["meta"].zero_()
+            iv["version"], iv["now"] = self.pool._version, self.pool.now
+
+    # -- incremental SEAV view -------------------------------------------------
+    def _iv(self):
+        """State of the incrementally maintained SEAV view, or None when the
+        stamp width / geometry has no tracked scan (u16 stamps, g = 8 one-byte
+        registers, power-of-two k and lc)."""
+        st = getattr(self, "_iv_state", False)
+        if st is not False:
+            return st
+        st = None
+        p, pool = self._params, self.pool
+        ok = (self.incremental_seav and pool.ts_bytes == 2 and p.g == 8 and p.reg_bytes == 1
+              and (p.k & (p.k - 1)) == 0 and (p.lc & (p.lc - 1)) == 0 and p.slot_total < (1 << 32)
+              and all((int(p.slot_row_base[i]) & 7) == 0 and (int(p.seav_row_off[i]) & 3) == 0
+                      and ((int(p.sc[i]) << p.r) & 3) == 0 for i in range(p.sr)))
+        if ok:
+            import torch
+
+            from ._device import device
+
+            nseg = 1 << (pool.window_slices + 2 - 1).bit_length()
+            st = {"view": SeavSketch(self.seav_config, self.seeds, restore_cap=self.params.restore_cap,
+                                     _ldca_config=self.ldca_config),
+                  "log": torch.empty(self.seav_log_entries, dtype=torch.int32, device=device()),
+                  "meta": torch.zeros(4 + nseg, dtype=torch.int64, device=device()),
+                  "nseg": nseg, "version": pool._version, "now": pool.now}
+            if pool._version or pool.now or self.pair_count:
+                st["meta"][1] = 1  # enabled late: the view starts invalid (full materialization)
+        self._iv_state = st
+        return st
+
+    def _iv_check(self, iv):
+        """Stamps written around the detector (TimestampPool.touch*, .ts,
+        advance_slice on the pool itself) invalidate the incremental view:
+        from then on every detect materializes it in full (exact)."""
+        pool = self.pool
+        if pool._version != iv["version"] or pool.now != iv["now"]:
+            iv["meta"][1] = 1
+            iv["version"], iv["now"] = pool._version, pool.now
+
+    def _seav_view(self):
+        """The SEAV active-bit view for the current slice as a SeavSketch
+        (device): the incremental one (materialized in full only if it was
+        invalidated), else a full K4 materialization."""
+        iv = self._iv()
+        if iv is None:
+            seav = getattr(self, "_view", None)  # reused across slides: K4 overwrites every register
+            if seav is None:
+                seav = self._view = self.materialize_seav()
+            else:
+                self._materialize_into(seav)
+            return seav
+        from ._device import call, stream_ptr
+
+        self._iv_check(iv)
+        pool = self.pool
+        call("sspd_materialize_seav_if", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, iv["view"].device_buffer().data_ptr(),
+             iv["meta"][1:].data_ptr(), stream_ptr())
+        return iv["view"]
 
     @traced("observe")
     def observe_batch(self, hips, oips):
@@ -227,8 +311,16 @@ class SlidingDetector:
         # once detection is pipelined (detect_async), the scan leaves SM room
         # for the finalize kernels running on the side stream
         cap = self.pipelined_scan_blocks_per_sm if getattr(self, "_async", None) else 0
-        call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
-             pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
+        iv = self._iv()
+        if iv is not None:
+            self._iv_check(iv)
+            call("sspd_scan_sliding_tracked", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+                 pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
+                 iv["view"].device_buffer().data_ptr(), iv["log"].data_ptr(), iv["log"].numel(),
+                 iv["meta"].data_ptr(), stream_ptr())
+        else:
+            call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+                 pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
         self.pair_count += int(h.numel())
 
     def observe(self, hip: int, oip: int):
@@ -287,11 +379,7 @@ class SlidingDetector:
 
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
-        seav = getattr(self, "_view", None)  # reused across slides: K4 overwrites every register
-        if seav is None:
-            seav = self._view = self.materialize_seav()
-        else:
-            self._materialize_into(seav)
+        seav = self._seav_view()
         lview = getattr(self, "_ldca_view", None)
         if lview is None:
             lview = self._ldca_view = zeros_bytes(self._params.ldca_bytes)
@@ -335,7 +423,11 @@ class SlidingDetector:
             vset[2].resolve()  # the finalize `pipeline_depth` calls ago is done with this view set
         seav, lview = vset[0], vset[1]
         pool = self.pool
-        self._materialize_into(seav)
+        if self._iv() is not None:  # snapshot of the incremental view (16 MiB at r=16)
+            src = self._seav_view().device_buffer()
+            seav.device_buffer()[: src.numel()].copy_(src)
+        else:
+            self._materialize_into(seav)
         call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
              pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
         views_ready = torch.cuda.Event()

@@ -329,3 +329,57 @@ def test_config4_scaled_trace_vs_oracle(cuda, oracle):
         assert got == rows, s
         assert all(r.window_id == s for r in list(pending[s])[:3])
     assert sum(len(pending[s]) for s in pending) > 0
+
+
+def test_incremental_seav_view_equals_full_materialization(cuda):
+    """The incrementally maintained SEAV view (stamp-time set + per-slice
+    expiry log) equals a full K4 materialization of the pool at every
+    slide: through expiries (400 slides > w = 150), hosts coming and going,
+    re-touched slots, empty slices, a pool write that bypasses the detector
+    (the view then degrades to full materialization, still exact), and a
+    reset; detect() equals a detector without the incremental view."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=512, r=8, k=4096, lr=2, lc=64, design_n=1e5)
+    w = 150
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=w)
+        b = SlidingDetector(params, window_slices=w)
+    b.incremental_seav = False
+    assert a.pool.ts_bytes == 2
+    rng = np.random.default_rng(31)
+    heavy = rng.integers(0, 2**32, size=5, dtype=np.uint64)
+
+    def step(s):
+        n = 0 if s % 37 == 5 else int(rng.integers(500, 12_000))
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        if n:
+            hips[: n // 3] = heavy[(s // 60) % len(heavy)]
+            oips[: n // 6] = oips[0]  # re-touched slots within the slice
+        for det in (a, b):
+            det.observe_batch(hips, oips)
+        inc = a._seav_view().device_buffer()
+        full = a.materialize_seav().device_buffer()
+        assert torch.equal(inc[: full.numel()], full), s
+        if s % 25 == 0:
+            assert rep_list(a.detect()) == rep_list(b.detect()), s
+        for det in (a, b):
+            det.advance_slice()
+
+    for s in range(400):
+        step(s)
+    assert a._iv() is not None and int(a._iv()["meta"][1].item()) == 0  # stayed incremental
+    a.pool.touch_batch(np.arange(0, 64, 3))  # bypasses the detector
+    b.pool.touch_batch(np.arange(0, 64, 3))
+    for s in range(400, 420):
+        step(s)
+    assert int(a._iv()["meta"][1].item()) == 1  # invalidated -> full materialization
+    for det in (a, b):
+        det.reset()
+    assert int(a._iv()["meta"][1].item()) == 0
+    for s in range(420, 600):
+        step(s)
