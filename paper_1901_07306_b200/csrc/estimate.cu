@@ -320,11 +320,18 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
     G.sync();
   }
 
-  restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
-  G.sync();
-  if (misc->total > cap) {
-    if (G.tid == 0) overflow[slot] = 1;
-    return;
+  // The counting pass only matters when the SEA could exceed the cap: the
+  // complete tuples are at most (row-0 x row-1 pairs) x hot(2) x ... x
+  // hot(SR-1); when that bound is <= cap the emit pass alone is exact.
+  uint64_t bound = misc->pairs;
+  for (uint32_t i = 2; i < sr && bound <= cap; ++i) bound *= misc->hot[i];
+  if (bound > cap) {
+    restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
+    G.sync();
+    if (misc->total > cap) {
+      if (G.tid == 0) overflow[slot] = 1;
+      return;
+    }
   }
   restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
 }
