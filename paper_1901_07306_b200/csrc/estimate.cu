@@ -500,29 +500,38 @@ __global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict
 // owned by block b: pass 1 counts each segment, pass 2 sums the preceding
 // counts (<= 1024 of them) and scatters its segment in order with a
 // ballot-based block scan.
-constexpr uint32_t kSeg = 8192;
+constexpr uint32_t kSeg = 1024;  // one 1,024-thread pass per segment (many blocks in flight)
 
 __device__ void compact_segment(const uint32_t* __restrict__ ip, const uint32_t* __restrict__ z0,
                                 const uint8_t* __restrict__ keep, uint64_t lo, uint64_t hi, uint32_t* ip_out,
                                 uint32_t* z0_out, unsigned long long base) {
-  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t warp_pre[32];
+  __shared__ uint32_t tile_total;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint64_t start = lo; start < hi; start += blockDim.x) {
     const uint64_t j = start + threadIdx.x;
     const uint32_t f = (j < hi && keep[j]) ? 1u : 0u;
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, f);
-    if (lane == 0) warp_sums[wid] = __popc(ballot);
+    if (lane == 0) warp_pre[wid] = __popc(ballot);
     __syncthreads();
-    uint32_t before = __popc(ballot & ((1u << lane) - 1u)), total = 0;
-    for (uint32_t wv = 0; wv < nw; ++wv) {
-      if (wv < wid) before += warp_sums[wv];
-      total += warp_sums[wv];
+    if (wid == 0) {  // exclusive scan of the per-warp counts (lane i owns entry i)
+      const uint32_t v = lane < nw ? warp_pre[lane] : 0u;
+      uint32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (lane < nw) warp_pre[lane] = incl - v;
+      if (lane == 31) tile_total = incl;
     }
+    __syncthreads();
+    const uint32_t before = warp_pre[wid] + __popc(ballot & ((1u << lane) - 1u));
     if (f) {
       ip_out[base + before] = ip[j];
       z0_out[base + before] = z0[j];
     }
-    base += total;
+    base += tile_total;
     __syncthreads();
   }
 }
