@@ -543,10 +543,18 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
     kern = mode == kPow2 ? (void*)scan_partitioned_kernel<false, kPow2>
                          : (mode == kFast32 ? (void*)scan_partitioned_kernel<false, kFast32>
                                             : (void*)scan_partitioned_kernel<false, kGeneric>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  if (per_sm < 1) return SSPD_ERR_CONFIG;
+  // the attribute/occupancy answers only change with (kernel, smem, device):
+  // cached so a launch costs one driver call (a benign race recomputes)
+  static void* c_kern = nullptr;
+  static uint64_t c_smem = 0;
+  static int c_dev = -1, c_per_sm = 0;
+  if (kern != c_kern || smem != c_smem || dev != c_dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    c_kern = kern, c_smem = smem, c_dev = dev, c_per_sm = per_sm;
+  }
+  if (c_per_sm < 1) return SSPD_ERR_CONFIG;
   const uint32_t* h = hips;
   const uint32_t* o = oips;
   sspd_params pv = *p;

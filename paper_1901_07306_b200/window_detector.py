@@ -330,7 +330,7 @@ class DetectorState:
     # the LDCA fits in the SMs' shared memory, else the direct L2 scan (K1).
     scan_mode = "auto"  # or "direct" / "partitioned" (class attributes, not dataclass fields)
     partitioned_min_packets = 1 << 22
-    partitioned_chunk = 0  # 0: library default (4 whole 4096-packet tiles per SM per chunk)
+    partitioned_chunk = 0  # 0: library default (8 whole 4096-packet tiles per SM per chunk)
 
     def _scan(self, h_ptr: int, o_ptr: int, n: int):
         from ._abi import ERR_CONFIG, check, lib
