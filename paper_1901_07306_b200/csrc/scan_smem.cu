@@ -168,9 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = (uint32_t)((t - 1) & 1);
       const uint32_t* cnts = P.counts + ((size_t)b * np + self) * ns;
       const uint32_t* regions = P.buckets + ((size_t)b * np + self) * (size_t)ns * P.region_cap;
-      // warp w drains sources w, w+32, ...: fetch all of its run lengths at
-      // once (lane j holds source w+32j) so no region waits on its count
-      const uint32_t my_src = warp + 32u * lane;
+      // warp w drains sources w, w+W, ... (W = warps per CTA): fetch all of
+      // its run lengths at once (lane j holds source w+W*j) so no region
+      // waits on its count
+      const uint32_t my_src = warp + nwarps * lane;
       const uint32_t my_cnt = my_src < ns ? min(__ldcg(cnts + my_src), P.region_cap) : 0u;
       for (uint32_t src = warp, j = 0; src < ns; src += nwarps, ++j) {
         const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
