@@ -296,11 +296,33 @@ def run_gpu(args) -> dict | None:
             scan_ev.append((a, b))
         if merger is not None:
             merger.merge_to_root()
-        reps = st.finalize_window() if rank == 0 else []
+        if rank != 0:
+            st.reset()
+            return []
+        if args.sync_finalize:
+            reps = st.finalize_window()
+            st.reset()
+            if reports_out is not None:
+                reports_out.append(len(reps))
+            return reps
+        # pipelined windows: this window's finalize runs on a device snapshot
+        # and is resolved after the next window's scan has been enqueued, so
+        # the GPU never waits for the host between windows
+        reps = st.finalize_window_async()
         st.reset()
-        if reports_out is not None:
-            reports_out.append(len(reps))
+        drain_all()  # the previous window's list (its finalize ran before this scan)
+        pending.append((reps, reports_out))
         return reps
+
+    pending: list = []
+
+    def drain_all():
+        """Resolve the pending report lists (counts read back)."""
+        while pending:
+            r, out = pending.pop(0)
+            n_r = len(r)
+            if out is not None:
+                out.append(n_r)
 
     def barrier():
         torch.cuda.synchronize()
@@ -314,6 +336,7 @@ def run_gpu(args) -> dict | None:
         e0.record(stream)
         for _ in range(steps):
             fn()
+        drain_all()  # every window's list is resolved inside the timed region
         e1.record(stream)
         barrier()
         ms = e0.elapsed_time(e1) / steps
@@ -328,6 +351,7 @@ def run_gpu(args) -> dict | None:
     for _ in range(args.warmup):
         r = step()
         first = first if first is not None else r
+    drain_all()
     found = {x.ip for x in first} if first else set()
     planted_found = len(set(supers.tolist()) & found) if rank == 0 else None
 
@@ -798,6 +822,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
     ap.add_argument("--sync-detect", action="store_true", help="config 4: synchronous detect() per slide")
+    ap.add_argument("--sync-finalize", action="store_true",
+                    help="config 2: synchronous finalize_window() per window (default: pipelined windows)")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="2 = headline discrete window; 3 = 8 router shards OR-merged (strong scaling); "
                          "4 = sliding window, detect every slide; 5 = 2^32 pkts streamed from host")

@@ -13,7 +13,6 @@ view (K4), restores (K5) and filters straight from the pool (K6 sliding).
 
 from __future__ import annotations
 
-from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -21,7 +20,7 @@ import numpy as np
 from .errors import ConfigError
 from .long_sketch import ldc_estimate
 from .short_sketch import SeavSketch
-from .window_detector import DetectionReport, DetectorParams, DeviceFinalize, ReportList
+from .window_detector import DetectionReport, DetectorParams, DeviceFinalize, PendingReports, ReportList
 from .trace import traced
 
 _UNSIGNED = ((1, np.uint8), (2, np.uint16), (4, np.uint32), (8, np.uint64))
@@ -438,42 +437,6 @@ class SlidingDetector:
         vset[2] = fin
         now = self.now
         return PendingReports(lambda: fin.reports(now, "sliding"))
-
-
-class PendingReports(Sequence):
-    """Report list of `SlidingDetector.detect_async`: the device pipeline
-    runs on a side stream; the first access waits for it, then this
-    behaves exactly like the ReportList `detect()` returns."""
-
-    __slots__ = ("_resolve", "_value")
-
-    def __init__(self, resolve):
-        self._resolve = resolve
-        self._value = None
-
-    def result(self) -> ReportList:
-        if self._value is None:
-            self._value = self._resolve()
-            self._resolve = None
-        return self._value
-
-    def done(self) -> bool:
-        return self._value is not None
-
-    def __len__(self) -> int:
-        return len(self.result())
-
-    def __getitem__(self, i):
-        return self.result()[i]
-
-    def __iter__(self):
-        return iter(self.result())
-
-    def __eq__(self, other) -> bool:
-        return self.result() == (other.result() if isinstance(other, PendingReports) else other)
-
-    def __repr__(self) -> str:
-        return f"PendingReports({self.result()!r})" if self.done() else "PendingReports(<running>)"
 
 
 def _async_state(det):

@@ -354,3 +354,31 @@ def test_config5_geometry_host_stream_windows_vs_oracle(cuda, oracle):
         assert set(heavy.tolist()) <= set(want)
         assert all(r.window_id == window for r in list(reps)[:3])
         st.reset()
+
+
+def test_finalize_window_async_equals_sync(cuda):
+    """Pipelined windows: finalize_window_async (device snapshot, resolved
+    later, two snapshots alternating) gives the same lists as
+    finalize_window, including a capacity re-run resolved after later
+    windows were already scanned into the live sketches."""
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=1e6)
+    a, b = make_state(dp), make_state(dp)
+    a.seav._cand_cap = b.seav._cand_cap = 8  # force the re-run path
+    rng = np.random.default_rng(77)
+    pend, want = [], []
+    for w in range(5):
+        n = 200_000
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        for i in range(6 + w):
+            hips[i * 4000:(i + 1) * 4000] = rng.integers(0, 2**32, dtype=np.uint64)
+        for st in (a, b):
+            st.process_batch(hips, oips)
+        pend.append(a.finalize_window_async())
+        want.append([(r.ip, r.estimated_cardinality, r.saturated, r.window_id) for r in b.finalize_window()])
+        a.reset()
+        b.reset()
+    got = [[(r.ip, r.estimated_cardinality, r.saturated, r.window_id) for r in p] for p in pend]
+    assert got == want and all(len(x) >= 6 for x in want)
