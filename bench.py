@@ -517,6 +517,8 @@ def run_sliding(args) -> dict:
         warnings.simplefilter("ignore")
         det = SlidingDetector(DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=1024, design_n=2.15e8),
                               window_slices=300)
+    if args.direct_stamps:
+        det.defer_ldca_stamps = False
     if os.environ.get("SSPD_PIPELINE_DEPTH"):
         det.pipeline_depth = int(os.environ["SSPD_PIPELINE_DEPTH"])
     stream = torch.cuda.current_stream()
@@ -592,6 +594,8 @@ def run_sliding(args) -> dict:
         "config": {"workload": f"config4: {n} pkts, {n_sl} slices, w=300, r=16, LDCA 8x1024x8192, detect every slide",
                    "detect": "synchronous detect()" if args.sync_detect else
                              "detect_async(): K5/K6 of slide s on a side stream, overlapping K2 of slide s+1",
+                   "ldca_stamps": "direct u16 stores" if args.direct_stamps else
+                                  "deferred: dirty-bitmap red.or in the scan, one fold per slide fused with the LDCA view",
                    "pool_bytes": det.pool.memory_bytes(), "l2": "pool 403 MB exceeds L2; inputs 4 GiB"},
         "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
@@ -822,6 +826,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
     ap.add_argument("--sync-detect", action="store_true", help="config 4: synchronous detect() per slide")
+    ap.add_argument("--direct-stamps", action="store_true",
+                    help="config 4: store LDCA stamps directly instead of the deferred dirty bitmap + fold")
     ap.add_argument("--sync-finalize", action="store_true",
                     help="config 2: synchronous finalize_window() per window (default: pipelined windows)")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],

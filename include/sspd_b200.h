@@ -161,6 +161,29 @@ SSPD_API int sspd_materialize_seav_if(const void* pool, uint32_t ts_bytes, const
                                       uint64_t now_wrapped, uint64_t window_slices, uint8_t* seav_out,
                                       const unsigned long long* flag, void* stream);
 
+/* ---- deferred LDCA stamps of a sliding pool (u16 stamps) ---------------
+ * touch_batch (sliding.py:77-79) stores `now` into every LDCA slot a packet
+ * selects -- 8 random 2-byte stores per packet into a region larger than L2.
+ * Within one slice every such store writes the same value, so the scan may
+ * instead record the slot in an LDCA-shaped dirty bitmap (ldca_bytes):
+ *   sspd_scan_sliding_deferred = sspd_scan_sliding_tracked (seav_view may be
+ *       NULL: no tracking) whose LDCA stamps go to `ldca_dirty` (may be
+ *       NULL: stored directly; also when the u16 fast path does not apply);
+ *   sspd_ldca_fold             = stamp now_wrapped into every dirty slot and
+ *       clear the bitmap; with ldca_view != NULL also write the packed
+ *       active-bit LDCA (as sspd_materialize_ldca after the fold) in the
+ *       same pass.  Must run before the slice advances or the stamps are
+ *       read (SlidingDetector does; TimestampPool.flush).
+ * SSPD_ERR_CONFIG when the stamps are not u16 / the layout is not 8-slot
+ * aligned. */
+SSPD_API int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                        const sspd_params* p, void* pool, uint32_t ts_bytes,
+                                        uint64_t now_wrapped, uint32_t max_blocks_per_sm,
+                                        uint8_t* seav_view, uint32_t* log, uint64_t log_entries,
+                                        unsigned long long* log_head, uint32_t* ldca_dirty, void* stream);
+SSPD_API int sspd_ldca_fold(void* pool, uint32_t ts_bytes, const sspd_params* p, uint32_t* ldca_dirty,
+                            uint64_t now_wrapped, uint64_t window_slices, uint8_t* ldca_view, void* stream);
+
 /* ---- K3 sweep: TimestampPool._sweep (sliding.py:88-94) ---------------- */
 SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
                uint64_t now_wrapped, uint64_t window_slices,

@@ -189,12 +189,20 @@ struct SeavTracker {
   uint32_t log_mask;             // ring size - 1
 };
 
-template <bool kTrack>
+// Deferred LDCA stamps (optional, `dirty != nullptr`): instead of storing
+// `now` into the 134 MB LDCA stamp region (8 random 2-byte stores per
+// packet, most of them DRAM read-modify-writes), the scan sets the slot's
+// bit in an LDCA-shaped dirty bitmap (8 MiB, L2-resident) with a `red.or`;
+// sspd_ldca_fold later writes `now` into every dirty slot in one coalesced
+// pass (and can emit the active-bit view in the same pass).  Exact: every
+// stamp written during one slice is the same `now`, and the host folds
+// before the slice changes or the stamps are read.
+template <bool kTrack, bool kDefer>
 __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32_t* __restrict__ hips,
                                                                     const uint32_t* __restrict__ oips, uint64_t n,
                                                                     const __grid_constant__ sspd_params p,
                                                                     uint16_t* pool, uint16_t now, float l2_frac,
-                                                                    SeavTracker tr) {
+                                                                    SeavTracker tr, uint32_t* dirty) {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(l2_frac));
   const uint32_t tmask = tau_mask(p.tau);
@@ -237,7 +245,11 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
 #pragma unroll 8
     for (uint32_t i = 0; i < p.lr; ++i) {
       const uint32_t c = (uint32_t)mix64(hip ^ p.seed_lh[i]) & lc_mask;
-      st_u16_hint(lpool + (((cell + c) << log2k) | b), now, pol);
+      const uint32_t slot = ((cell + c) << log2k) | b;
+      if (kDefer)
+        red_or(dirty + (slot >> 5), 1u << (slot & 31));
+      else
+        st_u16_hint(lpool + slot, now, pol);
       cell += p.lc;
     }
   };
@@ -288,13 +300,13 @@ extern "C" int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, ui
 
 static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                              void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
-                             SeavTracker tracker, void* stream);
+                             SeavTracker tracker, uint32_t* dirty, void* stream);
 
 extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                         const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
                                         uint32_t max_blocks_per_sm, void* stream) {
   return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm,
-                           SeavTracker{nullptr, nullptr, nullptr, 0u}, stream);
+                           SeavTracker{nullptr, nullptr, nullptr, 0u}, nullptr, stream);
 }
 
 extern "C" int sspd_scan_sliding_tracked(const uint32_t* hips, const uint32_t* oips, uint64_t n,
@@ -307,7 +319,26 @@ extern "C" int sspd_scan_sliding_tracked(const uint32_t* hips, const uint32_t* o
   return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm,
                            SeavTracker{reinterpret_cast<uint32_t*>(seav_view), log, log_head,
                                        (uint32_t)(log_entries - 1)},
-                           stream);
+                           nullptr, stream);
+}
+
+// Tracked (optional: seav_view may be null) scan with deferred LDCA stamps
+// (optional: ldca_dirty may be null).  When the u16 fast path does not apply
+// the stamps are stored directly -- the same result.
+extern "C" int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                          const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                          uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
+                                          uint64_t log_entries, unsigned long long* log_head, uint32_t* ldca_dirty,
+                                          void* stream) {
+  SeavTracker tr{nullptr, nullptr, nullptr, 0u};
+  if (seav_view) {
+    if (!log || !log_head || log_entries == 0 || (log_entries & (log_entries - 1)) || log_entries > (1ull << 32) ||
+        (reinterpret_cast<uintptr_t>(seav_view) & 3u))
+      return SSPD_ERR_DATA;
+    tr = SeavTracker{reinterpret_cast<uint32_t*>(seav_view), log, log_head, (uint32_t)(log_entries - 1)};
+  }
+  if (ldca_dirty && (reinterpret_cast<uintptr_t>(ldca_dirty) & 3u)) return SSPD_ERR_DATA;
+  return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm, tr, ldca_dirty, stream);
 }
 
 extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
@@ -317,7 +348,7 @@ extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uin
 
 static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                              void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
-                             SeavTracker tracker, void* stream) {
+                             SeavTracker tracker, uint32_t* dirty, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
   if (tracker.view && ts_bytes != 2) return SSPD_ERR_CONFIG;  // tracking exists only on the u16 fast path
@@ -338,7 +369,8 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
         float frac = 0.85f;
         if (const char* e = getenv("SSPD_SLIDE_L2_FRAC")) frac = (float)atof(e);
         frac = frac < 0.f ? 0.f : (frac > 1.f ? 1.f : frac);
-        auto kern = tracker.view ? scan_sliding_u16_fast_kernel<true> : scan_sliding_u16_fast_kernel<false>;
+        auto kern = tracker.view ? (dirty ? scan_sliding_u16_fast_kernel<true, true> : scan_sliding_u16_fast_kernel<true, false>)
+                                 : (dirty ? scan_sliding_u16_fast_kernel<false, true> : scan_sliding_u16_fast_kernel<false, false>);
         int grid = grid_for(kern, 256, (n + 3) / 4);
         // optional cap (blocks per SM) so kernels on other streams (the
         // pipelined detect) stay co-resident with this store-bound scan
@@ -351,7 +383,7 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
           const int cap = (int)cap_bps * sms;
           if (grid > cap) grid = cap;
         }
-        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker);
+        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker, dirty);
         break;
       }
       if (tracker.view) return SSPD_ERR_CONFIG;  // tracking exists only on the fast path

@@ -293,6 +293,70 @@ extern "C" int sspd_materialize_ldca(const void* pool, uint32_t ts_bytes, const 
   return check_launch();
 }
 
+// Fold of the deferred LDCA stamps (scan.cu, kDefer): every slot whose bit
+// is set in `dirty` gets stamp `now`, the bitmap is cleared, and -- when
+// `view` is given -- the packed active-bit LDCA view (sliding.py:205-220) is
+// written in the same pass: active = dirty | (age(old stamp) < w).  One
+// thread per dirty word = 32 slots = 64 B of stamps.  Without a view, clean
+// words cost only the 4-byte bitmap read.
+__device__ __forceinline__ uint32_t stamp_pairs(uint32_t w, uint32_t m2, uint32_t now) {
+  const uint32_t lo = (m2 & 1u) ? now : (w & 0xFFFFu);
+  const uint32_t hi = (m2 & 2u) ? now : (w >> 16);
+  return lo | (hi << 16);
+}
+
+template <bool kView>
+__global__ void __launch_bounds__(256) ldca_fold_u16_kernel(uint16_t* __restrict__ pool, uint64_t base,
+                                                            uint64_t nwords, uint32_t* __restrict__ dirty,
+                                                            uint16_t now, uint32_t window, uint32_t* __restrict__ view) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) {
+    const uint32_t d = __ldcg(dirty + q);
+    if (!kView && d == 0) continue;
+    uint4* src = reinterpret_cast<uint4*>(pool + base) + q * 4;
+    uint32_t act = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) {
+      const uint32_t m = (d >> (8 * j)) & 0xFFu;
+      if (!kView && m == 0) continue;
+      uint4 v = __ldcg(src + j);
+      if (kView) act |= active8_u16(v, now, window) << (8 * j);
+      if (m) {
+        v.x = stamp_pairs(v.x, m, now);
+        v.y = stamp_pairs(v.y, m >> 2, now);
+        v.z = stamp_pairs(v.z, m >> 4, now);
+        v.w = stamp_pairs(v.w, m >> 6, now);
+        src[j] = v;
+      }
+    }
+    if (kView) view[q] = act | d;  // a dirty slot is stamped `now`: age 0 < w
+    if (d) dirty[q] = 0;
+  }
+}
+
+extern "C" int sspd_ldca_fold(void* pool, uint32_t ts_bytes, const sspd_params* p, uint32_t* dirty,
+                              uint64_t now_wrapped, uint64_t window_slices, uint8_t* ldca_view, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!pool || !dirty) return SSPD_ERR_DATA;
+  if (ts_bytes != 2 || (p->ldca_bytes & 3u) || (p->slot_ldca_base & 7u) || (reinterpret_cast<uintptr_t>(pool) & 15u) ||
+      (reinterpret_cast<uintptr_t>(dirty) & 3u) || (reinterpret_cast<uintptr_t>(ldca_view) & 3u))
+    return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nwords = p->ldca_bytes >> 2;
+  if (ldca_view) {
+    const int grid = grid_for(ldca_fold_u16_kernel<true>, 256, nwords);
+    ldca_fold_u16_kernel<true><<<grid, 256, 0, st>>>((uint16_t*)pool, p->slot_ldca_base, nwords, dirty,
+                                                     (uint16_t)now_wrapped, (uint32_t)window_slices,
+                                                     reinterpret_cast<uint32_t*>(ldca_view));
+  } else {
+    const int grid = grid_for(ldca_fold_u16_kernel<false>, 256, nwords);
+    ldca_fold_u16_kernel<false><<<grid, 256, 0, st>>>((uint16_t*)pool, p->slot_ldca_base, nwords, dirty,
+                                                      (uint16_t)now_wrapped, (uint32_t)window_slices, nullptr);
+  }
+  return check_launch();
+}
+
 static bool seav_fast_layout(const void* pool, const sspd_params* p, const void* out) {
   bool ok = p->g == 8 && p->reg_bytes == 1 && (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
             (reinterpret_cast<uintptr_t>(out) & 3u) == 0;

@@ -71,16 +71,42 @@ class TimestampPool:
         self._since_sweep = 0
         self.sweep_count = 0
         self._version = 0  # bumped by every stamp write that bypasses SlidingDetector
+        self._deferred = None  # _DeferredLdca of the owning SlidingDetector (pending LDCA stamps)
         init = (-window_slices) & self._mask  # age == window: just expired
         self._buf = torch.full((n_slots,), _as_signed(init, self.ts_bytes),
                                dtype=_signed_torch(self.ts_bytes), device=device())
 
     # -- state --------------------------------------------------------------
     def device_buffer(self):
+        """The stamp array on the device, with any deferred stamps applied."""
+        self.flush()
         return self._buf
+
+    def flush(self, ldca_view=None):
+        """Apply the LDCA stamps a deferred scan recorded in its dirty bitmap
+        (sspd_ldca_fold); with `ldca_view` (a device byte buffer) also write
+        the packed active-bit LDCA in the same pass.  Returns True when the
+        view was written."""
+        d = self._deferred
+        if d is None or not d.pending:
+            return False
+        from ._device import call, stream_ptr
+
+        call("sspd_ldca_fold", self._buf.data_ptr(), self.ts_bytes, d.params, d.dirty.data_ptr(),
+             self._wrapped_now(), self.window_slices, None if ldca_view is None else ldca_view.data_ptr(),
+             stream_ptr())
+        d.pending = False
+        return ldca_view is not None
+
+    def _drop_deferred(self):
+        d = self._deferred
+        if d is not None and d.pending:
+            d.dirty.zero_()
+            d.pending = False
 
     def reset(self):
         """Back to the constructor state (slice 0, every slot just expired)."""
+        self._drop_deferred()
         self.now = 0
         self._since_sweep = 0
         self.sweep_count = 0
@@ -89,7 +115,7 @@ class TimestampPool:
 
     @property
     def ts(self) -> np.ndarray:
-        return self._buf.cpu().numpy().view(self.dtype)
+        return self.device_buffer().cpu().numpy().view(self.dtype)
 
     @ts.setter
     def ts(self, values: np.ndarray):
@@ -99,6 +125,7 @@ class TimestampPool:
         if arr.shape != (self.n_slots,):
             raise ConfigError("timestamp array shape mismatch")
         signed = arr.view(_signed_torch_np(self.ts_bytes))
+        self._drop_deferred()  # the new array replaces every stamp
         self._version += 1
         self._buf.copy_(torch.from_numpy(signed))
 
@@ -117,7 +144,7 @@ class TimestampPool:
         candidate_age = self.now - now
         if candidate_age < 0:
             raise ConfigError(f"cannot stamp future slice {now} (pool is at {self.now})")
-        current = int(self._buf[slot_index].item()) & self._mask
+        current = int(self.device_buffer()[slot_index].item()) & self._mask
         existing_age = (self._wrapped_now() - current) & self._mask
         if candidate_age < existing_age:
             self._version += 1
@@ -127,10 +154,12 @@ class TimestampPool:
         import torch
 
         idx = torch.as_tensor(np.asarray(slot_indexes, dtype=np.int64)).to(self._buf.device)
+        self.flush()
         self._version += 1
         self._buf.index_fill_(0, idx, _as_signed(self._wrapped_now(), self.ts_bytes))
 
     def advance_slice(self):
+        self.flush()  # deferred stamps belong to the slice that ends here
         self.now += 1
         self._since_sweep += 1
         if self._since_sweep >= self._sweep_period:
@@ -152,7 +181,7 @@ class TimestampPool:
         from ._device import call, stream_ptr
 
         out = torch.empty(self.n_slots, dtype=torch.int64, device=self._buf.device)
-        call("sspd_pool_ages", self._buf.data_ptr(), self.n_slots, self.ts_bytes, self._wrapped_now(),
+        call("sspd_pool_ages", self.device_buffer().data_ptr(), self.n_slots, self.ts_bytes, self._wrapped_now(),
              out.data_ptr(), stream_ptr())
         return out.cpu().numpy().view(np.uint64)
 
@@ -160,7 +189,7 @@ class TimestampPool:
         return self.ages() < self.window_slices
 
     def is_active(self, slot_index: int) -> bool:
-        current = int(self._buf[slot_index].item()) & self._mask
+        current = int(self.device_buffer()[slot_index].item()) & self._mask
         return ((self._wrapped_now() - current) & self._mask) < self.window_slices
 
 
@@ -176,6 +205,17 @@ def touch(pool: TimestampPool, slot_index: int, now: int) -> TimestampPool:
 def advance_slice(pool: TimestampPool) -> TimestampPool:
     pool.advance_slice()
     return pool
+
+
+class _DeferredLdca:
+    """Dirty bitmap of LDCA stamps not yet written (sspd_scan_sliding_deferred)."""
+
+    def __init__(self, params, nbytes: int):
+        from ._device import zeros_bytes
+
+        self.params = params
+        self.dirty = zeros_bytes(nbytes)
+        self.pending = False
 
 
 @dataclass(frozen=True)
@@ -194,6 +234,9 @@ class SlidingDetector:
     # instead of re-reading the whole SEAV stamp region at every detect
     incremental_seav = True
     seav_log_entries = 1 << 25  # ring of logged SEAV stamps (4 B each)
+    # record LDCA stamps in a dirty bitmap and write them once per slice
+    # (sspd_ldca_fold, fused with the LDCA view at detect)
+    defer_ldca_stamps = True
 
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
@@ -276,6 +319,27 @@ class SlidingDetector:
             iv["meta"][1] = 1
             iv["version"], iv["now"] = pool._version, pool.now
 
+    def _deferred(self):
+        """The pool's deferred-LDCA state (created on first use), or None when
+        the stamps are not u16 with an 8-slot aligned LDCA region."""
+        pool, p = self.pool, self._params
+        d = pool._deferred
+        if d is None and self.defer_ldca_stamps and pool.ts_bytes == 2 and (p.slot_ldca_base & 7) == 0 \
+                and p.ldca_bytes % 4 == 0 and p.slot_total < (1 << 32):
+            d = pool._deferred = _DeferredLdca(p, p.ldca_bytes)
+        return d if self.defer_ldca_stamps else None
+
+    def _ldca_view_into(self, lview):
+        """Packed active-bit LDCA into `lview`: fused with the fold of the
+        deferred stamps when some are pending, else K4 over the stamps."""
+        pool = self.pool
+        if pool.flush(ldca_view=lview):
+            return
+        from ._device import call, stream_ptr
+
+        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+             pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
+
     def _seav_view(self):
         """The SEAV active-bit view for the current slice as a SeavSketch
         (device): the incremental one (materialized in full only if it was
@@ -311,12 +375,20 @@ class SlidingDetector:
         # for the finalize kernels running on the side stream
         cap = self.pipelined_scan_blocks_per_sm if getattr(self, "_async", None) else 0
         iv = self._iv()
-        if iv is not None:
-            self._iv_check(iv)
-            call("sspd_scan_sliding_tracked", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
-                 pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
-                 iv["view"].device_buffer().data_ptr(), iv["log"].data_ptr(), iv["log"].numel(),
-                 iv["meta"].data_ptr(), stream_ptr())
+        dfr = self._deferred()
+        if iv is not None or dfr is not None:
+            if iv is not None:
+                self._iv_check(iv)
+            # pool._buf: the scan itself needs no flush (pending and new
+            # deferred stamps are the same `now`)
+            call("sspd_scan_sliding_deferred", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+                 pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
+                 None if iv is None else iv["view"].device_buffer().data_ptr(),
+                 None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
+                 None if iv is None else iv["meta"].data_ptr(),
+                 None if dfr is None else dfr.dirty.data_ptr(), stream_ptr())
+            if dfr is not None:
+                dfr.pending = True
         else:
             call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
                  pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
@@ -339,14 +411,12 @@ class SlidingDetector:
         return sketch
 
     def materialize_ldca(self) -> np.ndarray:
-        from ._device import call, stream_ptr, zeros_bytes
+        from ._device import zeros_bytes
 
-        pool = self.pool
         lc = self.ldca_config
         nbytes = lc.lr * lc.lc * lc.k // 8
         out = zeros_bytes(nbytes)
-        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
-             pool._wrapped_now(), pool.window_slices, out.data_ptr(), stream_ptr())
+        self._ldca_view_into(out)
         return out[:nbytes].cpu().numpy().reshape(lc.lr, lc.lc, lc.k // 8)
 
     def materialize_ldca_cell(self, row: int, col: int) -> np.ndarray:
@@ -374,17 +444,15 @@ class SlidingDetector:
         """Materialise (K4: SEAV registers + packed LDCA) -> fused finalize
         (K5 restore, sort, K6 filter, compaction; one host round trip)
         (sliding.py:232-248)."""
-        from ._device import call, stream_ptr, zeros_bytes
+        from ._device import zeros_bytes
 
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
-        seav = self._seav_view()
         lview = getattr(self, "_ldca_view", None)
         if lview is None:
             lview = self._ldca_view = zeros_bytes(self._params.ldca_bytes)
-        pool = self.pool
-        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
-             pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
+        self._ldca_view_into(lview)  # first: fused with the fold of deferred stamps
+        seav = self._seav_view()
         fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff)
         return fin.reports(self.now, "sliding")
 
@@ -403,7 +471,7 @@ class SlidingDetector:
         as `detect()` (window_id = the slice of this call)."""
         import torch
 
-        from ._device import call, stream_ptr, zeros_bytes
+        from ._device import zeros_bytes
 
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
@@ -421,14 +489,12 @@ class SlidingDetector:
         elif vset[2] is not None:
             vset[2].resolve()  # the finalize `pipeline_depth` calls ago is done with this view set
         seav, lview = vset[0], vset[1]
-        pool = self.pool
+        self._ldca_view_into(lview)  # first: fused with the fold of deferred stamps
         if self._iv() is not None:  # snapshot of the incremental view (16 MiB at r=16)
             src = self._seav_view().device_buffer()
             seav.device_buffer()[: src.numel()].copy_(src)
         else:
             self._materialize_into(seav)
-        call("sspd_materialize_ldca", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
-             pool._wrapped_now(), pool.window_slices, lview.data_ptr(), stream_ptr())
         views_ready = torch.cuda.Event()
         views_ready.record(torch.cuda.current_stream())
         side = st["side"]

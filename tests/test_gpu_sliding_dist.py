@@ -383,3 +383,80 @@ def test_incremental_seav_view_equals_full_materialization(cuda):
     assert int(a._iv()["meta"][1].item()) == 0
     for s in range(420, 600):
         step(s)
+
+
+def test_deferred_ldca_stamps_equal_direct_stamps(cuda):
+    """Deferred LDCA stamps (dirty bitmap + sspd_ldca_fold, fused with the
+    LDCA view at detect) leave exactly the pool the direct u16 stores leave,
+    through every way the pool is read or written: several observes per
+    slice, reads mid-slice (ts, ages, is_active, materialize_ldca), detect
+    and detect_async, touch / touch_batch / ts assignment around the
+    detector, a forced anti-alias sweep, pool merge, and reset."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector, merge_timestamp_pools
+
+    params = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5)
+    w = 130  # u16 stamps (2w + 2 > 255); 170 slices so slots expire
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=w)
+        b = SlidingDetector(params, window_slices=w)
+    b.defer_ldca_stamps = False
+    assert a.pool.ts_bytes == 2 and a._deferred() is not None and b._deferred() is None
+    rng = np.random.default_rng(99)
+    heavy = rng.integers(0, 2**32, size=4, dtype=np.uint64)
+    base = a.layout.ldca_base
+    pend = []
+    for s in range(170):
+        for _ in range(1 + s % 3):  # several batches per slice
+            n = int(rng.integers(1, 20_000))
+            hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+            oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+            hips[: n // 3] = heavy[(s // 9) % len(heavy)]
+            a.observe_batch(hips, oips)
+            b.observe_batch(hips, oips)
+        if s % 7 == 3:  # reads mid-slice, then more packets in the same slice
+            assert np.array_equal(a.pool.ts, b.pool.ts), s
+            slot = base + int(rng.integers(0, a.layout.total - base))
+            assert a.pool.is_active(slot) == b.pool.is_active(slot)
+            assert np.array_equal(a.materialize_ldca(), b.materialize_ldca()), s
+            hips = rng.integers(0, 2**32, size=5000, dtype=np.uint64)
+            oips = rng.integers(0, 2**32, size=5000, dtype=np.uint64)
+            a.observe_batch(hips, oips)
+            b.observe_batch(hips, oips)
+        if s % 5 == 1 and s % 20 == 1:
+            assert rep_list(a.detect()) == rep_list(b.detect()), s
+        else:
+            pend.append((a.detect_async(), b.detect_async()))
+        if s == 20:  # writes around the detector
+            idx = np.arange(base, base + 4096, 7)
+            for det in (a, b):
+                det.pool.touch_batch(idx)
+                det.pool.touch(base + 5)
+        if s == 30:
+            ts = a.pool.ts.copy()
+            ts[base: base + 1000] = (a.pool.now - 3) & a.pool._mask
+            a.observe_batch(heavy, heavy)  # pending deferred stamps, then replaced
+            a.pool.ts = ts
+            b.observe_batch(heavy, heavy)
+            b.pool.ts = ts
+        if s == 150:  # force the anti-alias sweep at the next advance
+            for det in (a, b):
+                det.pool._since_sweep = det.pool._sweep_period - 1
+        a.advance_slice()
+        b.advance_slice()
+        assert np.array_equal(a.pool.ages(), b.pool.ages()), s
+    assert a.pool.sweep_count == b.pool.sweep_count == 1
+    for x, y in pend:
+        assert rep_list(x) == rep_list(y)
+    assert sum(len(x) for x, _ in pend) > 0
+    # merge: the deferred pool's pending stamps take part
+    hips = rng.integers(0, 2**32, size=3000, dtype=np.uint64)
+    a.observe_batch(hips, hips)
+    b.observe_batch(hips, hips)
+    ma = merge_timestamp_pools([a.pool, b.pool])
+    assert np.array_equal(ma.ts, b.pool.ts) and ma._deferred is None
+    a.observe_batch(hips, hips[::-1].copy())
+    a.reset()
+    b.reset()
+    assert np.array_equal(a.pool.ts, b.pool.ts)
+    assert not a.pool._deferred.pending and int(a.pool._deferred.dirty.count_nonzero()) == 0
