@@ -15,14 +15,28 @@ except ImportError as exc:  # pragma: no cover - torch is part of the image
     raise DeviceError("PyTorch is required for device buffers") from exc
 
 
+_ready = False
+
+
 def device():
-    if not torch.cuda.is_available():
-        raise DeviceError("no CUDA device: the sspd B200 path has no CPU fallback")
-    lib()
+    global _ready
+    if not _ready:
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the sspd B200 path has no CPU fallback")
+        lib()
+        _ready = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_cur_dev = getattr(torch._C, "_cuda_getDevice", None)
+
+
 def stream_ptr() -> int:
+    """Raw cudaStream_t of the current torch stream (a per-launch call: the
+    direct C accessors instead of building a torch.cuda.Stream object)."""
+    if _raw_stream is not None and _cur_dev is not None:
+        return _raw_stream(_cur_dev())
     return torch.cuda.current_stream().cuda_stream
 
 

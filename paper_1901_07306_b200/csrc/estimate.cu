@@ -784,10 +784,12 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t C = (size_t)capacity;
   const size_t vec = ((C * 4 + 255) / 256) * 256;
+  // the filter and the report list need the candidate IPs only: sort keys
+  // (restore's AND-weights are not part of a report)
   size_t sort_tmp = 0;
   {
-    cub::DoubleBuffer<uint32_t> k0(nullptr, nullptr), v0(nullptr, nullptr);
-    if (cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, k0, v0, (int)C, 0, 32, st) != cudaSuccess)
+    cub::DoubleBuffer<uint32_t> k0(nullptr, nullptr);
+    if (cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, k0, (int)C, 0, 32, st) != cudaSuccess)
       return SSPD_ERR_CUDA;
   }
   const size_t segs = (C + kSeg - 1) / kSeg;
@@ -816,8 +818,8 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   rc = sspd_restore(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, stream);
   if (rc) return rc;
   size_t tb = sort_tmp;
-  cub::DoubleBuffer<uint32_t> kb(ip, ipa), vb(aux, auxa);
-  if (cub::DeviceRadixSort::SortPairs(s8 + o_tmp, tb, kb, vb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
+  cub::DoubleBuffer<uint32_t> kb(ip, ipa);
+  if (cub::DeviceRadixSort::SortKeys(s8 + o_tmp, tb, kb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
   const uint32_t* sorted = kb.Current();
   const int grid = grid_for(filter_kernel, 256, C * 32);
   filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);

@@ -311,26 +311,48 @@ __global__ void __launch_bounds__(256) ldca_fold_u16_kernel(uint16_t* __restrict
                                                             uint16_t now, uint32_t window, uint32_t* __restrict__ view) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) {
-    const uint32_t d = __ldcg(dirty + q);
-    if (!kView && d == 0) continue;
     uint4* src = reinterpret_cast<uint4*>(pool + base) + q * 4;
-    uint32_t act = 0;
+    const uint32_t d = __ldcg(dirty + q);
+    if (kView) {
+      // the view needs every stamp: issue the four 16-B loads with the
+      // bitmap load instead of after it
+      uint4 v[4];
 #pragma unroll
-    for (uint32_t j = 0; j < 4; ++j) {
-      const uint32_t m = (d >> (8 * j)) & 0xFFu;
-      if (!kView && m == 0) continue;
-      uint4 v = __ldcg(src + j);
-      if (kView) act |= active8_u16(v, now, window) << (8 * j);
-      if (m) {
-        v.x = stamp_pairs(v.x, m, now);
-        v.y = stamp_pairs(v.y, m >> 2, now);
-        v.z = stamp_pairs(v.z, m >> 4, now);
-        v.w = stamp_pairs(v.w, m >> 6, now);
-        src[j] = v;
+      for (uint32_t j = 0; j < 4; ++j) v[j] = __ldcg(src + j);
+      uint32_t act = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) act |= active8_u16(v[j], now, window) << (8 * j);
+      view[q] = act | d;  // a dirty slot is stamped `now`: age 0 < w
+      if (d == 0) continue;
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) {
+        const uint32_t m = (d >> (8 * j)) & 0xFFu;
+        if (m) {
+          uint4 u = v[j];
+          u.x = stamp_pairs(u.x, m, now);
+          u.y = stamp_pairs(u.y, m >> 2, now);
+          u.z = stamp_pairs(u.z, m >> 4, now);
+          u.w = stamp_pairs(u.w, m >> 6, now);
+          src[j] = u;
+        }
       }
+      dirty[q] = 0;
+    } else {
+      if (d == 0) continue;
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) {
+        const uint32_t m = (d >> (8 * j)) & 0xFFu;
+        if (m) {
+          uint4 u = __ldcg(src + j);
+          u.x = stamp_pairs(u.x, m, now);
+          u.y = stamp_pairs(u.y, m >> 2, now);
+          u.z = stamp_pairs(u.z, m >> 4, now);
+          u.w = stamp_pairs(u.w, m >> 6, now);
+          src[j] = u;
+        }
+      }
+      dirty[q] = 0;
     }
-    if (kView) view[q] = act | d;  // a dirty slot is stamped `now`: age 0 < w
-    if (d) dirty[q] = 0;
   }
 }
 

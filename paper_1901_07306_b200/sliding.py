@@ -72,6 +72,7 @@ class TimestampPool:
         self.sweep_count = 0
         self._version = 0  # bumped by every stamp write that bypasses SlidingDetector
         self._deferred = None  # _DeferredLdca of the owning SlidingDetector (pending LDCA stamps)
+        self._pristine = True  # constructor/reset state (no stamp written since)
         init = (-window_slices) & self._mask  # age == window: just expired
         self._buf = torch.full((n_slots,), _as_signed(init, self.ts_bytes),
                                dtype=_signed_torch(self.ts_bytes), device=device())
@@ -111,6 +112,7 @@ class TimestampPool:
         self._since_sweep = 0
         self.sweep_count = 0
         self._version += 1
+        self._pristine = True
         self._buf.fill_(_as_signed((-self.window_slices) & self._mask, self.ts_bytes))
 
     @property
@@ -127,6 +129,7 @@ class TimestampPool:
         signed = arr.view(_signed_torch_np(self.ts_bytes))
         self._drop_deferred()  # the new array replaces every stamp
         self._version += 1
+        self._pristine = False
         self._buf.copy_(torch.from_numpy(signed))
 
     def memory_bytes(self) -> int:
@@ -148,6 +151,7 @@ class TimestampPool:
         existing_age = (self._wrapped_now() - current) & self._mask
         if candidate_age < existing_age:
             self._version += 1
+            self._pristine = False
             self._buf[slot_index] = _as_signed(now & self._mask, self.ts_bytes)
 
     def touch_batch(self, slot_indexes):
@@ -156,6 +160,7 @@ class TimestampPool:
         idx = torch.as_tensor(np.asarray(slot_indexes, dtype=np.int64)).to(self._buf.device)
         self.flush()
         self._version += 1
+        self._pristine = False
         self._buf.index_fill_(0, idx, _as_signed(self._wrapped_now(), self.ts_bytes))
 
     def advance_slice(self):
@@ -305,7 +310,7 @@ class SlidingDetector:
                   "log": torch.empty(self.seav_log_entries, dtype=torch.int32, device=device()),
                   "meta": torch.zeros(4 + nseg, dtype=torch.int64, device=device()),
                   "nseg": nseg, "version": pool._version, "now": pool.now}
-            if pool._version or pool.now or self.pair_count:
+            if not pool._pristine or pool.now or self.pair_count:
                 st["meta"][1] = 1  # enabled late: the view starts invalid (full materialization)
         self._iv_state = st
         return st

@@ -192,6 +192,9 @@ def device_keep_table(k: int, cutoff: float):
     return t
 
 
+_FINALIZE_SCRATCH: dict = {}  # capacity -> sspd_finalize work-space bytes
+
+
 class DeviceFinalize:
     """One fused finalize (`sspd_finalize`: K5 restore -> sort -> K6 filter ->
     compaction) enqueued on a stream without any host round trip.
@@ -222,23 +225,26 @@ class DeviceFinalize:
 
         seav = self.seav
         self.cap = cap
+        nflag_words = ((1 << seav.config.r) + 3) // 4
         with torch.cuda.stream(self.stream):
             dev = seav._buf.device
             table = device_keep_table(self.k, self.cutoff)
-            self.out = torch.empty(2 * cap + 4, dtype=torch.int32, device=dev)  # ip | z0 | counts (2 x u64)
-            ovf = torch.empty(1 << seav.config.r, dtype=torch.uint8, device=dev)
-            need = ctypes.c_size_t(0)
-            call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None,
-                 ctypes.byref(need), 0)
-            scratch = seav._scratch(need.value)
+            # one device block: ip[cap] | z0[cap] | counts (2 x u64) | overflow flags (2^r B)
+            self.out = torch.empty(2 * cap + 4 + nflag_words, dtype=torch.int32, device=dev)
+            base = self.out.data_ptr()
+            need = _FINALIZE_SCRATCH.get(cap)
+            if need is None:
+                nb = ctypes.c_size_t(0)
+                call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None,
+                     ctypes.byref(nb), 0)
+                need = _FINALIZE_SCRATCH[cap] = nb.value
+            scratch = seav._scratch(need)
             call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
-                 table.data_ptr(), cap, self.out.data_ptr(), self.out[cap:].data_ptr(),
-                 self.out[2 * cap:].data_ptr(), ovf.data_ptr(), scratch.data_ptr(), ctypes.byref(need),
-                 self.stream.cuda_stream)
-            self.h_counts = torch.empty(4, dtype=torch.int32, pin_memory=True)
-            self.h_ovf = torch.empty(ovf.numel(), dtype=torch.uint8, pin_memory=True)
-            self.h_counts.copy_(self.out[2 * cap:], non_blocking=True)
-            self.h_ovf.copy_(ovf, non_blocking=True)
+                 table.data_ptr(), cap, base, base + 4 * cap, base + 8 * cap, base + 8 * cap + 16,
+                 scratch.data_ptr(), ctypes.byref(ctypes.c_size_t(need)), self.stream.cuda_stream)
+            # counts + flags back in ONE pinned copy
+            self.h_tail = torch.empty(4 + nflag_words, dtype=torch.int32, pin_memory=True)
+            self.h_tail.copy_(self.out[2 * cap:], non_blocking=True)
             self.event = torch.cuda.Event()
             self.event.record(self.stream)
 
@@ -249,13 +255,15 @@ class DeviceFinalize:
         from .errors import SeaOverflowError
 
         self.event.synchronize()
-        found, kept = (int(x) for x in self.h_counts.numpy().view(np.int64))
+        found, kept = (int(x) for x in self.h_tail[:4].numpy().view(np.int64))
         if found > self.cap:  # candidates did not fit: learn the size, run again
             self.seav._cand_cap = 1 << (found - 1).bit_length()
             self._launch(self.seav._cand_cap)
             self.event.synchronize()
-            found, kept = (int(x) for x in self.h_counts.numpy().view(np.int64))
-        for rp in np.nonzero(self.h_ovf.numpy())[0].tolist():
+            found, kept = (int(x) for x in self.h_tail[:4].numpy().view(np.int64))
+        self.found = found  # candidates restored
+        flags = self.h_tail[4:].numpy().view(np.uint8)[: 1 << self.seav.config.r]
+        for rp in np.nonzero(flags)[0].tolist():
             err = SeaOverflowError(rp, self.seav.restore_cap)
             if self.on_overflow != "warn":
                 raise err
