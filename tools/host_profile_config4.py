@@ -1,3 +1,12 @@
+"""Host-side cost of the config-4 sliding loop (diagnostic, not a bench).
+
+    python tools/host_profile_config4.py
+
+Runs the bench's per-slide loop (observe_batch -> detect_async ->
+advance_slice) twice and prints the host time per call and per slide, then a
+cProfile of one more pass: separates Python/launch overhead from waiting on
+the device (Event.synchronize).
+"""
 import sys, time, warnings, torch, numpy as np
 sys.path.insert(0, '.')
 from paper_1901_07306_b200 import DetectorParams, SlidingDetector
