@@ -552,13 +552,16 @@ def run_sliding(args) -> dict:
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    # K2 alone over the same trace (observe + advance, same grid cap as in
-    # the timed run) against the measured random-u16-store rate at the LDCA
-    # stamp footprint: the store-bound roofline of the sliding scan
+    # K2 alone over the same trace.  Deferred stamps (default): observe
+    # every slice without advancing (the dirty bitmap absorbs it, no fold),
+    # against the live-measured random L2 red.or rate -- the scan's bound;
+    # direct stamps: observe + advance against the random u16 store rate at
+    # the LDCA stamp footprint.
     import ctypes
 
     from paper_1901_07306_b200._abi import lib
 
+    deferred = not args.direct_stamps
     det.reset()
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -567,24 +570,50 @@ def run_sliding(args) -> dict:
         lo, hi = bounds[s], bounds[s + 1]
         if hi > lo:
             det.observe_batch(hips[lo:hi], oips[lo:hi])
-        det.advance_slice()
+        if not deferred:
+            det.advance_slice()
     s1.record(stream)
     torch.cuda.synchronize()
     scan_ms = s0.elapsed_time(s1)
+    det.reset()
     lcfg = det.ldca_config
-    foot = 1 << max(1, (2 * lcfg.lr * lcfg.lc * lcfg.k - 1).bit_length())  # LDCA stamp bytes, pow2
-    sbuf = torch.empty(foot, dtype=torch.uint8, device=dev)
-    rate = ctypes.c_double(0.0)
-    lib().sspd_microbench_store16(sbuf.data_ptr(), foot, 8, 256, ctypes.byref(rate), stream.cuda_stream)
-    del sbuf
-    stores_pp = lcfg.lr + det.seav_config.sr / (1 << det.seav_config.tau)
     scan_gpps = n / (scan_ms * 1e-3) / 1e9
-    store_roof = rate.value / stores_pp / 1e9
-    # roofline of K2: 8 scattered 2-byte stores/packet into a 403 MB pool (> L2):
-    # HBM sector read-modify-write bound (8 + 8.031 x 32 B)
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
-    bytes_pp = 8 + 8.031 * 32
+    seav_pp = det.seav_config.sr / (1 << det.seav_config.tau)
+    if deferred:
+        buf = torch.empty(8 << 20, dtype=torch.uint8, device=dev)
+        rate = ctypes.c_double(0.0)
+        lib().sspd_microbench_red(buf.data_ptr(), 8 << 20, 8, 256, ctypes.byref(rate), stream.cuda_stream)
+        del buf
+        ops_pp = lcfg.lr + 2 * seav_pp  # LDCA dirty bits + SEAV view bits (+ SEAV stamps, stores)
+        scan_roof = {"bound": "l2_red", "l2_red_ops_per_s": round(rate.value / 1e9, 2), "reds_per_packet": ops_pp,
+                     "note": "K2 (deferred) over the whole trace alone: 8 dirty-bitmap red.or + the SEAV view "
+                             "atomics per packet into L2-resident bitmaps, vs the live-measured random red.or rate"}
+    else:
+        foot = 1 << max(1, (2 * lcfg.lr * lcfg.lc * lcfg.k - 1).bit_length())  # LDCA stamp bytes, pow2
+        sbuf = torch.empty(foot, dtype=torch.uint8, device=dev)
+        rate = ctypes.c_double(0.0)
+        lib().sspd_microbench_store16(sbuf.data_ptr(), foot, 8, 256, ctypes.byref(rate), stream.cuda_stream)
+        del sbuf
+        ops_pp = lcfg.lr + seav_pp
+        scan_roof = {"bound": "random_u16_store", "store_rate_gops": round(rate.value / 1e9, 2),
+                     "footprint_bytes": foot, "stores_per_packet": round(ops_pp, 4),
+                     "note": "K2 over the whole trace alone vs the live-measured random st.global.u16 rate at "
+                             "the LDCA stamp footprint"}
+    roof_gpps = rate.value / ops_pp / 1e9
+    scan_roof.update({"roofline_gpps": round(roof_gpps, 3), "achieved_gpps": round(scan_gpps, 3),
+                      "frac": round(scan_gpps / roof_gpps, 4), "scan_ms_per_trace": round(scan_ms, 3)})
+    # whole-trace HBM model: the input (8 B/pkt) plus, deferred, one fold per
+    # slide that reads and rewrites the LDCA stamp region (2 B/slot) and
+    # reads/clears the dirty bitmap + writes the view; direct, one 32-B sector
+    # read-modify-write per scattered stamp (8 + 8.031 x 32 B)
+    ldca_bytes = lcfg.lr * lcfg.lc * lcfg.k // 8
+    if deferred:
+        fold_bytes = 2 * (2 * lcfg.lr * lcfg.lc * lcfg.k) + 3 * ldca_bytes
+        bytes_pp = 8 + fold_bytes * n_sl / n
+    else:
+        bytes_pp = 8 + 8.031 * 32
     value = n / (ms * 1e-3) / 1e6
     return {
         "metric": "packets/sec (Mpps) sliding scan+detect at every slide", "value": round(value, 3), "unit": UNIT,
@@ -599,15 +628,9 @@ def run_sliding(args) -> dict:
                    "pool_bytes": det.pool.memory_bytes(), "l2": "pool 403 MB exceeds L2; inputs 4 GiB"},
         "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
-                     "kernel": "whole trace (K2 + per-slide K4/K5/K6)", "bytes_per_packet_model": bytes_pp},
-        "scan_roofline": {"bound": "random_u16_store", "store_rate_gops": round(rate.value / 1e9, 2),
-                          "footprint_bytes": foot, "stores_per_packet": round(stores_pp, 4),
-                          "roofline_gpps": round(store_roof, 3), "achieved_gpps": round(scan_gpps, 3),
-                          "frac": round(scan_gpps / store_roof, 4), "scan_ms_per_trace": round(scan_ms, 3),
-                          "scan_share_of_step": round(scan_ms / ms, 4),
-                          "note": "K2 over the whole trace alone vs the live-measured random st.global.u16 rate at "
-                                  "the LDCA stamp footprint (the SURVEY's 265 B/pkt HBM model assumes peak "
-                                  "bandwidth for random 32 B sector writes)"},
+                     "kernel": "whole trace (K2 + per-slide fold/K4/K5/K6)",
+                     "bytes_per_packet_model": round(bytes_pp, 2)},
+        "scan_roofline": {**scan_roof, "scan_share_of_step": round(scan_ms / ms, 4)},
         "clocks": clk, "detect": {"reports_total": counts[0] if counts else None, "slides": n_sl,
                                   "planted": len(supers)},
         "gen_s": round(t_gen, 2),
