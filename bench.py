@@ -84,6 +84,13 @@ class ClockSampler:
         self.lines: list[str] = []
         self.samples: list[tuple[float, float, int]] = []
         self._stop = threading.Event()
+        self._mark = 0
+
+    def mark(self):
+        """Start of the timed region: stop() reports the samples from here on
+        (the sampler is started before the warm-up so that NVML's start-up
+        does not overlap the timed steps)."""
+        self._mark = len(self.samples) if self.nvml is not None else len(self.lines)
 
     def start(self):
         try:
@@ -126,9 +133,10 @@ class ClockSampler:
         if self.nvml is not None:
             self._stop.set()
             self._t.join(timeout=2)
-            sm = [a for a, _, _ in self.samples]
-            mx = [b for _, b, _ in self.samples]
-            found = {name for bit, name in self.REASONS.items() for _, _, r in self.samples if r & bit}
+            samples = self.samples[self._mark:] or self.samples[-1:]
+            sm = [a for a, _, _ in samples]
+            mx = [b for _, b, _ in samples]
+            found = {name for bit, name in self.REASONS.items() for _, _, r in samples if r & bit}
             return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                     "reasons": sorted(found), "samples": len(sm), "source": "nvml"}
         if self.proc is None:
@@ -140,7 +148,7 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for line in self.lines[self._mark:] or self.lines[-1:]:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) != 6:
                 continue
@@ -347,6 +355,8 @@ def run_gpu(args) -> dict | None:
         return ms
 
     # warm-up (also checks the planted supers come out)
+    clocks = ClockSampler(local)
+    clocks.start()
     first = None
     for _ in range(args.warmup):
         r = step()
@@ -355,8 +365,7 @@ def run_gpu(args) -> dict | None:
     found = {x.ip for x in first} if first else set()
     planted_found = len(set(supers.tolist()) & found) if rank == 0 else None
 
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     counts: list[int] = []
     ms = timed(lambda: step(counts, time_scan=True), args.steps)
     clk = clocks.stop()
@@ -527,6 +536,7 @@ def run_sliding(args) -> dict:
     def step(record=None):
         det.reset()
         pending = []
+        total = 0
         for s in range(n_sl):
             lo, hi = bounds[s], bounds[s + 1]
             if hi > lo:
@@ -535,23 +545,33 @@ def run_sliding(args) -> dict:
             # async form overlaps restore/filter of slide s with the scan of s+1
             pending.append(det.detect() if args.sync_detect else det.detect_async())
             det.advance_slice()
-        total = sum(len(r) for r in pending)  # all lists resolved before the step ends
+            # consume lists as a monitor would (the pipeline has already
+            # resolved those older than its depth): their device report
+            # buffers are released instead of 299 being held to the end
+            while len(pending) > det.pipeline_depth:
+                total += len(pending.pop(0))
+        total += sum(len(r) for r in pending)  # all lists resolved before the step ends
         if record is not None:
             record.append(total)
 
-    for _ in range(args.warmup):
-        step()
     clocks = ClockSampler(0)
     clocks.start()
+    for _ in range(args.warmup):
+        step()
+    clocks.mark()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    marks = []
     for _ in range(args.steps):
         step(counts)
+        marks.append(torch.cuda.Event(enable_timing=True))
+        marks[-1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    step_ms = [round(a.elapsed_time(b), 3) for a, b in zip([e0] + marks[:-1], marks)]
     # K2 alone over the same trace.  Deferred stamps (default): observe
     # every slice without advancing (the dirty bitmap absorbs it, no fold),
     # against the live-measured random L2 red.or rate -- the scan's bound;
@@ -631,6 +651,7 @@ def run_sliding(args) -> dict:
                      "kernel": "whole trace (K2 + per-slide fold/K4/K5/K6)",
                      "bytes_per_packet_model": round(bytes_pp, 2)},
         "scan_roofline": {**scan_roof, "scan_share_of_step": round(scan_ms / ms, 4)},
+        "step_ms": step_ms,
         "clocks": clk, "detect": {"reports_total": counts[0] if counts else None, "slides": n_sl,
                                   "planted": len(supers)},
         "gen_s": round(t_gen, 2),
@@ -706,13 +727,14 @@ def run_sharded(args) -> dict | None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     first: list = []
     for i in range(max(1, args.warmup)):
         step(first if i == 0 else None)
     found = {r.ip for r in first[0]} if rank == 0 else set()
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -791,10 +813,11 @@ def run_streaming(args) -> dict:
         if record is not None:
             record.append(total)
 
-    for _ in range(args.warmup):
-        step()
     clocks = ClockSampler(0)
     clocks.start()
+    for _ in range(args.warmup):
+        step()
+    clocks.mark()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
