@@ -33,5 +33,5 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan
 # full captures of the config-4 scan (deferred) and fold+view kernels
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_sliding_u16_fast --launch-skip 400 -c 1 -f \
   -o "$OUT/k2_deferred_full" python bench.py --config 4 --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1; echo "ncu_k2=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:ldca_fold --launch-skip 400 -c 1 -f \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:ldca_fold --launch-skip 150 -c 1 -f \
   -o "$OUT/fold_full" python bench.py --config 4 --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1; echo "ncu_fold=$?"
