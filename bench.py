@@ -528,6 +528,8 @@ def run_sliding(args) -> dict:
                               window_slices=300)
     if args.direct_stamps:
         det.defer_ldca_stamps = False
+    if args.no_ldca_ring:
+        det.ldca_ring_max_bytes = 0  # deferred single-bitmap mode (one fold + view per slide)
     if os.environ.get("SSPD_PIPELINE_DEPTH"):
         det.pipeline_depth = int(os.environ["SSPD_PIPELINE_DEPTH"])
     stream = torch.cuda.current_stream()
@@ -624,12 +626,19 @@ def run_sliding(args) -> dict:
     roof_gpps = rate.value / ops_pp / 1e9
     scan_roof.update({"roofline_gpps": round(roof_gpps, 3), "achieved_gpps": round(scan_gpps, 3),
                       "frac": round(scan_gpps / roof_gpps, 4), "scan_ms_per_trace": round(scan_ms, 3)})
-    # whole-trace HBM model: the input (8 B/pkt) plus, deferred, one fold per
-    # slide that reads and rewrites the LDCA stamp region (2 B/slot) and
-    # reads/clears the dirty bitmap + writes the view; direct, one 32-B sector
-    # read-modify-write per scattered stamp (8 + 8.031 x 32 B)
+    # whole-trace HBM model: the input (8 B/pkt) plus, per slide, deferred
+    # in ring mode the sliding-window OR of the bitmaps (read the slice's
+    # bitmap and the block OR, write the block OR and the view, clear the next
+    # slot: 5 x LDCA bytes; the stamps are folded lazily, when read), deferred
+    # single-bitmap one fold that reads and rewrites the LDCA stamp region
+    # (2 B/slot) + reads/clears the bitmap + writes the view; direct, one 32-B
+    # sector read-modify-write per scattered stamp (8 + 8.031 x 32 B)
     ldca_bytes = lcfg.lr * lcfg.lc * lcfg.k // 8
-    if deferred:
+    dfr = det._deferred()
+    ring = deferred and dfr is not None and dfr.ring is not None
+    if ring:
+        bytes_pp = 8 + 5 * ldca_bytes * n_sl / n
+    elif deferred:
         fold_bytes = 2 * (2 * lcfg.lr * lcfg.lc * lcfg.k) + 3 * ldca_bytes
         bytes_pp = 8 + fold_bytes * n_sl / n
     else:
@@ -644,11 +653,14 @@ def run_sliding(args) -> dict:
                    "detect": "synchronous detect()" if args.sync_detect else
                              "detect_async(): K5/K6 of slide s on a side stream, overlapping K2 of slide s+1",
                    "ldca_stamps": "direct u16 stores" if args.direct_stamps else
-                                  "deferred: dirty-bitmap red.or in the scan, one fold per slide fused with the LDCA view",
+                                  ("deferred, ring mode: per-slice dirty bitmaps (red.or in the scan) kept for the "
+                                   "window; LDCA view = two-stack sliding-window OR; stamps folded when read"
+                                   if ring else "deferred: dirty-bitmap red.or in the scan, one fold per slide "
+                                                "fused with the LDCA view"),
                    "pool_bytes": det.pool.memory_bytes(), "l2": "pool 403 MB exceeds L2; inputs 4 GiB"},
         "roofline": {"bound": "hbm", "achieved": round(value * 1e6 * bytes_pp / 1e9, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(value * 1e6 * bytes_pp / 1e9 / hbm, 4), "traffic": None,
-                     "kernel": "whole trace (K2 + per-slide fold/K4/K5/K6)",
+                     "kernel": "whole trace (K2 + per-slide LDCA view/K4/K5/K6)",
                      "bytes_per_packet_model": round(bytes_pp, 2)},
         "scan_roofline": {**scan_roof, "scan_share_of_step": round(scan_ms / ms, 4)},
         "step_ms": step_ms,
@@ -872,6 +884,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
     ap.add_argument("--sync-detect", action="store_true", help="config 4: synchronous detect() per slide")
+    ap.add_argument("--no-ldca-ring", action="store_true",
+                    help="config 4: deferred LDCA stamps without the ring of per-slice bitmaps (fold per slide)")
     ap.add_argument("--direct-stamps", action="store_true",
                     help="config 4: store LDCA stamps directly instead of the deferred dirty bitmap + fold")
     ap.add_argument("--sync-finalize", action="store_true",

@@ -184,6 +184,24 @@ SSPD_API int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oi
 SSPD_API int sspd_ldca_fold(void* pool, uint32_t ts_bytes, const sspd_params* p, uint32_t* ldca_dirty,
                             uint64_t now_wrapped, uint64_t window_slices, uint8_t* ldca_view, void* stream);
 
+/* Ring mode of the deferred LDCA stamps (SlidingDetector keeps the dirty
+ * bitmap of every slice of the window, slot = slice % ring_slots; a slot is
+ * active iff stamped in one of the last w slices, sliding.py:98-106, so the
+ * packed view of materialize_ldca (sliding.py:215-220) is an OR of bitmaps):
+ *   sspd_ldca_window_or = acc |= cur; view = acc | suffix; zero[:] = 0 (each
+ *       pointer may be NULL; 16-byte aligned, nbytes % 4 == 0);
+ *   sspd_ldca_fold_ring = TimestampPool.touch_batch of the LDCA slots for the
+ *       ring slices [slice_lo, slice_hi], newest slice winning (stamp =
+ *       slice & 0xFFFF); slice_hi - slice_lo < ring_slots;
+ *   sspd_ldca_suffix_or = in place, bitmap of slice e <- OR of slices
+ *       e .. first_slice + count - 1 (the two-stack suffix pass at a block end). */
+SSPD_API int sspd_ldca_window_or(const uint32_t* cur, uint32_t* acc, const uint32_t* suffix, uint32_t* view,
+                                 uint32_t* zero, uint64_t nbytes, void* stream);
+SSPD_API int sspd_ldca_fold_ring(void* pool, uint32_t ts_bytes, const sspd_params* p, const uint32_t* ring,
+                                 uint32_t ring_slots, uint64_t slice_lo, uint64_t slice_hi, void* stream);
+SSPD_API int sspd_ldca_suffix_or(uint32_t* ring, uint32_t ring_slots, uint64_t nbytes, uint64_t first_slice,
+                                 uint64_t count, void* stream);
+
 /* ---- K3 sweep: TimestampPool._sweep (sliding.py:88-94) ---------------- */
 SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
                uint64_t now_wrapped, uint64_t window_slices,

@@ -379,6 +379,175 @@ extern "C" int sspd_ldca_fold(void* pool, uint32_t ts_bytes, const sspd_params* 
   return check_launch();
 }
 
+// ---- ring mode of the deferred LDCA stamps (SlidingDetector._DeferredLdca)
+//
+// The dirty bitmap of every slice of the window is kept (ring of R = w+1
+// LDCA-shaped bitmaps, slot = slice % R).  A slot is active at `now` iff it
+// was stamped in one of the slices now-w+1 .. now (sliding.py:98-106: the
+// anti-alias sweep keeps wrapped ages exact), so the active-bit LDCA view is
+// the OR of those w bitmaps.  It is kept with the two-stack sliding-window
+// OR: `acc` = OR of the current block's bitmaps (blocks of w slices), and at
+// each block end the block's bitmaps are turned in place into suffix ORs
+// (sspd_ldca_suffix_or), so view(now) = suffix[now-w+1] | acc | dirty[now]:
+// three bitmap reads and two writes per detect instead of every LDCA stamp.
+// Stamps are written lazily (sspd_ldca_fold_ring) when the pool is read and
+// at block ends, before the suffix pass overwrites the raw bitmaps.
+
+// acc |= cur; view = acc | suffix (when view); zero = 0 (when zero).  Any of
+// cur / suffix / view / zero may be NULL.  Word granularity n32, vectorised.
+__global__ void __launch_bounds__(256) ldca_window_or_kernel(const uint32_t* __restrict__ cur,
+                                                             uint32_t* __restrict__ acc,
+                                                             const uint32_t* __restrict__ suffix,
+                                                             uint32_t* __restrict__ view, uint32_t* __restrict__ zero,
+                                                             uint64_t n32) {
+  const uint64_t n128 = n32 >> 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t i = t0; i < n128; i += stride) {
+    uint4 a = reinterpret_cast<const uint4*>(acc)[i];
+    if (cur) {
+      const uint4 c = __ldcg(reinterpret_cast<const uint4*>(cur) + i);
+      a.x |= c.x, a.y |= c.y, a.z |= c.z, a.w |= c.w;
+      reinterpret_cast<uint4*>(acc)[i] = a;
+    }
+    if (view) {
+      if (suffix) {
+        const uint4 s = __ldcg(reinterpret_cast<const uint4*>(suffix) + i);
+        a.x |= s.x, a.y |= s.y, a.z |= s.z, a.w |= s.w;
+      }
+      reinterpret_cast<uint4*>(view)[i] = a;
+    }
+    if (zero) reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (uint64_t i = (n128 << 2) + t0; i < n32; i += stride) {  // tail words
+    uint32_t a = acc[i];
+    if (cur) acc[i] = a = a | cur[i];
+    if (view) view[i] = suffix ? (a | suffix[i]) : a;
+    if (zero) zero[i] = 0;
+  }
+}
+
+// Stamps of the ring slices [lo, hi] into the LDCA slots, the newest slice
+// of each slot winning (slice e writes stamp e & 0xFFFF, as the direct scan
+// would have at slice e).  One thread per 32 slots; the walk stops once all
+// 32 have been seen.
+__global__ void __launch_bounds__(256) ldca_fold_ring_kernel(uint16_t* __restrict__ pool, uint64_t base,
+                                                             uint64_t nwords, const uint32_t* __restrict__ ring,
+                                                             uint32_t ring_slots, uint64_t lo, uint64_t hi) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t slot_hi = (uint32_t)(hi % ring_slots);
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) {
+    uint4* src = reinterpret_cast<uint4*>(pool + base) + q * 4;
+    uint4 v[4];
+    uint32_t seen = 0;
+    bool loaded = false;
+    uint32_t slot = slot_hi;
+    for (uint64_t e = hi + 1; e-- > lo && seen != 0xFFFFFFFFu;) {
+      const uint32_t d = __ldcg(ring + (uint64_t)slot * nwords + q);
+      slot = slot == 0 ? ring_slots - 1 : slot - 1;
+      const uint32_t m = d & ~seen;
+      if (!m) continue;
+      if (!loaded) {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) v[j] = __ldcg(src + j);
+        loaded = true;
+      }
+      const uint32_t s16 = (uint32_t)(e & 0xFFFFu);
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) {
+        const uint32_t mj = (m >> (8 * j)) & 0xFFu;
+        if (mj) {
+          v[j].x = stamp_pairs(v[j].x, mj, s16);
+          v[j].y = stamp_pairs(v[j].y, mj >> 2, s16);
+          v[j].z = stamp_pairs(v[j].z, mj >> 4, s16);
+          v[j].w = stamp_pairs(v[j].w, mj >> 6, s16);
+        }
+      }
+      seen |= m;
+    }
+    if (loaded) {
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j)
+        if ((seen >> (8 * j)) & 0xFFu) src[j] = v[j];
+    }
+  }
+}
+
+// In place: bitmap of slice e <- OR of slices e .. first+count-1 (suffix ORs
+// of one block), walking the block from its last slice down.
+template <typename V>
+__global__ void __launch_bounds__(256) ldca_suffix_or_kernel(V* __restrict__ ring, uint32_t ring_slots, uint64_t nvec,
+                                                             uint64_t first, uint64_t count) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t slot_last = (uint32_t)((first + count - 1) % ring_slots);
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nvec; q += stride) {
+    V acc{};
+    uint32_t slot = slot_last;
+    for (uint64_t c = 0; c < count; ++c) {
+      V* p = ring + (uint64_t)slot * nvec + q;
+      const V x = __ldcg(p);
+      if constexpr (sizeof(V) == 16) {
+        acc.x |= x.x, acc.y |= x.y, acc.z |= x.z, acc.w |= x.w;
+      } else {
+        acc |= x;
+      }
+      if (c) *p = acc;  // the block's last bitmap is its own suffix
+      slot = slot == 0 ? ring_slots - 1 : slot - 1;
+    }
+  }
+}
+
+extern "C" int sspd_ldca_window_or(const uint32_t* cur, uint32_t* acc, const uint32_t* suffix, uint32_t* view,
+                                   uint32_t* zero, uint64_t nbytes, void* stream) {
+  if (nbytes == 0) return SSPD_OK;
+  if (!acc || (nbytes & 3u)) return SSPD_ERR_DATA;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(cur) | reinterpret_cast<uintptr_t>(acc) |
+                       reinterpret_cast<uintptr_t>(suffix) | reinterpret_cast<uintptr_t>(view) |
+                       reinterpret_cast<uintptr_t>(zero);
+  if (al & 15u) return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t n32 = nbytes >> 2;
+  const int grid = grid_for(ldca_window_or_kernel, 256, (n32 + 3) >> 2);
+  ldca_window_or_kernel<<<grid, 256, 0, st>>>(cur, acc, suffix, view, zero, n32);
+  return check_launch();
+}
+
+extern "C" int sspd_ldca_fold_ring(void* pool, uint32_t ts_bytes, const sspd_params* p, const uint32_t* ring,
+                                   uint32_t ring_slots, uint64_t slice_lo, uint64_t slice_hi, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!pool || !ring || ring_slots == 0) return SSPD_ERR_DATA;
+  if (ts_bytes != 2 || (p->ldca_bytes & 3u) || (p->slot_ldca_base & 7u) || (reinterpret_cast<uintptr_t>(pool) & 15u) ||
+      (reinterpret_cast<uintptr_t>(ring) & 3u))
+    return SSPD_ERR_CONFIG;
+  if (slice_hi < slice_lo) return SSPD_OK;
+  if (slice_hi - slice_lo >= ring_slots) return SSPD_ERR_DATA;  // the ring holds R slices at most
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nwords = p->ldca_bytes >> 2;
+  const int grid = grid_for(ldca_fold_ring_kernel, 256, nwords);
+  ldca_fold_ring_kernel<<<grid, 256, 0, st>>>((uint16_t*)pool, p->slot_ldca_base, nwords, ring, ring_slots, slice_lo,
+                                              slice_hi);
+  return check_launch();
+}
+
+extern "C" int sspd_ldca_suffix_or(uint32_t* ring, uint32_t ring_slots, uint64_t nbytes, uint64_t first_slice,
+                                   uint64_t count, void* stream) {
+  if (count == 0 || nbytes == 0) return SSPD_OK;
+  if (!ring || (nbytes & 3u) || count > ring_slots) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((nbytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ring) & 15u) == 0) {
+    const uint64_t nvec = nbytes >> 4;
+    const int grid = grid_for(ldca_suffix_or_kernel<uint4>, 256, nvec);
+    ldca_suffix_or_kernel<uint4><<<grid, 256, 0, st>>>(reinterpret_cast<uint4*>(ring), ring_slots, nvec, first_slice,
+                                                       count);
+  } else {
+    const uint64_t nvec = nbytes >> 2;
+    const int grid = grid_for(ldca_suffix_or_kernel<uint32_t>, 256, nvec);
+    ldca_suffix_or_kernel<uint32_t><<<grid, 256, 0, st>>>(ring, ring_slots, nvec, first_slice, count);
+  }
+  return check_launch();
+}
+
 static bool seav_fast_layout(const void* pool, const sspd_params* p, const void* out) {
   bool ok = p->g == 8 && p->reg_bytes == 1 && (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
             (reinterpret_cast<uintptr_t>(out) & 3u) == 0;

@@ -84,26 +84,20 @@ class TimestampPool:
         return self._buf
 
     def flush(self, ldca_view=None):
-        """Apply the LDCA stamps a deferred scan recorded in its dirty bitmap
-        (sspd_ldca_fold); with `ldca_view` (a device byte buffer) also write
-        the packed active-bit LDCA in the same pass.  Returns True when the
-        view was written."""
+        """Apply the LDCA stamps a deferred scan recorded (sspd_ldca_fold /
+        sspd_ldca_fold_ring); in single-bitmap mode with `ldca_view` (a device
+        byte buffer) also write the packed active-bit LDCA in the same pass.
+        Returns True when the view was written."""
         d = self._deferred
-        if d is None or not d.pending:
+        if d is None:
             return False
-        from ._device import call, stream_ptr
-
-        call("sspd_ldca_fold", self._buf.data_ptr(), self.ts_bytes, d.params, d.dirty.data_ptr(),
-             self._wrapped_now(), self.window_slices, None if ldca_view is None else ldca_view.data_ptr(),
-             stream_ptr())
-        d.pending = False
-        return ldca_view is not None
+        return d.flush(self, ldca_view)
 
     def _drop_deferred(self):
+        """Pending deferred stamps are superseded (every stamp is replaced)."""
         d = self._deferred
-        if d is not None and d.pending:
-            d.dirty.zero_()
-            d.pending = False
+        if d is not None:
+            d.drop()
 
     def reset(self):
         """Back to the constructor state (slice 0, every slot just expired)."""
@@ -114,6 +108,8 @@ class TimestampPool:
         self._version += 1
         self._pristine = True
         self._buf.fill_(_as_signed((-self.window_slices) & self._mask, self.ts_bytes))
+        if self._deferred is not None:
+            self._deferred.restart(self, pristine=True)
 
     @property
     def ts(self) -> np.ndarray:
@@ -165,6 +161,9 @@ class TimestampPool:
 
     def advance_slice(self):
         self.flush()  # deferred stamps belong to the slice that ends here
+        self._advance()
+
+    def _advance(self):
         self.now += 1
         self._since_sweep += 1
         if self._since_sweep >= self._sweep_period:
@@ -173,6 +172,7 @@ class TimestampPool:
     def _sweep(self):
         from ._device import call, stream_ptr
 
+        self.flush()
         clamp = (self.now - self.window_slices) & self._mask
         call("sspd_sweep", self._buf.data_ptr(), self.n_slots, self.ts_bytes, self._wrapped_now(),
              self.window_slices, clamp, stream_ptr())
@@ -213,14 +213,163 @@ def advance_slice(pool: TimestampPool) -> TimestampPool:
 
 
 class _DeferredLdca:
-    """Dirty bitmap of LDCA stamps not yet written (sspd_scan_sliding_deferred)."""
+    """LDCA stamps recorded as dirty bitmaps instead of stored
+    (sspd_scan_sliding_deferred): within one slice every LDCA store of the
+    reference's touch_batch (sliding.py:77-79) writes the same `now`, so the
+    scan only marks the touched slots (one red.or into an L2-resident
+    LDCA-shaped bitmap) and the stamps are written later, exactly.
 
-    def __init__(self, params, nbytes: int):
+    Single-bitmap mode: `dirty` holds the current slice; sspd_ldca_fold
+    writes it once per slice (fused with the LDCA view at detect) and clears it.
+
+    Ring mode (when w+1 bitmaps fit `SlidingDetector.ldca_ring_max_bytes`):
+    the bitmap of every slice of the window is kept, slot = slice % (w+1).  A
+    slot is active iff it was stamped in one of the last w slices, so the
+    packed LDCA view is the OR of w bitmaps, maintained as a two-stack
+    sliding-window OR: `acc` = OR of the current block's bitmaps (blocks of w
+    slices starting at `blk0`); at a block end the block's bitmaps are turned
+    in place into suffix ORs, so view(now) = suffix[now-w+1] | acc | dirty[now]
+    (sspd_ldca_window_or: a few bitmap passes per detect instead of reading
+    and rewriting every LDCA stamp).  Stamps are folded lazily
+    (sspd_ldca_fold_ring: slices [fold_lo, cur], newest wins) whenever the
+    pool is read, before a sweep, and at block ends before the suffix pass
+    overwrites the raw bitmaps.  The view is exact from a pristine pool
+    (nothing active before blk0) or once a full block has been recorded since
+    the last stamp write that bypassed the detector (`prev_ok`); in between,
+    detect folds and materializes the view from the stamps."""
+
+    def __init__(self, params, nbytes: int, window_slices: int = 0, ring: bool = False):
         from ._device import zeros_bytes
 
         self.params = params
-        self.dirty = zeros_bytes(nbytes)
+        self.nbytes = nbytes
+        self.w = window_slices
+        self.ring = None
+        self.pending = False  # scanned since the last fold
+        if ring:
+            import torch
+
+            from ._device import device
+
+            self.slots = window_slices + 1
+            self.stride = -(-nbytes // 16) * 16
+            self.ring = torch.zeros(self.slots * self.stride, dtype=torch.uint8, device=device())
+            self.acc = zeros_bytes(nbytes)
+            self.cur = self.blk0 = self.fold_lo = 0
+            self.cur_merged = True
+            self.prev_ok = False
+            self.pristine = True
+            self.version = None
+        else:
+            self.dirty = zeros_bytes(nbytes)
+
+    # -- common ---------------------------------------------------------------
+    def dirty_ptr(self) -> int:
+        return self.slot_ptr(self.cur) if self.ring is not None else self.dirty.data_ptr()
+
+    def mark_scanned(self):
+        self.pending = True
+        if self.ring is not None:
+            self.cur_merged = False
+
+    def flush(self, pool, ldca_view=None) -> bool:
+        if not self.pending:
+            return False
+        from ._device import call, stream_ptr
+
+        if self.ring is not None:
+            call("sspd_ldca_fold_ring", pool._buf.data_ptr(), pool.ts_bytes, self.params, self.ring.data_ptr(),
+                 self.slots, self.fold_lo, self.cur, stream_ptr())
+            self.fold_lo = self.cur  # the current slice may gather more bits: folded again next time
+            self.pending = False
+            return False
+        call("sspd_ldca_fold", pool._buf.data_ptr(), pool.ts_bytes, self.params, self.dirty.data_ptr(),
+             pool._wrapped_now(), pool.window_slices, None if ldca_view is None else ldca_view.data_ptr(),
+             stream_ptr())
         self.pending = False
+        return ldca_view is not None
+
+    def drop(self):
+        """Forget the pending stamps (the pool's stamps are all replaced)."""
+        if self.ring is not None:
+            self._zero_slot(self.cur)
+            self.fold_lo = self.cur
+        elif self.pending:
+            self.dirty.zero_()
+        self.pending = False
+
+    # -- ring mode ------------------------------------------------------------
+    @property
+    def current(self):
+        """The current slice's bitmap (a device view)."""
+        if self.ring is None:
+            return self.dirty
+        off = (self.cur % self.slots) * self.stride
+        return self.ring[off: off + self.nbytes]
+
+    def slot_ptr(self, e: int) -> int:
+        return self.ring.data_ptr() + (e % self.slots) * self.stride
+
+    def _zero_slot(self, e: int):
+        off = (e % self.slots) * self.stride
+        self.ring[off: off + self.stride].zero_()
+
+    def restart(self, pool, pristine: bool):
+        """Start a new block at the pool's slice.  The caller has folded every
+        pending stamp (or dropped it); the view is exact from here only if
+        `pristine` (no stamp active) -- else after one full block."""
+        if self.ring is None:
+            self.drop()
+            return
+        self.cur = self.blk0 = self.fold_lo = pool.now
+        self._zero_slot(self.cur)
+        self.acc.zero_()
+        self.cur_merged = True
+        self.prev_ok = False
+        self.pristine = pristine
+        self.pending = False
+        self.version = pool._version
+
+    def sync(self, pool):
+        """Stamps written around the detector (touch*, .ts, the pool's own
+        advance_slice) restart the block structure (those paths flushed first)."""
+        if pool._version != self.version or pool.now != self.cur:
+            self.restart(pool, pristine=False)
+
+    def valid(self) -> bool:
+        return self.pristine or self.prev_ok
+
+    def view_into(self, lview):
+        """view = suffix[now-w+1] | (acc |= dirty[now])."""
+        from ._device import call, stream_ptr
+
+        first = self.cur - self.w + 1
+        suffix = self.slot_ptr(first) if self.prev_ok and first <= self.blk0 - 1 else None
+        call("sspd_ldca_window_or", self.slot_ptr(self.cur), self.acc.data_ptr(), suffix, lview.data_ptr(), None,
+             self.nbytes, stream_ptr())
+        self.cur_merged = True
+
+    def advance(self, pool):
+        """End of slice `cur` (before the pool's slice advances)."""
+        from ._device import call, stream_ptr
+
+        if self.cur == self.blk0 + self.w - 1:  # block end: fold, then suffix ORs in place
+            self.flush(pool)
+            call("sspd_ldca_suffix_or", self.ring.data_ptr(), self.slots, self.stride, self.blk0, self.w, stream_ptr())
+            self.prev_ok = True
+            self.pristine = False
+            self.blk0 = self.cur + 1
+            self.acc.zero_()
+            self._zero_slot(self.cur + 1)
+        elif not self.cur_merged:  # acc |= dirty[cur], and clear the next slice's slot
+            call("sspd_ldca_window_or", self.slot_ptr(self.cur), self.acc.data_ptr(), None, None,
+                 self.slot_ptr(self.cur + 1), self.nbytes, stream_ptr())
+        else:
+            self._zero_slot(self.cur + 1)
+        if not self.pending:
+            self.fold_lo = self.cur + 1
+        self.cur += 1
+        self.cur_merged = True
 
 
 @dataclass(frozen=True)
@@ -242,6 +391,10 @@ class SlidingDetector:
     # record LDCA stamps in a dirty bitmap and write them once per slice
     # (sspd_ldca_fold, fused with the LDCA view at detect)
     defer_ldca_stamps = True
+    # ring mode of the deferred stamps: keep the bitmaps of the whole window
+    # ((w+1) x LDCA bytes; 2.5 GB at config 4) and build the LDCA view as a
+    # sliding-window OR instead of from the stamps
+    ldca_ring_max_bytes = 8 << 30
 
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
@@ -265,16 +418,22 @@ class SlidingDetector:
 
     def advance_slice(self):
         iv = self._iv()
+        pool = self.pool
         if iv is not None:
             from ._device import call, stream_ptr
 
             self._iv_check(iv)
-            pool = self.pool
-            call("sspd_seav_advance", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+            # reads SEAV stamps only (never deferred): no LDCA fold needed
+            call("sspd_seav_advance", pool._buf.data_ptr(), pool.ts_bytes, self._params,
                  iv["view"].device_buffer().data_ptr(), iv["log"].data_ptr(), iv["log"].numel(),
                  iv["meta"].data_ptr(), iv["nseg"], pool.now, pool.window_slices, stream_ptr())
             iv["now"] = pool.now + 1
-        self.pool.advance_slice()
+        ring = self._ring()
+        if ring is not None:  # bitmaps stay in the ring: no per-slice fold
+            ring.advance(pool)
+            pool._advance()
+        else:
+            pool.advance_slice()
 
     def reset(self):
         self.pool.reset()
@@ -331,13 +490,30 @@ class SlidingDetector:
         d = pool._deferred
         if d is None and self.defer_ldca_stamps and pool.ts_bytes == 2 and (p.slot_ldca_base & 7) == 0 \
                 and p.ldca_bytes % 4 == 0 and p.slot_total < (1 << 32):
-            d = pool._deferred = _DeferredLdca(p, p.ldca_bytes)
+            ring = (pool.window_slices + 1) * (-(-p.ldca_bytes // 16) * 16) <= self.ldca_ring_max_bytes
+            d = pool._deferred = _DeferredLdca(p, p.ldca_bytes, pool.window_slices, ring=ring)
+            # nothing is active in a pool no stamp was ever written to
+            d.restart(pool, pristine=pool._pristine and self.pair_count == 0)
         return d if self.defer_ldca_stamps else None
 
+    def _ring(self):
+        """The deferred-LDCA state when it runs in ring mode (synchronised
+        with the pool), else None."""
+        d = self._deferred()
+        if d is None or d.ring is None:
+            return None
+        d.sync(self.pool)
+        return d
+
     def _ldca_view_into(self, lview):
-        """Packed active-bit LDCA into `lview`: fused with the fold of the
-        deferred stamps when some are pending, else K4 over the stamps."""
+        """Packed active-bit LDCA into `lview`: the sliding-window OR of the
+        ring bitmaps, or fused with the fold of the deferred stamps when
+        some are pending, else K4 over the stamps."""
         pool = self.pool
+        ring = self._ring()
+        if ring is not None and ring.valid():
+            ring.view_into(lview)
+            return
         if pool.flush(ldca_view=lview):
             return
         from ._device import call, stream_ptr
@@ -361,7 +537,7 @@ class SlidingDetector:
 
         self._iv_check(iv)
         pool = self.pool
-        call("sspd_materialize_seav_if", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+        call("sspd_materialize_seav_if", pool._buf.data_ptr(), pool.ts_bytes, self._params,
              pool._wrapped_now(), pool.window_slices, iv["view"].device_buffer().data_ptr(),
              iv["meta"][1:].data_ptr(), stream_ptr())
         return iv["view"]
@@ -381,6 +557,8 @@ class SlidingDetector:
         cap = self.pipelined_scan_blocks_per_sm if getattr(self, "_async", None) else 0
         iv = self._iv()
         dfr = self._deferred()
+        if dfr is not None and dfr.ring is not None:
+            dfr.sync(pool)
         if iv is not None or dfr is not None:
             if iv is not None:
                 self._iv_check(iv)
@@ -391,9 +569,9 @@ class SlidingDetector:
                  None if iv is None else iv["view"].device_buffer().data_ptr(),
                  None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
                  None if iv is None else iv["meta"].data_ptr(),
-                 None if dfr is None else dfr.dirty.data_ptr(), stream_ptr())
+                 None if dfr is None else dfr.dirty_ptr(), stream_ptr())
             if dfr is not None:
-                dfr.pending = True
+                dfr.mark_scanned()
         else:
             call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
                  pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
@@ -406,7 +584,7 @@ class SlidingDetector:
         from ._device import call, stream_ptr
 
         pool = self.pool
-        call("sspd_materialize_seav", pool.device_buffer().data_ptr(), pool.ts_bytes, self._params,
+        call("sspd_materialize_seav", pool._buf.data_ptr(), pool.ts_bytes, self._params,
              pool._wrapped_now(), pool.window_slices, sketch.device_buffer().data_ptr(), stream_ptr())
 
     def materialize_seav(self) -> SeavSketch:

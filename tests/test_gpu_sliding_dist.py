@@ -459,4 +459,60 @@ def test_deferred_ldca_stamps_equal_direct_stamps(cuda):
     a.reset()
     b.reset()
     assert np.array_equal(a.pool.ts, b.pool.ts)
-    assert not a.pool._deferred.pending and int(a.pool._deferred.dirty.count_nonzero()) == 0
+    assert not a.pool._deferred.pending and int(a.pool._deferred.current.count_nonzero()) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("async_detect", [False, True])
+def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect):
+    """Ring mode of the deferred LDCA stamps (the LDCA view as a two-stack
+    sliding-window OR of per-slice bitmaps, stamps folded lazily) against
+    direct u16 stores over 2.7 windows from a pristine pool: detect at every
+    slide across two block ends (suffix passes) with expiring slots, pool
+    reads mid-block, a write around the detector (restart: stamps-based view
+    for one block, then the ring again), and reset."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5)
+    w = 129
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=w)
+        b = SlidingDetector(params, window_slices=w)
+    b.defer_ldca_stamps = False
+    assert a._deferred().ring is not None and a._deferred().valid()
+    rng = np.random.default_rng(7)
+    heavy = rng.integers(0, 2**32, size=3, dtype=np.uint64)
+    base = a.layout.ldca_base
+    pend = []
+    modes = []
+    for s in range(350):
+        n = int(rng.integers(0, 3000)) if s % 11 else 0  # some empty slices
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        if s < 40 or 150 <= s < 175:  # bursts that expire inside the run
+            hips[: n // 2] = heavy[s % 3]
+        a.observe_batch(hips, oips)
+        b.observe_batch(hips, oips)
+        if s == 200:  # a write around the detector: restart, stamps-based view for one block
+            for det in (a, b):
+                det.pool.touch_batch(np.arange(base, base + 2048, 5))
+        if s % 37 == 5:
+            assert np.array_equal(a.pool.ts, b.pool.ts), s
+            assert np.array_equal(a.materialize_ldca(), b.materialize_ldca()), s
+        modes.append(a._ring().valid())
+        if async_detect:
+            pend.append((s, a.detect_async(), b.detect_async()))
+        else:
+            assert rep_list(a.detect()) == rep_list(b.detect()), s
+        a.advance_slice()
+        b.advance_slice()
+    for s, x, y in pend:
+        assert rep_list(x) == rep_list(y), s
+    assert np.array_equal(a.pool.ts, b.pool.ts)
+    d = a._ring()
+    assert d.prev_ok and d.blk0 == 200 + w  # block ends after 128, 257 (pristine), 328 (restart at 200)
+    assert all(modes[:200]) and not any(modes[200:200 + w]) and all(modes[200 + w:])
+    a.reset()
+    b.reset()
+    assert a._ring().valid() and np.array_equal(a.pool.ts, b.pool.ts)
