@@ -281,12 +281,16 @@ SSPD_API int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0,
  * compaction into out_ip/out_z0 (capacity entries each).  counts (device,
  * 2 x u64): [0] candidates found -- if it exceeds `capacity` the outputs
  * are incomplete and the caller re-runs with a larger capacity -- and [1]
- * reports kept.  overflow (device, 2^r bytes): 1 for every register array
- * dropped by the cap.  scratch NULL queries *scratch_bytes. */
+ * reports kept.  overflow (device, 2^r + 1 bytes): 1 for every register
+ * array dropped by the cap; byte [2^r] = 1 when the bucket sort met a
+ * bucket it cannot order (skewed addresses): the outputs are then invalid
+ * and the caller re-runs with flags bit 0 (radix sort).  scratch NULL
+ * queries *scratch_bytes. */
 SSPD_API int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p,
                            uint64_t restore_cap, const uint8_t* keep_table, uint64_t capacity,
                            uint32_t* out_ip, uint32_t* out_z0, unsigned long long* counts,
-                           uint8_t* overflow, void* scratch, size_t* scratch_bytes, void* stream);
+                           uint8_t* overflow, void* scratch, size_t* scratch_bytes, uint32_t flags,
+                           void* stream);
 
 /* ---- K7 merge ----------------------------------------------------------
  * Bytewise OR of n_src equal-length buffers into dst (dst may alias

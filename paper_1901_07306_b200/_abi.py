@@ -136,7 +136,7 @@ _SIGS = {
     "sspd_unpack_records": (C.c_int, [_VP, _U64, _VP, _VP, _VP, _VP]),
     "sspd_crc32": (C.c_int, [_VP, _U64, _VP, _VP, C.POINTER(_U64), _VP]),
     "sspd_finalize": (C.c_int, [_VP, _VP, _PP, _U64, _VP, _U64, _VP, _VP, _VP, _VP, _VP, C.POINTER(C.c_size_t),
-                                _VP]),
+                                _U32, _VP]),
     "sspd_exact_cardinalities": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _VP, _VP, C.POINTER(C.c_size_t), _VP]),
 }
 

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <cooperative_groups/details/partitioning.h>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
@@ -45,8 +46,9 @@ struct RestorePlan {
   uint32_t keymask[SSPD_MAX_SR];  // column bits that sit on fixed_i
   uint32_t nk[SSPD_MAX_SR];       // popcount(keymask)
   uint32_t off_regs[SSPD_MAX_SR], off_cols[SSPD_MAX_SR], off_bstart[SSPD_MAX_SR];
-  uint32_t off_pref0, off_misc, smem_bytes, pad_;
+  uint32_t off_pref0, off_misc, smem_bytes, hshift;
   uint64_t seav_row_off[SSPD_MAX_SR];
+  uint32_t* hist;  // optional: per-bucket candidate counts (bucket = ip >> hshift) for the bucket sort
 };
 
 __device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
@@ -146,8 +148,10 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
           if (keep.thread_rank() == 0) base = atomicAdd(out_count, (unsigned long long)keep.size());
           const unsigned long long slot = keep.shfl(base, 0) + keep.thread_rank();
           if (slot < out_capacity) {
-            out_ip[slot] = (uint32_t)((lp << P.r) | rp);
+            const uint32_t ip = (uint32_t)((lp << P.r) | rp);
+            out_ip[slot] = ip;
             out_aux[slot] = (rp << 8) | wgt;
+            if (P.hist) atomicAdd(P.hist + (ip >> P.hshift), 1u);
           }
         }
       } else {
@@ -632,16 +636,120 @@ static int build_plan(const sspd_params& p, RestorePlan& P) {
     off = align(off + 2u * p.sc[i], 16);
   }
   P.smem_bytes = off;
+  P.hist = nullptr;
+  P.hshift = 0;
   return SSPD_OK;
+}
+
+// ---- bucket sort of the candidates (sspd_finalize) -----------------------
+// The candidates are unique IPv4 keys, uniformly spread for random traffic.
+// The restore counts them per bucket (bucket = ip >> hshift, nb buckets,
+// ~16 keys per bucket at full capacity); one pass turns the counts into
+// bucket starts and scatters the keys into their buckets, and one warp per
+// bucket then orders its <= 64 keys in registers (rank = number of smaller
+// keys).  Two launches instead of a radix sort's six.  A bucket with more
+// than kBucketMax keys (skewed addresses) raises *too_big: the caller
+// re-runs the finalize with the radix sort (exact either way).
+constexpr uint32_t kBucketMax = 64;
+
+__global__ void __launch_bounds__(1024) bucket_scatter_kernel(const uint32_t* __restrict__ ip,
+                                                              const unsigned long long* __restrict__ found,
+                                                              uint64_t cap, const uint32_t* __restrict__ hist,
+                                                              uint32_t nb, uint32_t hshift, uint32_t* cursor,
+                                                              uint32_t* start_out, uint32_t* __restrict__ bucketed) {
+  extern __shared__ uint32_t pre[];  // [nb] bucket starts
+  __shared__ uint32_t wsum[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (nb + 1023) / 1024;  // contiguous counts per thread
+  uint32_t tsum = 0;
+  for (uint32_t e = 0; e < per; ++e) {
+    const uint32_t i = tid * per + e;
+    if (i < nb) tsum += hist[i];
+  }
+  uint32_t x = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= (uint32_t)o) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  uint32_t run = x - tsum + (warp ? wsum[warp - 1] : 0u);
+  for (uint32_t e = 0; e < per; ++e) {
+    const uint32_t i = tid * per + e;
+    if (i < nb) {
+      pre[i] = run;
+      run += hist[i];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (uint32_t i = tid; i < nb; i += blockDim.x) start_out[i] = pre[i];
+    if (tid == 0) start_out[nb] = wsum[31];
+  }
+  const uint64_t n = min((uint64_t)*found, cap);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + tid; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ip[i];
+    const uint32_t b = k >> hshift;
+    bucketed[pre[b] + atomicAdd(cursor + b, 1u)] = k;
+  }
+}
+
+__global__ void __launch_bounds__(256) bucket_sort_kernel(const uint32_t* __restrict__ bucketed,
+                                                          const uint32_t* __restrict__ start, uint32_t nb,
+                                                          uint32_t* __restrict__ out, uint8_t* too_big) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += nwarps) {
+    const uint32_t lo = start[b], n = start[b + 1] - lo;
+    if (n == 0) continue;
+    if (n > kBucketMax) {
+      if (lane == 0) *too_big = 1;
+      continue;
+    }
+    const uint32_t k0 = lane < n ? bucketed[lo + lane] : 0xFFFFFFFFu;
+    const uint32_t k1 = lane + 32 < n ? bucketed[lo + 32 + lane] : 0xFFFFFFFFu;
+    uint32_t r0 = 0, r1 = 0;
+    for (uint32_t j = 0; j < n; ++j) {  // n is warp-uniform
+      const uint32_t kj = __shfl_sync(0xFFFFFFFFu, j < 32 ? k0 : k1, j & 31);
+      r0 += (kj < k0) | ((kj == k0) & (j < lane));
+      r1 += (kj < k1) | ((kj == k1) & (j < lane + 32));
+    }
+    if (lane < n) out[lo + r0] = k0;
+    if (lane + 32 < n) out[lo + r1] = k1;
+  }
 }
 
 }  // namespace sspd
 
 using namespace sspd;
 
+static int restore_launch(const uint8_t* seav, const sspd_params* p, uint32_t rp_begin, uint32_t rp_count,
+                          uint64_t cap, uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
+                          unsigned long long* out_count, uint8_t* overflow, uint32_t* hist, uint32_t hshift,
+                          void* stream);
+
 extern "C" int sspd_restore(const uint8_t* seav, const sspd_params* p, uint32_t rp_begin, uint32_t rp_count,
                             uint64_t cap, uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
                             unsigned long long* out_count, uint8_t* overflow, void* stream) {
+  return restore_launch(seav, p, rp_begin, rp_count, cap, out_ip, out_aux, out_capacity, out_count, overflow,
+                        nullptr, 0, stream);
+}
+
+static int restore_launch(const uint8_t* seav, const sspd_params* p, uint32_t rp_begin, uint32_t rp_count,
+                          uint64_t cap, uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
+                          unsigned long long* out_count, uint8_t* overflow, uint32_t* hist, uint32_t hshift,
+                          void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
   if ((uint64_t)rp_begin + rp_count > (1ull << p->r)) return SSPD_ERR_CONFIG;
@@ -649,6 +757,8 @@ extern "C" int sspd_restore(const uint8_t* seav, const sspd_params* p, uint32_t 
   if (rp_count == 0) return SSPD_OK;
   RestorePlan P;
   build_plan(*p, P);
+  P.hist = hist;
+  P.hshift = hshift;
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -768,22 +878,32 @@ extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, cons
 
 // One finalize without host round trips (restore -> sort -> filter ->
 // compaction), every count kept on the device.  The candidate buffers have a
-// fixed capacity C: the key buffer is pre-filled with 0xFFFFFFFF so the
-// radix sort of all C slots leaves the live candidates first (stable on
-// equal keys), the filter marks slots past the live count as not kept, and
-// the compaction runs over C.  counts[0] = candidates found (may exceed C:
-// the outputs are then incomplete and the caller retries with a larger C),
-// counts[1] = reports kept.
+// fixed capacity C; slots past the live count (counts[0], on the device) are
+// never reported: the filter marks them not kept and the compaction runs over
+// C.  Sort: bucket sort (above) for C <= kBucketSortMaxCap unless `flags` bit
+// 0 asks for the radix sort, which sorts all C slots of a key buffer
+// pre-filled with 0xFFFFFFFF (the live candidates come first).  counts[0] =
+// candidates found (may exceed C: the outputs are then incomplete and the
+// caller retries with a larger C), counts[1] = reports kept; overflow[2^r] = 1
+// when a bucket was too large for the bucket sort (the caller re-runs with
+// the radix sort).
+constexpr uint64_t kBucketSortMaxCap = 1ull << 18;
+
 extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p, uint64_t restore_cap,
                              const uint8_t* keep_table, uint64_t capacity, uint32_t* out_ip, uint32_t* out_z0,
                              unsigned long long* counts, uint8_t* overflow, void* scratch, size_t* scratch_bytes,
-                             void* stream) {
+                             uint32_t flags, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
   if (!scratch_bytes || capacity == 0 || capacity >= (1ull << 31)) return SSPD_ERR_CONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t C = (size_t)capacity;
   const size_t vec = ((C * 4 + 255) / 256) * 256;
+  const bool bucket = (flags & 1u) == 0 && C <= kBucketSortMaxCap;
+  // bucket count: ~16 keys per bucket at full capacity, power of two
+  uint32_t nb = 256;
+  while ((uint64_t)nb * 16 < C && nb < 16384) nb <<= 1;
+  const uint32_t hshift = 32 - (31 - __builtin_clz(nb));
   // the filter and the report list need the candidate IPs only: sort keys
   // (restore's AND-weights are not part of a report)
   size_t sort_tmp = 0;
@@ -793,11 +913,13 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
       return SSPD_ERR_CUDA;
   }
   const size_t segs = (C + kSeg - 1) / kSeg;
-  // [ip | aux | ip_alt | aux_alt | z0 | keep | sort temp | compaction segs]
+  // [ip | aux | ip_alt | aux_alt | z0 | keep | sort temp | compaction segs | hist, cursor | starts]
   const size_t o_aux = vec, o_ipa = 2 * vec, o_auxa = 3 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;
   const size_t o_tmp = o_keep + ((C + 255) / 256) * 256;
   const size_t o_seg = o_tmp + ((sort_tmp + 255) / 256) * 256;
-  const size_t need = o_seg + 4 * segs + 256;
+  const size_t o_hist = o_seg + ((4 * segs + 255) / 256) * 256;
+  const size_t o_start = o_hist + 8ull * 16384;
+  const size_t need = o_start + 4ull * (16384 + 1) + 256;
   if (!scratch) {
     *scratch_bytes = need;
     return SSPD_OK;
@@ -808,19 +930,34 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   uint32_t* ip = reinterpret_cast<uint32_t*>(s8);
   uint32_t* aux = reinterpret_cast<uint32_t*>(s8 + o_aux);
   uint32_t* ipa = reinterpret_cast<uint32_t*>(s8 + o_ipa);
-  uint32_t* auxa = reinterpret_cast<uint32_t*>(s8 + o_auxa);
   uint32_t* z0 = reinterpret_cast<uint32_t*>(s8 + o_z0);
   uint8_t* keep = s8 + o_keep;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(s8 + o_hist);
+  uint32_t* cursor = hist + nb;
+  uint32_t* starts = reinterpret_cast<uint32_t*>(s8 + o_start);
   const uint32_t rp_count = 1u << p->r;
-  if (cudaMemsetAsync(ip, 0xFF, C * 4, st) != cudaSuccess || cudaMemsetAsync(counts, 0, 16, st) != cudaSuccess ||
-      cudaMemsetAsync(overflow, 0, rp_count, st) != cudaSuccess)
+  if (cudaMemsetAsync(counts, 0, 16, st) != cudaSuccess || cudaMemsetAsync(overflow, 0, rp_count + 1, st) != cudaSuccess)
     return SSPD_ERR_CUDA;
-  rc = sspd_restore(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, stream);
-  if (rc) return rc;
-  size_t tb = sort_tmp;
-  cub::DoubleBuffer<uint32_t> kb(ip, ipa);
-  if (cub::DeviceRadixSort::SortKeys(s8 + o_tmp, tb, kb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
-  const uint32_t* sorted = kb.Current();
+  const uint32_t* sorted = ip;
+  if (bucket) {
+    if (cudaMemsetAsync(hist, 0, 8ull * nb, st) != cudaSuccess) return SSPD_ERR_CUDA;
+    rc = restore_launch(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, hist, hshift, stream);
+    if (rc) return rc;
+    const uint32_t smem = 4u * nb;
+    if (smem > 48u * 1024u)
+      cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint32_t grid = (uint32_t)std::min<size_t>(296, (C + 4095) / 4096);
+    bucket_scatter_kernel<<<grid, 1024, smem, st>>>(ip, counts, C, hist, nb, hshift, cursor, starts, ipa);
+    bucket_sort_kernel<<<(nb * 32 + 255) / 256, 256, 0, st>>>(ipa, starts, nb, ip, overflow + rp_count);
+  } else {
+    if (cudaMemsetAsync(ip, 0xFF, C * 4, st) != cudaSuccess) return SSPD_ERR_CUDA;
+    rc = restore_launch(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, nullptr, 0, stream);
+    if (rc) return rc;
+    size_t tb = sort_tmp;
+    cub::DoubleBuffer<uint32_t> kb(ip, ipa);
+    if (cub::DeviceRadixSort::SortKeys(s8 + o_tmp, tb, kb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
+    sorted = kb.Current();
+  }
   const int grid = grid_for(filter_kernel, 256, C * 32);
   filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);
   size_t cb = 4 * segs;

@@ -242,6 +242,7 @@ class SeavSketch:
         self._params = build_params(config, _ldca_config or LdcaConfig(lr=1, lc=1, k=8), seeds)
         self._buf = zeros_bytes(config.memory_bytes())
         self._cand_cap = 1 << 14
+        self._radix_sort = False  # learned: candidates too skewed for the finalize's bucket sort
         self._scratch_buf = None
 
     def _scratch(self, nbytes: int):

@@ -225,23 +225,24 @@ class DeviceFinalize:
 
         seav = self.seav
         self.cap = cap
-        nflag_words = ((1 << seav.config.r) + 3) // 4
+        nflag_words = ((1 << seav.config.r) + 1 + 3) // 4  # + the bucket-sort flag byte
         with torch.cuda.stream(self.stream):
             dev = seav._buf.device
             table = device_keep_table(self.k, self.cutoff)
-            # one device block: ip[cap] | z0[cap] | counts (2 x u64) | overflow flags (2^r B)
+            # one device block: ip[cap] | z0[cap] | counts (2 x u64) | overflow flags (2^r B) | bucket flag (1 B)
             self.out = torch.empty(2 * cap + 4 + nflag_words, dtype=torch.int32, device=dev)
             base = self.out.data_ptr()
             need = _FINALIZE_SCRATCH.get(cap)
             if need is None:
                 nb = ctypes.c_size_t(0)
                 call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None,
-                     ctypes.byref(nb), 0)
+                     ctypes.byref(nb), 0, 0)
                 need = _FINALIZE_SCRATCH[cap] = nb.value
             scratch = seav._scratch(need)
             call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
                  table.data_ptr(), cap, base, base + 4 * cap, base + 8 * cap, base + 8 * cap + 16,
-                 scratch.data_ptr(), ctypes.byref(ctypes.c_size_t(need)), self.stream.cuda_stream)
+                 scratch.data_ptr(), ctypes.byref(ctypes.c_size_t(need)), 1 if seav._radix_sort else 0,
+                 self.stream.cuda_stream)
             # counts + flags back in ONE pinned copy
             self.h_tail = torch.empty(4 + nflag_words, dtype=torch.int32, pin_memory=True)
             self.h_tail.copy_(self.out[2 * cap:], non_blocking=True)
@@ -255,14 +256,20 @@ class DeviceFinalize:
         from .errors import SeaOverflowError
 
         self.event.synchronize()
+        nsea = 1 << self.seav.config.r
         found, kept = (int(x) for x in self.h_tail[:4].numpy().view(np.int64))
         if found > self.cap:  # candidates did not fit: learn the size, run again
             self.seav._cand_cap = 1 << (found - 1).bit_length()
             self._launch(self.seav._cand_cap)
             self.event.synchronize()
             found, kept = (int(x) for x in self.h_tail[:4].numpy().view(np.int64))
+        if self.h_tail[4:].numpy().view(np.uint8)[nsea]:  # a bucket too large to order: radix sort from now on
+            self.seav._radix_sort = True
+            self._launch(self.cap)
+            self.event.synchronize()
+            found, kept = (int(x) for x in self.h_tail[:4].numpy().view(np.int64))
         self.found = found  # candidates restored
-        flags = self.h_tail[4:].numpy().view(np.uint8)[: 1 << self.seav.config.r]
+        flags = self.h_tail[4:].numpy().view(np.uint8)[:nsea]
         for rp in np.nonzero(flags)[0].tolist():
             err = SeaOverflowError(rp, self.seav.restore_cap)
             if self.on_overflow != "warn":
@@ -486,6 +493,7 @@ class DetectorState:
         sv.copy_(self.seav.device_buffer()[: sv.numel()])
         snap[1].copy_(self.ldca.device_buffer()[: snap[1].numel()])
         snap[0]._cand_cap = max(snap[0]._cand_cap, self.seav._cand_cap, *(s[0]._cand_cap for s in snaps if s))
+        snap[0]._radix_sort = snap[0]._radix_sort or self.seav._radix_sort or any(s[0]._radix_sort for s in snaps if s)
         fin = DeviceFinalize(snap[0], snap[1], self.seav._params, k, cutoff)
         snap[2] = fin
         wid = self.window_id

@@ -382,3 +382,45 @@ def test_finalize_window_async_equals_sync(cuda):
         b.reset()
     got = [[(r.ip, r.estimated_cardinality, r.saturated, r.window_id) for r in p] for p in pend]
     assert got == want and all(len(x) >= 6 for x in want)
+
+
+@pytest.mark.parametrize("skewed", [False, True])
+def test_finalize_bucket_sort_vs_oracle(cuda, oracle, skewed):
+    """The fused finalize orders candidates with a bucket sort (buckets of
+    the top IP bits, <= 64 keys per warp); a bucket above that (here: 150
+    super points inside one /16) raises the kernel's flag and the finalize is
+    re-run with the radix sort, learned for the sketch.  Both give the
+    oracle's report list."""
+    import math
+
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=4e5)
+    _, _, p = params_block(dp)
+    rng = np.random.default_rng(31 + skewed)
+    n = 1_200_000
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    nheavy = 150
+    if skewed:
+        heavy = (0x0A0B0000 + rng.choice(1 << 16, size=nheavy, replace=False)).astype(np.uint64)
+    else:
+        heavy = rng.integers(0, 2**32, size=nheavy, dtype=np.uint64)
+    per = 1200
+    hips[: nheavy * per] = np.repeat(heavy, per)
+    perm = rng.permutation(n)
+    hips, oips = hips[perm], oips[perm]
+    st = make_state(dp)
+    st.process_batch(hips, oips)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        reports = st.finalize_window()
+    seav, ldca = oracle.scan(p, hips, oips, threads=8)
+    ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+    z0 = oracle.filter_z0(p, ldca, ips)
+    k = dp.k
+    want = [int(ip) for ip, z in zip(ips, z0) if z == 0 or -k * math.log(z / k) >= dp.beta * dp.theta]
+    got = [r.ip for r in reports]
+    assert got == want
+    assert st.seav._radix_sort == skewed
+    assert len(set(heavy.tolist()) & set(got)) > nheavy // 2
