@@ -528,6 +528,8 @@ def run_sliding(args) -> dict:
                               window_slices=300)
     if args.direct_stamps:
         det.defer_ldca_stamps = False
+    if args.no_finalize_graphs:
+        det.finalize_graphs = False  # the fused finalize launched op by op from the host
     if args.no_ldca_ring:
         det.ldca_ring_max_bytes = 0  # deferred single-bitmap mode (one fold + view per slide)
     if os.environ.get("SSPD_PIPELINE_DEPTH"):
@@ -884,6 +886,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="process-group backend (N > 1)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on GPU 0 (multi-rank protocol test)")
     ap.add_argument("--sync-detect", action="store_true", help="config 4: synchronous detect() per slide")
+    ap.add_argument("--no-finalize-graphs", action="store_true",
+                    help="config 4: launch the per-slide finalize op by op instead of replaying its CUDA graph")
     ap.add_argument("--no-ldca-ring", action="store_true",
                     help="config 4: deferred LDCA stamps without the ring of per-slice bitmaps (fold per slide)")
     ap.add_argument("--direct-stamps", action="store_true",

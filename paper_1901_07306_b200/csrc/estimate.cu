@@ -49,6 +49,12 @@ struct RestorePlan {
   uint32_t off_pref0, off_misc, smem_bytes, hshift;
   uint64_t seav_row_off[SSPD_MAX_SR];
   uint32_t* hist;  // optional: per-bucket candidate counts (bucket = ip >> hshift) for the bucket sort
+  // one-load staging of a whole SEA by a warp (g = 8 one-byte registers,
+  // rows of multiples of 8 bytes, <= 256 bytes per SEA, e.g. r = 16): lane l
+  // loads 8 bytes of row lane_row[l] at byte lane_off[l] (lane_row >= sr: idle)
+  uint32_t lane_fast;
+  uint32_t row_lanes[SSPD_MAX_SR];  // ballot mask of the lanes holding row i
+  uint8_t lane_row[32], lane_off[32];
 };
 
 __device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
@@ -233,26 +239,49 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t sr = P.sr;
 
-  // fast reject straight from global memory: a row without a hot register
-  // admits no complete tuple (short_sketch.py:360-361), so the SEA has no
-  // candidates and no survivors (it cannot overflow either).  Most SEAs of
-  // a large, sparse SEAV end here without touching shared memory.
-  for (uint32_t i = 0; i < sr; ++i) {
-    const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * P.sc[i] * P.reg_bytes;
-    bool hot = false;
-    for (uint32_t c = G.tid; c < P.sc[i]; c += G.size) hot |= __popcll(load_reg(src, c, P.reg_bytes)) >= 3;
-    if (!G.any(hot)) return;
+  // fast reject: a row without a hot register admits no complete tuple
+  // (short_sketch.py:360-361), so the SEA has no candidates and no
+  // survivors (it cannot overflow either).  Most SEAs of a large, sparse
+  // SEAV end here without touching shared memory.
+  bool staged = false;
+  if (kWarp && P.lane_fast) {
+    // the whole SEA in ONE independent 8-byte load per lane (instead of a
+    // dependent round trip per row, which is what a restore co-running with
+    // the L2-atomic-bound sliding scan waits on); hot = a byte of weight >= 3
+    const uint32_t row = P.lane_row[G.tid];
+    const bool act = row < sr;
+    uint64_t v = 0;
+    if (act)
+      v = __ldg(reinterpret_cast<const uint64_t*>(seav + P.seav_row_off[row] + (uint64_t)rp * P.sc[row] +
+                                                  P.lane_off[G.tid]));
+    uint64_t c = v - ((v >> 1) & 0x5555555555555555ull);
+    c = (c & 0x3333333333333333ull) + ((c >> 2) & 0x3333333333333333ull);
+    c = (c + (c >> 4)) & 0x0F0F0F0F0F0F0F0Full;                      // per-byte popcounts (<= 8)
+    const bool hot = act && ((c + 0x7D7D7D7D7D7D7D7Dull) & 0x8080808080808080ull) != 0;  // some byte >= 3
+    const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hot);
+    for (uint32_t i = 0; i < sr; ++i)
+      if ((hb & P.row_lanes[i]) == 0) return;
+    if (act) *reinterpret_cast<uint64_t*>(sm + P.off_regs[row] + P.lane_off[G.tid]) = v;
+    staged = true;
+  } else {
+    for (uint32_t i = 0; i < sr; ++i) {
+      const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * P.sc[i] * P.reg_bytes;
+      bool hot = false;
+      for (uint32_t c = G.tid; c < P.sc[i]; c += G.size) hot |= __popcll(load_reg(src, c, P.reg_bytes)) >= 3;
+      if (!G.any(hot)) return;
+    }
   }
 
-  // stage the SEA's registers and clear the bucket tables
+  // stage the SEA's registers (unless the one-load path did) and clear the
+  // bucket tables
   for (uint32_t i = 0; i < sr; ++i) {
     const uint32_t nbytes = P.sc[i] * P.reg_bytes;
     const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * nbytes;
     uint8_t* dst = sm + P.off_regs[i];
-    if ((nbytes & 15u) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+    if (!staged && (nbytes & 15u) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
       for (uint32_t o = G.tid * 16; o < nbytes; o += G.size * 16)
         *reinterpret_cast<uint4*>(dst + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
-    } else {
+    } else if (!staged) {
       for (uint32_t o = G.tid; o < nbytes; o += G.size) dst[o] = src[o];
     }
     uint32_t* bs = reinterpret_cast<uint32_t*>(sm + P.off_bstart[i]);
@@ -638,6 +667,30 @@ static int build_plan(const sspd_params& p, RestorePlan& P) {
   P.smem_bytes = off;
   P.hist = nullptr;
   P.hshift = 0;
+  // one-load warp staging (see RestorePlan::lane_fast)
+  P.lane_fast = 0;
+  {
+    bool ok = p.reg_bytes == 1 && p.sr <= 32;
+    uint32_t lane = 0;
+    for (uint32_t i = 0; i < p.sr && ok; ++i) {
+      ok = (p.sc[i] % 8) == 0 && (p.seav_row_off[i] % 8) == 0 && (P.off_regs[i] % 8) == 0;
+      P.row_lanes[i] = 0;
+      for (uint32_t o = 0; ok && o < p.sc[i]; o += 8, ++lane) {
+        if (lane >= 32) {
+          ok = false;
+          break;
+        }
+        P.lane_row[lane] = (uint8_t)i;
+        P.lane_off[lane] = (uint8_t)o;
+        P.row_lanes[i] |= 1u << lane;
+      }
+    }
+    for (uint32_t l = lane; l < 32; ++l) {
+      P.lane_row[l] = 0xFF;
+      P.lane_off[l] = 0;
+    }
+    P.lane_fast = ok ? 1u : 0u;
+  }
   return SSPD_OK;
 }
 

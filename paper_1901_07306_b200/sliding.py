@@ -384,6 +384,9 @@ class SlidingDetector:
 
     pipelined_scan_blocks_per_sm = 2  # K2 grid cap while detect_async runs (measured best on B200)
     pipeline_depth = 2  # view sets of detect_async (detects in flight)
+    # detect_async replays the fused finalize of each view set as one CUDA
+    # graph (captured per capacity) instead of ~12 launches from the host
+    finalize_graphs = True
     # keep the SEAV active-bit view up to date (stamp-time set + expiry log)
     # instead of re-reading the whole SEAV stamp region at every detect
     incremental_seav = True
@@ -668,9 +671,10 @@ class SlidingDetector:
         st["n"] += 1
         vset = st["sets"][i]
         if vset is None:
-            vset = st["sets"][i] = [self.materialize_seav(), zeros_bytes(self._params.ldca_bytes), None]
+            vset = st["sets"][i] = [self.materialize_seav(), zeros_bytes(self._params.ldca_bytes), None, {}]
         elif vset[2] is not None:
             vset[2].resolve()  # the finalize `pipeline_depth` calls ago is done with this view set
+            vset[2].detach()  # its report arrays leave the set's graph buffers
         seav, lview = vset[0], vset[1]
         self._ldca_view_into(lview)  # first: fused with the fold of deferred stamps
         if self._iv() is not None:  # snapshot of the incremental view (16 MiB at r=16)
@@ -682,7 +686,8 @@ class SlidingDetector:
         views_ready.record(torch.cuda.current_stream())
         side = st["side"]
         side.wait_event(views_ready)
-        fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff, stream=side)
+        graphs = vset[3] if self.finalize_graphs else None
+        fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff, stream=side, graphs=graphs)
         vset[2] = fin
         now = self.now
         return PendingReports(lambda: fin.reports(now, "sliding"))

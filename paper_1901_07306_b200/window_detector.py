@@ -209,45 +209,97 @@ class DeviceFinalize:
     access."""
 
     def __init__(self, seav: SeavSketch, ldca_buf, params_block, k: int, cutoff: float, stream=None,
-                 on_overflow: str = "warn"):
+                 on_overflow: str = "warn", graphs: dict | None = None):
         import torch
 
         self.seav, self.ldca, self.p, self.k, self.cutoff = seav, ldca_buf, params_block, k, cutoff
         self.stream = stream or torch.cuda.current_stream()
         self.on_overflow = on_overflow
         self.m = None
+        self.graphs = graphs
+        self.shared = False  # self.out / self.h_tail belong to a replayed graph
         self._launch(max(1024, seav._cand_cap))
+
+    def _enqueue(self, cap: int, out, h_tail):
+        """sspd_finalize into `out` + the pinned copy of its counts/flags."""
+        from ._device import call, stream_ptr
+
+        seav = self.seav
+        table = device_keep_table(self.k, self.cutoff)
+        base = out.data_ptr()
+        need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
+        scratch = seav._scratch(need)
+        call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
+             table.data_ptr(), cap, base, base + 4 * cap, base + 8 * cap, base + 8 * cap + 16,
+             scratch.data_ptr(), ctypes.byref(ctypes.c_size_t(need)), 1 if seav._radix_sort else 0, stream_ptr())
+        # counts + flags back in ONE pinned copy
+        h_tail.copy_(out[2 * cap:], non_blocking=True)
 
     def _launch(self, cap: int):
         import torch
 
-        from ._device import call
-
         seav = self.seav
         self.cap = cap
         nflag_words = ((1 << seav.config.r) + 1 + 3) // 4  # + the bucket-sort flag byte
+        dev = seav._buf.device
+        # one device block: ip[cap] | z0[cap] | counts (2 x u64) | overflow flags (2^r B) | bucket flag (1 B)
+        shape = 2 * cap + 4 + nflag_words
+        if self.graphs is not None:
+            # per view set: the whole finalize (~12 launches, memsets and the
+            # D2H copy of the counts) captured once per capacity / sort mode
+            # and replayed as ONE graph launch; buffers belong to the graph
+            key = (cap, seav._radix_sort, self.ldca.data_ptr(), self.cutoff, seav.restore_cap)
+            g = self.graphs.get(key)
+            if g is None:
+                out = torch.empty(shape, dtype=torch.int32, device=dev)
+                h_tail = torch.empty(4 + nflag_words, dtype=torch.int32, pin_memory=True)
+                # allocations outside the capture: scratch size, scratch, keep table
+                need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
+                seav._scratch(need)
+                device_keep_table(self.k, self.cutoff)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=self.stream, capture_error_mode="thread_local"):
+                    self._enqueue(cap, out, h_tail)
+                g = self.graphs[key] = (graph, out, h_tail)
+            graph, self.out, self.h_tail = g
+            self.shared = True
+            with torch.cuda.stream(self.stream):
+                graph.replay()
+                self.event = torch.cuda.Event()
+                self.event.record(self.stream)
+            return
         with torch.cuda.stream(self.stream):
-            dev = seav._buf.device
-            table = device_keep_table(self.k, self.cutoff)
-            # one device block: ip[cap] | z0[cap] | counts (2 x u64) | overflow flags (2^r B) | bucket flag (1 B)
-            self.out = torch.empty(2 * cap + 4 + nflag_words, dtype=torch.int32, device=dev)
-            base = self.out.data_ptr()
-            need = _FINALIZE_SCRATCH.get(cap)
-            if need is None:
-                nb = ctypes.c_size_t(0)
-                call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None,
-                     ctypes.byref(nb), 0, 0)
-                need = _FINALIZE_SCRATCH[cap] = nb.value
-            scratch = seav._scratch(need)
-            call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
-                 table.data_ptr(), cap, base, base + 4 * cap, base + 8 * cap, base + 8 * cap + 16,
-                 scratch.data_ptr(), ctypes.byref(ctypes.c_size_t(need)), 1 if seav._radix_sort else 0,
-                 self.stream.cuda_stream)
-            # counts + flags back in ONE pinned copy
+            self.out = torch.empty(shape, dtype=torch.int32, device=dev)
             self.h_tail = torch.empty(4 + nflag_words, dtype=torch.int32, pin_memory=True)
-            self.h_tail.copy_(self.out[2 * cap:], non_blocking=True)
+            self._enqueue(cap, self.out, self.h_tail)
             self.event = torch.cuda.Event()
             self.event.record(self.stream)
+
+    def _scratch_query(self, cap: int):
+        from ._device import call
+
+        nb = ctypes.c_size_t(0)
+        call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None, ctypes.byref(nb), 0, 0)
+        _FINALIZE_SCRATCH[cap] = nb.value
+        return nb.value
+
+    def detach(self):
+        """Before the graph that produced this result is replayed again:
+        give a resolved, not yet fetched report list private copies of its
+        device arrays (async, on the finalize's stream)."""
+        import torch
+
+        if not self.shared or self.out is None:
+            return
+        self.resolve()
+        m, cap = self.m, self.cap
+        with torch.cuda.stream(self.stream):
+            own = torch.empty(2 * cap if m else 0, dtype=torch.int32, device=self.out.device)
+            if m:
+                own[:m].copy_(self.out[:m], non_blocking=True)
+                own[cap:cap + m].copy_(self.out[cap:cap + m], non_blocking=True)
+        self.out = own
+        self.shared = False
 
     def resolve(self) -> int:
         """Number of reports (waits for the device counts; idempotent)."""
