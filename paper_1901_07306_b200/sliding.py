@@ -257,6 +257,7 @@ class _DeferredLdca:
             self.acc = zeros_bytes(nbytes)
             self.cur = self.blk0 = self.fold_lo = 0
             self.cur_merged = True
+            self.next_zeroed = False
             self.prev_ok = False
             self.pristine = True
             self.version = None
@@ -325,6 +326,7 @@ class _DeferredLdca:
         self._zero_slot(self.cur)
         self.acc.zero_()
         self.cur_merged = True
+        self.next_zeroed = False
         self.prev_ok = False
         self.pristine = pristine
         self.pending = False
@@ -345,9 +347,12 @@ class _DeferredLdca:
 
         first = self.cur - self.w + 1
         suffix = self.slot_ptr(first) if self.prev_ok and first <= self.blk0 - 1 else None
-        call("sspd_ldca_window_or", self.slot_ptr(self.cur), self.acc.data_ptr(), suffix, lview.data_ptr(), None,
-             self.nbytes, stream_ptr())
+        # the next slice's slot (= slice cur - w, outside the window) is
+        # cleared in the same pass
+        call("sspd_ldca_window_or", self.slot_ptr(self.cur), self.acc.data_ptr(), suffix, lview.data_ptr(),
+             self.slot_ptr(self.cur + 1), self.nbytes, stream_ptr())
         self.cur_merged = True
+        self.next_zeroed = True
 
     def advance(self, pool):
         """End of slice `cur` (before the pool's slice advances)."""
@@ -360,12 +365,14 @@ class _DeferredLdca:
             self.pristine = False
             self.blk0 = self.cur + 1
             self.acc.zero_()
-            self._zero_slot(self.cur + 1)
+            if not self.next_zeroed:
+                self._zero_slot(self.cur + 1)
         elif not self.cur_merged:  # acc |= dirty[cur], and clear the next slice's slot
             call("sspd_ldca_window_or", self.slot_ptr(self.cur), self.acc.data_ptr(), None, None,
                  self.slot_ptr(self.cur + 1), self.nbytes, stream_ptr())
-        else:
+        elif not self.next_zeroed:
             self._zero_slot(self.cur + 1)
+        self.next_zeroed = False
         if not self.pending:
             self.fold_lo = self.cur + 1
         self.cur += 1

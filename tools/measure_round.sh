@@ -15,7 +15,7 @@ timeout 600 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$
 timeout 900 python bench.py --config 3 --steps 3 --warmup 1 > "$OUT/bench_config3.json" 2> "$OUT/bench_config3.err"; echo "c3=$?"
 timeout 600 python bench.py --config 4 --steps 3 --warmup 1 > "$OUT/bench_config4.json" 2> "$OUT/bench_config4.err"; echo "c4=$?"
 # config-4 launch list inside the timed step (the warmup step is ~5,000 launches)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled --launch-skip 5600 -c 170 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled --launch-skip 3600 -c 180 --csv \
   --log-file "$OUT/launches_config4.csv" python bench.py --config 4 --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1
 echo "launches4=$?"
 timeout 900 python bench.py --config 5 --steps 1 --warmup 1 > "$OUT/bench_config5.json" 2> "$OUT/bench_config5.err"; echo "c5=$?"
@@ -30,8 +30,8 @@ echo "launches=$?"
 # full capture of the dominant kernel
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_partitioned -c 1 -f -o "$OUT/k1p_full" \
   python tools/sweep_k1p.py --reps 1 "" > /dev/null 2>&1; echo "ncu_full=$?"
-# full captures of the config-4 scan (deferred) and fold+view kernels
+# full captures of the config-4 scan (deferred) and the restore (K5, warp per SEA)
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_sliding_u16_fast --launch-skip 400 -c 1 -f \
   -o "$OUT/k2_deferred_full" python bench.py --config 4 --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1; echo "ncu_k2=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:ldca_fold --launch-skip 150 -c 1 -f \
-  -o "$OUT/fold_full" python bench.py --config 4 --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1; echo "ncu_fold=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:restore_warp --launch-skip 150 -c 1 -f \
+  -o "$OUT/restore_full" python bench.py --config 4 --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1; echo "ncu_restore=$?"
