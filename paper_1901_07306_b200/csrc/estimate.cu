@@ -55,6 +55,12 @@ struct RestorePlan {
   uint32_t lane_fast;
   uint32_t row_lanes[SSPD_MAX_SR];  // ballot mask of the lanes holding row i
   uint8_t lane_row[32], lane_off[32];
+  // ... and, when every row has <= 64 registers, the tuples are enumerated
+  // straight from per-row hot-column masks (no bucket tables) as long as
+  // their number is <= kEnumMax and <= cap
+  uint32_t lane_enum, enum_max;
+  uint32_t row_lane0[SSPD_MAX_SR];  // first lane of row i
+  uint32_t row_bits[SSPD_MAX_SR];   // LP positions row i fixes (row_mask), w <= 32
 };
 
 __device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
@@ -82,6 +88,8 @@ struct Misc {
   uint32_t abort;
   uint32_t pairs;
   uint32_t hot[SSPD_MAX_SR];
+  uint8_t hmask[32];  // one-load path: per-lane hot-byte masks (8 registers each)
+  unsigned long long rmask[SSPD_MAX_SR];  // ... assembled per row (enumeration path)
 };
 
 // In-place exclusive scan of a[0..m) by one warp; returns the total.
@@ -101,6 +109,29 @@ __device__ uint32_t warp_exclusive_scan(uint32_t* a, uint32_t m) {
     carry += __shfl_sync(0xFFFFFFFFu, x, 31);
   }
   return carry;
+}
+
+// Emit one candidate (weight >= 3 already checked by the caller): the lanes
+// emitting together take one slot range from the shared counter.
+__device__ __forceinline__ void emit_candidate(const RestorePlan& P, uint64_t lp, uint32_t rp, uint32_t wgt,
+                                               uint32_t* out_ip, uint32_t* out_aux, uint64_t out_capacity,
+                                               unsigned long long* out_count) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(out_count, (unsigned long long)g.size());
+  const unsigned long long slot = g.shfl(base, 0) + g.thread_rank();
+  if (slot < out_capacity) {
+    const uint32_t ip = (uint32_t)((lp << P.r) | rp);
+    out_ip[slot] = ip;
+    out_aux[slot] = (rp << 8) | wgt;
+    if (P.hist) atomicAdd(P.hist + (ip >> P.hshift), 1u);
+  }
+}
+
+// k-th (0-based) set bit of a 64-bit mask
+__device__ __forceinline__ uint32_t nth_bit64(uint64_t m, uint32_t k) {
+  const uint32_t lo = (uint32_t)m, nlo = __popc(lo);
+  return k < nlo ? __fns(lo, 0, (int)k + 1) : 32u + __fns((uint32_t)(m >> 32), 0, (int)(k - nlo) + 1);
 }
 
 template <bool kEmit>
@@ -263,6 +294,48 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
       if ((hb & P.row_lanes[i]) == 0) return;
     if (act) *reinterpret_cast<uint64_t*>(sm + P.off_regs[row] + P.lane_off[G.tid]) = v;
     staged = true;
+    if (P.lane_enum) {
+      // per-row hot-column masks: lane l's 8 hot bits are bits lane_off..+7
+      // of its row's mask (bytes in lane order = little-endian mask bytes)
+      const uint64_t hb8 = ((c + 0x7D7D7D7D7D7D7D7Dull) >> 7) & 0x0101010101010101ull;
+      misc->hmask[G.tid] = act ? (uint8_t)((hb8 * 0x0102040810204080ull) >> 56) : (uint8_t)0;
+      __syncwarp();
+      if (G.tid < sr) {
+        uint64_t m = 0;
+        for (uint32_t j = 0; j < (P.sc[G.tid] >> 3); ++j)
+          m |= (uint64_t)misc->hmask[P.row_lane0[G.tid] + j] << (8 * j);
+        misc->rmask[G.tid] = m;
+      }
+      __syncwarp();
+      uint64_t tuples = 1;
+      for (uint32_t i = 0; i < sr && tuples <= P.enum_max; ++i) tuples *= (uint64_t)__popcll(misc->rmask[i]);
+      if (tuples <= P.enum_max && tuples <= cap) {
+        // every complete tuple is one LP, so the survivors (<= tuples) cannot
+        // exceed the cap: no counting pass.  Lane t walks tuples t, t+32, ...
+        // and keeps the consistent ones (the DFS prune of
+        // short_sketch.py:379-388 applied row by row)
+        const uint64_t full = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
+        for (uint32_t t = G.tid; t < (uint32_t)tuples; t += 32) {
+          uint32_t q = t;
+          uint64_t lp = 0, fixed = 0, acc = full;
+          bool ok = true;
+          for (uint32_t i = 0; i < sr; ++i) {
+            const uint64_t m = misc->rmask[i];
+            const uint32_t h = __popcll(m);
+            const uint32_t col = nth_bit64(m, q % h);
+            q /= h;
+            const uint64_t v = scatter_col(col, P.isb[i], P.ibn[i], P.w);
+            ok &= ((lp ^ v) & fixed & P.row_bits[i]) == 0;
+            lp |= v;
+            fixed |= P.row_bits[i];
+            acc &= sm[P.off_regs[i] + col];
+          }
+          const uint32_t wgt = (uint32_t)__popcll(acc);
+          if (ok && wgt >= 3) emit_candidate(P, lp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
+        }
+        return;
+      }
+    }
   } else {
     for (uint32_t i = 0; i < sr; ++i) {
       const uint8_t* src = seav + P.seav_row_off[i] + (uint64_t)rp * P.sc[i] * P.reg_bytes;
@@ -690,6 +763,18 @@ static int build_plan(const sspd_params& p, RestorePlan& P) {
       P.lane_off[l] = 0;
     }
     P.lane_fast = ok ? 1u : 0u;
+    bool en = ok && p.lp_bits <= 32;
+    uint32_t l0 = 0;
+    for (uint32_t i = 0; i < p.sr && en; ++i) {
+      en = p.sc[i] <= 64;
+      P.row_lane0[i] = l0;
+      l0 += p.sc[i] / 8;
+      P.row_bits[i] = (uint32_t)row_mask(p.isb[i], p.ibn[i], p.lp_bits);
+    }
+    P.lane_enum = en ? 1u : 0u;
+    // tuples a warp enumerates before the bucket tables pay off (measured)
+    P.enum_max = 128;
+    if (const char* e = getenv("SSPD_RESTORE_ENUM_MAX")) P.enum_max = (uint32_t)atoi(e);
   }
   return SSPD_OK;
 }
