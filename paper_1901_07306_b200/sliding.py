@@ -697,7 +697,12 @@ class SlidingDetector:
         fin = DeviceFinalize(seav, lview, self._params, self.ldca_config.k, cutoff, stream=side, graphs=graphs)
         vset[2] = fin
         now = self.now
-        return PendingReports(lambda: fin.reports(now, "sliding"))
+        pending = PendingReports(lambda: fin.reports(now, "sliding"))
+        if fin.shared:
+            import weakref
+
+            fin.owner = weakref.ref(pending)  # a dropped list needs no private copy of its arrays
+        return pending
 
 
 def _async_state(det):

@@ -71,7 +71,7 @@ class ReportList(Sequence):
     made by the fused device finalize knows its length from the device
     counts and copies the (ip, z0) arrays to the host on first access."""
 
-    __slots__ = ("_ips", "_z0s", "k", "window_id", "source", "_est", "_n", "_fetch")
+    __slots__ = ("_ips", "_z0s", "k", "window_id", "source", "_est", "_n", "_fetch", "__weakref__")
 
     def __init__(self, ips, z0s, k: int, window_id: int, source: str, n: int | None = None, fetch=None):
         self._ips = ips
@@ -218,6 +218,8 @@ class DeviceFinalize:
         self.m = None
         self.graphs = graphs
         self.shared = False  # self.out / self.h_tail belong to a replayed graph
+        self.owner = None  # weakref to the PendingReports handed out for this result, if any
+        self.list_ref = None  # weakref to the ReportList that still has to fetch its arrays
         self._launch(max(1024, seav._cand_cap))
 
     def _enqueue(self, cap: int, out, h_tail):
@@ -292,6 +294,11 @@ class DeviceFinalize:
         if not self.shared or self.out is None:
             return
         self.resolve()
+        rl = self.list_ref() if self.list_ref is not None else None
+        if self.owner is not None and self.owner() is None and rl is None:  # nobody can read the arrays any more
+            self.out = None
+            self.shared = False
+            return
         m, cap = self.m, self.cap
         with torch.cuda.stream(self.stream):
             own = torch.empty(2 * cap if m else 0, dtype=torch.int32, device=self.out.device)
@@ -349,7 +356,12 @@ class DeviceFinalize:
         m = self.resolve()
         if m == 0:
             return ReportList(np.zeros(0, dtype=np.uint32), np.zeros(0, dtype=np.uint32), self.k, window_id, source)
-        return ReportList(None, None, self.k, window_id, source, n=m, fetch=self._fetch)
+        rl = ReportList(None, None, self.k, window_id, source, n=m, fetch=self._fetch)
+        if self.shared:
+            import weakref
+
+            self.list_ref = weakref.ref(rl)
+        return rl
 
 
 class PendingReports(Sequence):
@@ -358,7 +370,7 @@ class PendingReports(Sequence):
     without a host round trip; the first access waits for it, then this
     behaves exactly like the ReportList the synchronous call returns."""
 
-    __slots__ = ("_resolve", "_value")
+    __slots__ = ("_resolve", "_value", "__weakref__")
 
     def __init__(self, resolve):
         self._resolve = resolve

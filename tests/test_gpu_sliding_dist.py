@@ -516,3 +516,40 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect):
     a.reset()
     b.reset()
     assert a._ring().valid() and np.array_equal(a.pool.ts, b.pool.ts)
+
+
+@pytest.mark.gpu
+def test_detect_async_lists_outlive_their_view_set(cuda):
+    """detect_async replays each view set's finalize graph into the same
+    device buffers: a list still held when its set is reused -- as the
+    PendingReports or only as the resolved ReportList -- keeps its own copy
+    of the arrays; dropped lists cost no copy.  Every held list equals the
+    synchronous detect() of a twin detector."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=256, r=16, k=4096, lr=4, lc=256, design_n=2e5)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=16)
+        b = SlidingDetector(params, window_slices=16)
+    rng = np.random.default_rng(5)
+    heavy = rng.integers(0, 2**32, size=5, dtype=np.uint64)
+    held, want = {}, {}
+    for s in range(30):
+        n = int(rng.integers(5_000, 40_000))
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        hips[: n // 3] = heavy[s % 5]
+        a.observe_batch(hips, oips)
+        b.observe_batch(hips, oips)
+        p = a.detect_async()
+        ref = rep_list(b.detect())
+        if s % 3 == 0:
+            held[s] = p  # the pending handle
+        elif s % 3 == 1:
+            held[s] = p.result()  # only the resolved list (its arrays not fetched yet)
+        want[s] = ref
+        a.advance_slice()
+        b.advance_slice()
+    assert {s: rep_list(x) for s, x in held.items()} == {s: want[s] for s in held}
+    assert sum(len(want[s]) for s in held) > 0
