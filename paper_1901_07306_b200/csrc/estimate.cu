@@ -128,6 +128,18 @@ __device__ __forceinline__ void emit_candidate(const RestorePlan& P, uint64_t lp
   }
 }
 
+// Columns c < sc (<= 64) whose bits on `km` equal those of v: per bit j of
+// km, intersect with the columns whose bit j is v's bit j.
+__device__ __forceinline__ uint64_t col_match(uint32_t km, uint32_t v, uint32_t sc) {
+  constexpr uint64_t kBit[6] = {0xAAAAAAAAAAAAAAAAull, 0xCCCCCCCCCCCCCCCCull, 0xF0F0F0F0F0F0F0F0ull,
+                                0xFF00FF00FF00FF00ull, 0xFFFF0000FFFF0000ull, 0xFFFFFFFF00000000ull};
+  uint64_t m = sc >= 64 ? ~0ull : ((1ull << sc) - 1ull);
+#pragma unroll
+  for (uint32_t j = 0; j < 6; ++j)
+    if ((km >> j) & 1u) m &= ((v >> j) & 1u) ? kBit[j] : ~kBit[j];
+  return m;
+}
+
 // k-th (0-based) set bit of a 64-bit mask
 __device__ __forceinline__ uint32_t nth_bit64(uint64_t m, uint32_t k) {
   const uint32_t lo = (uint32_t)m, nlo = __popc(lo);
@@ -308,30 +320,45 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
       }
       __syncwarp();
       uint64_t tuples = 1;
-      for (uint32_t i = 0; i < sr && tuples <= P.enum_max; ++i) tuples *= (uint64_t)__popcll(misc->rmask[i]);
-      if (tuples <= P.enum_max && tuples <= cap) {
+      for (uint32_t i = 0; i < sr && tuples <= cap; ++i) tuples *= (uint64_t)__popcll(misc->rmask[i]);
+      if (tuples <= cap && tuples <= P.enum_max) {
         // every complete tuple is one LP, so the survivors (<= tuples) cannot
-        // exceed the cap: no counting pass.  Lane t walks tuples t, t+32, ...
-        // and keeps the consistent ones (the DFS prune of
-        // short_sketch.py:379-388 applied row by row)
+        // exceed the cap: no counting pass.  Depth-first walk straight from
+        // the hot masks: lane t takes the t-th hot column of row 0; at row i
+        // the consistent hot columns are hot_i & (columns whose bits on the
+        // already-fixed LP positions equal the walk's) -- the prune of
+        // short_sketch.py:379-388 as one 64-bit mask, no bucket tables
         const uint64_t full = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
-        for (uint32_t t = G.tid; t < (uint32_t)tuples; t += 32) {
-          uint32_t q = t;
-          uint64_t lp = 0, fixed = 0, acc = full;
-          bool ok = true;
-          for (uint32_t i = 0; i < sr; ++i) {
-            const uint64_t m = misc->rmask[i];
-            const uint32_t h = __popcll(m);
-            const uint32_t col = nth_bit64(m, q % h);
-            q /= h;
-            const uint64_t v = scatter_col(col, P.isb[i], P.ibn[i], P.w);
-            ok &= ((lp ^ v) & fixed & P.row_bits[i]) == 0;
-            lp |= v;
-            fixed |= P.row_bits[i];
-            acc &= sm[P.off_regs[i] + col];
+        const uint64_t hot0 = misc->rmask[0];
+        const uint32_t h0 = (uint32_t)__popcll(hot0);
+        uint64_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR], rem_st[SSPD_MAX_SR];
+        for (uint32_t t = G.tid; t < h0; t += 32) {
+          const uint32_t c0 = nth_bit64(hot0, t);
+          lp_st[0] = scatter_col(c0, P.isb[0], P.ibn[0], P.w);
+          and_st[0] = full & sm[P.off_regs[0] + c0];
+          uint32_t lvl = 1;
+          rem_st[1] = misc->rmask[1] & col_match(P.keymask[1], index_of(lp_st[0], P.isb[1], P.ibn[1], P.w), P.sc[1]);
+          while (lvl >= 1) {
+            const uint64_t rem = rem_st[lvl];
+            if (rem == 0) {
+              --lvl;
+              continue;
+            }
+            const uint32_t c = (uint32_t)__ffsll((long long)rem) - 1;
+            rem_st[lvl] = rem & (rem - 1);
+            const uint64_t nlp = lp_st[lvl - 1] | scatter_col(c, P.isb[lvl], P.ibn[lvl], P.w);
+            const uint64_t nand = and_st[lvl - 1] & sm[P.off_regs[lvl] + c];
+            if (lvl + 1 == sr) {
+              const uint32_t wgt = (uint32_t)__popcll(nand);
+              if (wgt >= 3) emit_candidate(P, nlp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
+              continue;
+            }
+            lp_st[lvl] = nlp;
+            and_st[lvl] = nand;
+            ++lvl;
+            rem_st[lvl] = misc->rmask[lvl] &
+                          col_match(P.keymask[lvl], index_of(nlp, P.isb[lvl], P.ibn[lvl], P.w), P.sc[lvl]);
           }
-          const uint32_t wgt = (uint32_t)__popcll(acc);
-          if (ok && wgt >= 3) emit_candidate(P, lp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
         }
         return;
       }
@@ -772,8 +799,9 @@ static int build_plan(const sspd_params& p, RestorePlan& P) {
       P.row_bits[i] = (uint32_t)row_mask(p.isb[i], p.ibn[i], p.lp_bits);
     }
     P.lane_enum = en ? 1u : 0u;
-    // tuples a warp enumerates before the bucket tables pay off (measured)
-    P.enum_max = 128;
+    // mask walk whenever the tuple bound allows it (<= cap); the knob caps
+    // it further for A/B against the bucket tables
+    P.enum_max = 0xFFFFFFFFu;
     if (const char* e = getenv("SSPD_RESTORE_ENUM_MAX")) P.enum_max = (uint32_t)atoi(e);
   }
   return SSPD_OK;
