@@ -1080,7 +1080,7 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   }
   const size_t segs = (C + kSeg - 1) / kSeg;
   // [ip | aux | ip_alt | aux_alt | z0 | keep | sort temp | compaction segs | hist, cursor | starts]
-  const size_t o_aux = vec, o_ipa = 2 * vec, o_auxa = 3 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;
+  const size_t o_aux = vec, o_ipa = 2 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;  // [3 vec, 4 vec): spare
   const size_t o_tmp = o_keep + ((C + 255) / 256) * 256;
   const size_t o_seg = o_tmp + ((sort_tmp + 255) / 256) * 256;
   const size_t o_hist = o_seg + ((4 * segs + 255) / 256) * 256;
