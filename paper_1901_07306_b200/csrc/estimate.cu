@@ -83,6 +83,36 @@ __device__ __forceinline__ uint64_t load_reg(const uint8_t* base, uint32_t idx, 
   }
 }
 
+// Shared-memory copy of the plan fields the warp path indexes by lane or by
+// walk depth: indexed constant-bank loads with lane-divergent indices are
+// serialised (ncu: ADU pipe 80 % busy), shared-memory loads are not.
+struct WarpTab {
+  uint64_t lane_src[32];  // seav_row_off[row] + lane_off of the lane's 8 bytes
+  uint32_t lane_sc[32];   // sc[row] (the SEA stride of the lane's row); 0 = idle lane
+  uint32_t lane_dst[32];  // off_regs[row] + lane_off (staging offset)
+  uint32_t isb[SSPD_MAX_SR], ibn[SSPD_MAX_SR], sc[SSPD_MAX_SR], keymask[SSPD_MAX_SR], off_regs[SSPD_MAX_SR];
+  uint32_t row_lane0[SSPD_MAX_SR];
+};
+
+__device__ void fill_warp_tab(const RestorePlan& P, WarpTab* T) {
+  const uint32_t t = threadIdx.x;
+  if (t < 32) {
+    const uint32_t row = P.lane_row[t];
+    const bool act = row < P.sr;
+    T->lane_src[t] = act ? P.seav_row_off[row] + P.lane_off[t] : 0;
+    T->lane_sc[t] = act ? P.sc[row] : 0u;
+    T->lane_dst[t] = act ? P.off_regs[row] + P.lane_off[t] : 0u;
+  } else if (t < 32 + P.sr) {
+    const uint32_t i = t - 32;
+    T->isb[i] = P.isb[i];
+    T->ibn[i] = P.ibn[i];
+    T->sc[i] = P.sc[i];
+    T->keymask[i] = P.keymask[i];
+    T->off_regs[i] = P.off_regs[i];
+    T->row_lane0[i] = P.row_lane0[i];
+  }
+}
+
 struct Misc {
   unsigned long long total;  // consistent complete tuples counted so far
   uint32_t abort;
@@ -278,7 +308,7 @@ template <bool kWarp>
 __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const RestorePlan& P, uint8_t* sm, uint32_t rp,
                                   uint32_t slot, uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
                                   uint64_t out_capacity, unsigned long long* out_count, uint8_t* overflow,
-                                  const Group<kWarp> G) {
+                                  const Group<kWarp> G, const WarpTab* T) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t sr = P.sr;
 
@@ -291,12 +321,10 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
     // the whole SEA in ONE independent 8-byte load per lane (instead of a
     // dependent round trip per row, which is what a restore co-running with
     // the L2-atomic-bound sliding scan waits on); hot = a byte of weight >= 3
-    const uint32_t row = P.lane_row[G.tid];
-    const bool act = row < sr;
+    const uint32_t lsc = T->lane_sc[G.tid];
+    const bool act = lsc != 0;
     uint64_t v = 0;
-    if (act)
-      v = __ldg(reinterpret_cast<const uint64_t*>(seav + P.seav_row_off[row] + (uint64_t)rp * P.sc[row] +
-                                                  P.lane_off[G.tid]));
+    if (act) v = __ldg(reinterpret_cast<const uint64_t*>(seav + T->lane_src[G.tid] + (uint64_t)rp * lsc));
     uint64_t c = v - ((v >> 1) & 0x5555555555555555ull);
     c = (c & 0x3333333333333333ull) + ((c >> 2) & 0x3333333333333333ull);
     c = (c + (c >> 4)) & 0x0F0F0F0F0F0F0F0Full;                      // per-byte popcounts (<= 8)
@@ -304,7 +332,7 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
     const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hot);
     for (uint32_t i = 0; i < sr; ++i)
       if ((hb & P.row_lanes[i]) == 0) return;
-    if (act) *reinterpret_cast<uint64_t*>(sm + P.off_regs[row] + P.lane_off[G.tid]) = v;
+    if (act) *reinterpret_cast<uint64_t*>(sm + T->lane_dst[G.tid]) = v;
     staged = true;
     if (P.lane_enum) {
       // per-row hot-column masks: lane l's 8 hot bits are bits lane_off..+7
@@ -314,8 +342,8 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
       __syncwarp();
       if (G.tid < sr) {
         uint64_t m = 0;
-        for (uint32_t j = 0; j < (P.sc[G.tid] >> 3); ++j)
-          m |= (uint64_t)misc->hmask[P.row_lane0[G.tid] + j] << (8 * j);
+        for (uint32_t j = 0; j < (T->sc[G.tid] >> 3); ++j)
+          m |= (uint64_t)misc->hmask[T->row_lane0[G.tid] + j] << (8 * j);
         misc->rmask[G.tid] = m;
       }
       __syncwarp();
@@ -334,10 +362,10 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
         uint64_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR], rem_st[SSPD_MAX_SR];
         for (uint32_t t = G.tid; t < h0; t += 32) {
           const uint32_t c0 = nth_bit64(hot0, t);
-          lp_st[0] = scatter_col(c0, P.isb[0], P.ibn[0], P.w);
-          and_st[0] = full & sm[P.off_regs[0] + c0];
+          lp_st[0] = scatter_col(c0, T->isb[0], T->ibn[0], P.w);
+          and_st[0] = full & sm[T->off_regs[0] + c0];
           uint32_t lvl = 1;
-          rem_st[1] = misc->rmask[1] & col_match(P.keymask[1], index_of(lp_st[0], P.isb[1], P.ibn[1], P.w), P.sc[1]);
+          rem_st[1] = misc->rmask[1] & col_match(T->keymask[1], index_of(lp_st[0], T->isb[1], T->ibn[1], P.w), T->sc[1]);
           while (lvl >= 1) {
             const uint64_t rem = rem_st[lvl];
             if (rem == 0) {
@@ -346,8 +374,8 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
             }
             const uint32_t c = (uint32_t)__ffsll((long long)rem) - 1;
             rem_st[lvl] = rem & (rem - 1);
-            const uint64_t nlp = lp_st[lvl - 1] | scatter_col(c, P.isb[lvl], P.ibn[lvl], P.w);
-            const uint64_t nand = and_st[lvl - 1] & sm[P.off_regs[lvl] + c];
+            const uint64_t nlp = lp_st[lvl - 1] | scatter_col(c, T->isb[lvl], T->ibn[lvl], P.w);
+            const uint64_t nand = and_st[lvl - 1] & sm[T->off_regs[lvl] + c];
             if (lvl + 1 == sr) {
               const uint32_t wgt = (uint32_t)__popcll(nand);
               if (wgt >= 3) emit_candidate(P, nlp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
@@ -357,7 +385,7 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
             and_st[lvl] = nand;
             ++lvl;
             rem_st[lvl] = misc->rmask[lvl] &
-                          col_match(P.keymask[lvl], index_of(nlp, P.isb[lvl], P.ibn[lvl], P.w), P.sc[lvl]);
+                          col_match(T->keymask[lvl], index_of(nlp, T->isb[lvl], T->ibn[lvl], P.w), T->sc[lvl]);
           }
         }
         return;
@@ -476,12 +504,17 @@ __global__ void __launch_bounds__(128) restore_warp_kernel(const uint8_t* __rest
                                                            uint32_t* out_aux, uint64_t out_capacity,
                                                            unsigned long long* out_count, uint8_t* overflow) {
   extern __shared__ __align__(16) uint8_t smw[];
+  __shared__ WarpTab tab;
+  if (P.lane_fast) {
+    fill_warp_tab(P, &tab);
+    __syncthreads();
+  }
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + warp;
   if (slot >= rp_count) return;
   const Group<true> G{threadIdx.x & 31u, 32u, 0u, 1u};
   restore_sea_group<true>(seav, P, smw + (size_t)warp * P.smem_bytes, rp_begin + slot, slot, cap, out_ip, out_aux,
-                          out_capacity, out_count, overflow, G);
+                          out_capacity, out_count, overflow, G, &tab);
 }
 
 __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict__ seav,
@@ -492,7 +525,7 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
   extern __shared__ __align__(16) uint8_t sm[];
   const Group<false> G{threadIdx.x, blockDim.x, threadIdx.x >> 5, blockDim.x >> 5};
   restore_sea_group<false>(seav, P, sm, rp_begin + blockIdx.x, blockIdx.x, cap, out_ip, out_aux, out_capacity,
-                           out_count, overflow, G);
+                           out_count, overflow, G, nullptr);
 }
 
 // ------------------------------------------------------------------ filter
