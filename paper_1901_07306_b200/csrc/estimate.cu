@@ -91,12 +91,13 @@ struct WarpTab {
   uint32_t lane_sc[32];   // sc[row] (the SEA stride of the lane's row); 0 = idle lane
   uint32_t lane_dst[32];  // off_regs[row] + lane_off (staging offset)
   uint32_t isb[SSPD_MAX_SR], ibn[SSPD_MAX_SR], sc[SSPD_MAX_SR], keymask[SSPD_MAX_SR], off_regs[SSPD_MAX_SR];
-  uint32_t row_lane0[SSPD_MAX_SR];
+  uint32_t off_bstart[SSPD_MAX_SR], off_cols[SSPD_MAX_SR], row_lane0[SSPD_MAX_SR];
 };
 
 __device__ void fill_warp_tab(const RestorePlan& P, WarpTab* T) {
   const uint32_t t = threadIdx.x;
   if (t < 32) {
+    if (!P.lane_fast) return;
     const uint32_t row = P.lane_row[t];
     const bool act = row < P.sr;
     T->lane_src[t] = act ? P.seav_row_off[row] + P.lane_off[t] : 0;
@@ -109,6 +110,8 @@ __device__ void fill_warp_tab(const RestorePlan& P, WarpTab* T) {
     T->sc[i] = P.sc[i];
     T->keymask[i] = P.keymask[i];
     T->off_regs[i] = P.off_regs[i];
+    T->off_bstart[i] = P.off_bstart[i];
+    T->off_cols[i] = P.off_cols[i];
     T->row_lane0[i] = P.row_lane0[i];
   }
 }
@@ -179,16 +182,16 @@ __device__ __forceinline__ uint32_t nth_bit64(uint64_t m, uint32_t k) {
 template <bool kEmit>
 __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uint64_t cap, uint32_t* out_ip,
                              uint32_t* out_aux, uint64_t out_capacity, unsigned long long* out_count,
-                             uint32_t gtid, uint32_t gsize) {
+                             uint32_t gtid, uint32_t gsize, const WarpTab* T) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t* pref0 = reinterpret_cast<const uint32_t*>(sm + P.off_pref0);
   const uint32_t npairs = misc->pairs;
   const uint32_t h0 = misc->hot[0];
   const uint64_t full_bits = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
   const uint32_t sr = P.sr, w = P.w;
-  const uint16_t* cols0 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[0]);
-  const uint16_t* cols1 = reinterpret_cast<const uint16_t*>(sm + P.off_cols[1]);
-  const uint32_t* b1 = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[1]);
+  const uint16_t* cols0 = reinterpret_cast<const uint16_t*>(sm + T->off_cols[0]);
+  const uint16_t* cols1 = reinterpret_cast<const uint16_t*>(sm + T->off_cols[1]);
+  const uint32_t* b1 = reinterpret_cast<const uint32_t*>(sm + T->off_bstart[1]);
 
   uint64_t since_flush = 0;
   volatile uint32_t* abort_flag = &misc->abort;
@@ -203,15 +206,15 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
     }
     const uint32_t j0 = lo;
     const uint32_t c0 = cols0[j0];
-    const uint64_t v0 = scatter_col(c0, P.isb[0], P.ibn[0], w);
-    const uint32_t key1 = pext32(index_of(v0, P.isb[1], P.ibn[1], w) & P.keymask[1], P.keymask[1]);
+    const uint64_t v0 = scatter_col(c0, T->isb[0], T->ibn[0], w);
+    const uint32_t key1 = pext32(index_of(v0, T->isb[1], T->ibn[1], w) & T->keymask[1], T->keymask[1]);
     const uint32_t c1 = cols1[b1[key1] + (t - pref0[j0])];
-    const uint64_t v1 = scatter_col(c1, P.isb[1], P.ibn[1], w);
+    const uint64_t v1 = scatter_col(c1, T->isb[1], T->ibn[1], w);
     uint64_t lp_stack[SSPD_MAX_SR];
     uint64_t and_stack[SSPD_MAX_SR];
     uint32_t lo_stack[SSPD_MAX_SR], hi_stack[SSPD_MAX_SR];
-    const uint64_t and01 = full_bits & load_reg(sm + P.off_regs[0], c0, P.reg_bytes) &
-                           load_reg(sm + P.off_regs[1], c1, P.reg_bytes);
+    const uint64_t and01 = full_bits & load_reg(sm + T->off_regs[0], c0, P.reg_bytes) &
+                           load_reg(sm + T->off_regs[1], c1, P.reg_bytes);
     const uint64_t lp01 = v0 | v1;
 
     auto leaf = [&](uint64_t lp, uint64_t acc_and) {
@@ -251,17 +254,17 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
     lp_stack[2] = lp01;
     and_stack[2] = and01;
     {
-      const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[2]);
-      const uint32_t key = pext32(index_of(lp01, P.isb[2], P.ibn[2], w) & P.keymask[2], P.keymask[2]);
+      const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + T->off_bstart[2]);
+      const uint32_t key = pext32(index_of(lp01, T->isb[2], T->ibn[2], w) & T->keymask[2], T->keymask[2]);
       lo_stack[2] = bs[key];
       hi_stack[2] = bs[key + 1];
     }
     while (true) {
       if (lo_stack[lvl] < hi_stack[lvl]) {
-        const uint16_t* cols = reinterpret_cast<const uint16_t*>(sm + P.off_cols[lvl]);
+        const uint16_t* cols = reinterpret_cast<const uint16_t*>(sm + T->off_cols[lvl]);
         const uint32_t c = cols[lo_stack[lvl]++];
-        const uint64_t nlp = lp_stack[lvl] | scatter_col(c, P.isb[lvl], P.ibn[lvl], w);
-        const uint64_t nand = and_stack[lvl] & load_reg(sm + P.off_regs[lvl], c, P.reg_bytes);
+        const uint64_t nlp = lp_stack[lvl] | scatter_col(c, T->isb[lvl], T->ibn[lvl], w);
+        const uint64_t nand = and_stack[lvl] & load_reg(sm + T->off_regs[lvl], c, P.reg_bytes);
         if (lvl + 1 == sr) {
           leaf(nlp, nand);
           if (!kEmit && *abort_flag) break;
@@ -269,9 +272,9 @@ __device__ void restore_walk(const RestorePlan& P, uint8_t* sm, uint32_t rp, uin
           ++lvl;
           lp_stack[lvl] = nlp;
           and_stack[lvl] = nand;
-          const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + P.off_bstart[lvl]);
+          const uint32_t* bs = reinterpret_cast<const uint32_t*>(sm + T->off_bstart[lvl]);
           const uint32_t key =
-              pext32(index_of(nlp, P.isb[lvl], P.ibn[lvl], w) & P.keymask[lvl], P.keymask[lvl]);
+              pext32(index_of(nlp, T->isb[lvl], T->ibn[lvl], w) & T->keymask[lvl], T->keymask[lvl]);
           lo_stack[lvl] = bs[key];
           hi_stack[lvl] = bs[key + 1];
         }
@@ -487,14 +490,14 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
   uint64_t bound = misc->pairs;
   for (uint32_t i = 2; i < sr && bound <= cap; ++i) bound *= misc->hot[i];
   if (bound > cap) {
-    restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
+    restore_walk<false>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size, T);
     G.sync();
     if (misc->total > cap) {
       if (G.tid == 0) overflow[slot] = 1;
       return;
     }
   }
-  restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size);
+  restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size, T);
 }
 
 // one SEA per warp, 4 warps per CTA, each warp with its own smem slice
@@ -505,10 +508,8 @@ __global__ void __launch_bounds__(128) restore_warp_kernel(const uint8_t* __rest
                                                            unsigned long long* out_count, uint8_t* overflow) {
   extern __shared__ __align__(16) uint8_t smw[];
   __shared__ WarpTab tab;
-  if (P.lane_fast) {
-    fill_warp_tab(P, &tab);
-    __syncthreads();
-  }
+  fill_warp_tab(P, &tab);
+  __syncthreads();
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + warp;
   if (slot >= rp_count) return;
@@ -523,9 +524,12 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
                                                       uint64_t out_capacity, unsigned long long* out_count,
                                                       uint8_t* overflow) {
   extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ WarpTab tab;
+  fill_warp_tab(P, &tab);
+  __syncthreads();
   const Group<false> G{threadIdx.x, blockDim.x, threadIdx.x >> 5, blockDim.x >> 5};
   restore_sea_group<false>(seav, P, sm, rp_begin + blockIdx.x, blockIdx.x, cap, out_ip, out_aux, out_capacity,
-                           out_count, overflow, G, nullptr);
+                           out_count, overflow, G, &tab);
 }
 
 // ------------------------------------------------------------------ filter
@@ -542,6 +546,9 @@ __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t cell_bytes = p.k >> 3;
   const uint64_t live = n_dev ? min(n, (uint64_t)*n_dev) : n;
+  // lane i (and i+32) owns row i: its seed is loaded once (a lane-indexed
+  // constant load is serialised across the warp's distinct addresses)
+  const uint64_t seed_a = lane < p.lr ? p.seed_lh[lane] : 0, seed_b = lane + 32 < p.lr ? p.seed_lh[lane + 32] : 0;
   for (uint64_t j = warp; j < n; j += nwarps) {
     if (j >= live) {
       if (lane == 0 && keep_out) keep_out[j] = 0;
@@ -549,9 +556,9 @@ __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__
     }
     const uint32_t ip = ips[j];
     // lane i (and i+32) hashes row i once; cells are broadcast by shuffle
-    const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, p.seed_lh[lane], p.div_lc)) * cell_bytes : 0;
+    const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, seed_a, p.div_lc)) * cell_bytes : 0;
     const uint64_t off_b =
-        lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, p.seed_lh[lane + 32], p.div_lc)) * cell_bytes : 0;
+        lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, seed_b, p.div_lc)) * cell_bytes : 0;
     uint32_t pop = 0;
     if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
       // 16-byte loads: lane l ANDs words 4l..4l+3 of each 128-word stripe
@@ -611,14 +618,15 @@ __global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   constexpr uint32_t kVec = 16 / sizeof(T);  // stamps per 16-byte load
+  const uint64_t seed_a = lane < p.lr ? p.seed_lh[lane] : 0, seed_b = lane + 32 < p.lr ? p.seed_lh[lane + 32] : 0;
   for (uint64_t j = warp; j < n; j += nwarps) {
     const uint32_t ip = ips[j];
     // lane i (and i+32) hashes row i once; cell bases are broadcast by shuffle
     const uint64_t base_a =
-        lane < p.lr ? p.slot_ldca_base + ((uint64_t)lane * p.lc + hash_range(ip, p.seed_lh[lane], p.div_lc)) * p.k : 0;
+        lane < p.lr ? p.slot_ldca_base + ((uint64_t)lane * p.lc + hash_range(ip, seed_a, p.div_lc)) * p.k : 0;
     const uint64_t base_b =
         lane + 32 < p.lr
-            ? p.slot_ldca_base + ((uint64_t)(lane + 32) * p.lc + hash_range(ip, p.seed_lh[lane + 32], p.div_lc)) * p.k
+            ? p.slot_ldca_base + ((uint64_t)(lane + 32) * p.lc + hash_range(ip, seed_b, p.div_lc)) * p.k
             : 0;
     uint32_t pop = 0;
     bool vec = (p.k % (32 * kVec)) == 0;
