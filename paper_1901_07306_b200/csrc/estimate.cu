@@ -1153,7 +1153,7 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
     const uint32_t smem = 4u * nb;
     if (smem > 48u * 1024u)
       cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const uint32_t grid = (uint32_t)std::min<size_t>(296, (C + 4095) / 4096);
+    const uint32_t grid = (uint32_t)std::min<size_t>(296, (C + 1023) / 1024);  // ~1 key per thread
     bucket_scatter_kernel<<<grid, 1024, smem, st>>>(ip, counts, C, hist, nb, hshift, cursor, starts, ipa);
     bucket_sort_kernel<<<(nb * 32 + 255) / 256, 256, 0, st>>>(ipa, starts, nb, ip, overflow + rp_count);
   } else {
