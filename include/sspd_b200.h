@@ -192,13 +192,16 @@ SSPD_API int sspd_ldca_fold(void* pool, uint32_t ts_bytes, const sspd_params* p,
  *       pointer may be NULL; 16-byte aligned, nbytes % 4 == 0);
  *   sspd_ldca_fold_ring = TimestampPool.touch_batch of the LDCA slots for the
  *       ring slices [slice_lo, slice_hi], newest slice winning (stamp =
- *       slice & 0xFFFF); slice_hi - slice_lo < ring_slots;
+ *       slice & 0xFFFF); slice e's bitmap starts at byte
+ *       (e % ring_slots) * slot_stride_bytes of `ring` (stride >= ldca_bytes,
+ *       a multiple of 4); slice_hi - slice_lo < ring_slots;
  *   sspd_ldca_suffix_or = in place, bitmap of slice e <- OR of slices
  *       e .. first_slice + count - 1 (the two-stack suffix pass at a block end). */
 SSPD_API int sspd_ldca_window_or(const uint32_t* cur, uint32_t* acc, const uint32_t* suffix, uint32_t* view,
                                  uint32_t* zero, uint64_t nbytes, void* stream);
 SSPD_API int sspd_ldca_fold_ring(void* pool, uint32_t ts_bytes, const sspd_params* p, const uint32_t* ring,
-                                 uint32_t ring_slots, uint64_t slice_lo, uint64_t slice_hi, void* stream);
+                                 uint64_t slot_stride_bytes, uint32_t ring_slots, uint64_t slice_lo,
+                                 uint64_t slice_hi, void* stream);
 SSPD_API int sspd_ldca_suffix_or(uint32_t* ring, uint32_t ring_slots, uint64_t nbytes, uint64_t first_slice,
                                  uint64_t count, void* stream);
 

@@ -114,7 +114,7 @@ _SIGS = {
                                              _VP]),
     "sspd_ldca_fold": (C.c_int, [_VP, _U32, _PP, _VP, _U64, _U64, _VP, _VP]),
     "sspd_ldca_window_or": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
-    "sspd_ldca_fold_ring": (C.c_int, [_VP, _U32, _PP, _VP, _U32, _U64, _U64, _VP]),
+    "sspd_ldca_fold_ring": (C.c_int, [_VP, _U32, _PP, _VP, _U64, _U32, _U64, _U64, _VP]),
     "sspd_ldca_suffix_or": (C.c_int, [_VP, _U32, _U64, _U64, _U64, _VP]),
     "sspd_pool_ages": (C.c_int, [_VP, _U64, _U32, _U64, _VP, _VP]),
     "sspd_restore": (C.c_int, [_VP, _PP, _U32, _U32, _U64, _VP, _VP, _U64, _VP, _VP, _VP]),

@@ -671,9 +671,10 @@ __global__ void __launch_bounds__(256) filter_sliding_kernel(const T* __restrict
 }
 
 // Stable compaction of the kept candidates.  Segment b of kSeg entries is
-// owned by block b: pass 1 counts each segment, pass 2 sums the preceding
-// counts (<= 1024 of them) and scatters its segment in order with a
-// ballot-based block scan.
+// owned by block b: pass 1 counts each segment, pass 2 gets the number of
+// kept entries before it -- by summing the preceding counts when there are
+// at most kSegDirect segments, else from one exclusive scan of the counts --
+// and scatters its segment in order with a ballot-based block scan.
 constexpr uint32_t kSeg = 1024;  // one 1,024-thread pass per segment (many blocks in flight)
 
 __device__ void compact_segment(const uint32_t* __restrict__ ip, const uint32_t* __restrict__ z0,
@@ -727,25 +728,77 @@ __global__ void __launch_bounds__(1024) compact_count_kernel(const uint8_t* __re
   }
 }
 
+// Exclusive prefix of the segment counts (one 1,024-thread block; thread t
+// owns a contiguous run of ceil(segs/1024) counts): used when there are more
+// than kSegDirect segments, so the scatter reads its base in O(1) instead of
+// summing every earlier segment (O(segs^2) work over the grid).
+constexpr uint64_t kSegDirect = 1024;
+
+__global__ void __launch_bounds__(1024) compact_seg_scan_kernel(const uint32_t* __restrict__ seg_counts,
+                                                                uint64_t segs, uint32_t* __restrict__ seg_pre) {
+  __shared__ uint32_t ws[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t per = (segs + 1023) / 1024;
+  const uint64_t lo = min(segs, tid * per), hi = min(segs, lo + per);
+  uint32_t sum = 0;
+  for (uint64_t b = lo; b < hi; ++b) sum += seg_counts[b];
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) ws[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = ws[lane];
+    uint32_t wi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= (uint32_t)o) wi += y;
+    }
+    ws[lane] = wi - v;
+  }
+  __syncthreads();
+  uint32_t run = ws[wid] + incl - sum;
+  for (uint64_t b = lo; b < hi; ++b) {
+    const uint32_t c = seg_counts[b];
+    seg_pre[b] = run;
+    run += c;
+  }
+}
+
+// kPre: seg_pre holds the exclusive prefix (compact_seg_scan_kernel); else the
+// block sums the counts before it (<= kSegDirect of them).
+template <bool kPre>
 __global__ void __launch_bounds__(1024) compact_scatter_kernel(const uint32_t* __restrict__ ip,
                                                                const uint32_t* __restrict__ z0,
                                                                const uint8_t* __restrict__ keep, uint64_t n,
                                                                const uint32_t* __restrict__ seg_counts,
+                                                               const uint32_t* __restrict__ seg_pre,
                                                                uint32_t* ip_out, uint32_t* z0_out,
                                                                unsigned long long* out_count) {
   __shared__ unsigned long long base_s;
   __shared__ uint32_t ws[32];
-  uint32_t pre = 0;
-  for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += seg_counts[b];
+  if (kPre) {
+    if (threadIdx.x == 0) {
+      base_s = seg_pre[blockIdx.x];
+      if (blockIdx.x == gridDim.x - 1) *out_count = base_s + seg_counts[blockIdx.x];
+    }
+  } else {
+    uint32_t pre = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += seg_counts[b];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = pre;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += ws[w];
-    base_s = t;
-    if (blockIdx.x == gridDim.x - 1) *out_count = t + seg_counts[blockIdx.x];
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = pre;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += ws[w];
+      base_s = t;
+      if (blockIdx.x == gridDim.x - 1) *out_count = t + seg_counts[blockIdx.x];
+    }
   }
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * kSeg, hi = min(n, lo + kSeg);
@@ -1065,7 +1118,8 @@ extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, cons
   if (!out_count) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t segs = (n + kSeg - 1) / kSeg;
-  const size_t need = 4 * (segs ? segs : 1);
+  // [seg counts | exclusive prefix (more than kSegDirect segments only)]
+  const size_t need = 4 * (segs ? segs : 1) * (segs > kSegDirect ? 2 : 1);
   if (!scratch) {
     if (scratch_bytes) {  // size query
       *scratch_bytes = need;
@@ -1079,7 +1133,15 @@ extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, cons
                                                                                                  : SSPD_ERR_CUDA;
   uint32_t* seg_counts = static_cast<uint32_t*>(scratch);
   compact_count_kernel<<<(unsigned)segs, 1024, 0, st>>>(keep, n, seg_counts);
-  compact_scatter_kernel<<<(unsigned)segs, 1024, 0, st>>>(ip, z0, keep, n, seg_counts, ip_out, z0_out, out_count);
+  if (segs > kSegDirect) {
+    uint32_t* seg_pre = seg_counts + segs;
+    compact_seg_scan_kernel<<<1, 1024, 0, st>>>(seg_counts, segs, seg_pre);
+    compact_scatter_kernel<true><<<(unsigned)segs, 1024, 0, st>>>(ip, z0, keep, n, seg_counts, seg_pre, ip_out,
+                                                                  z0_out, out_count);
+  } else {
+    compact_scatter_kernel<false><<<(unsigned)segs, 1024, 0, st>>>(ip, z0, keep, n, seg_counts, nullptr, ip_out,
+                                                                   z0_out, out_count);
+  }
   return check_launch();
 }
 
@@ -1124,7 +1186,8 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   const size_t o_aux = vec, o_ipa = 2 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;  // [3 vec, 4 vec): spare
   const size_t o_tmp = o_keep + ((C + 255) / 256) * 256;
   const size_t o_seg = o_tmp + ((sort_tmp + 255) / 256) * 256;
-  const size_t o_hist = o_seg + ((4 * segs + 255) / 256) * 256;
+  const size_t seg_bytes = 4 * segs * (segs > kSegDirect ? 2 : 1);  // sspd_compact_reports scratch
+  const size_t o_hist = o_seg + ((seg_bytes + 255) / 256) * 256;
   const size_t o_start = o_hist + 8ull * 16384;
   const size_t need = o_start + 4ull * (16384 + 1) + 256;
   if (!scratch) {
@@ -1167,7 +1230,7 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   }
   const int grid = grid_for(filter_kernel, 256, C * 32);
   filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);
-  size_t cb = 4 * segs;
+  size_t cb = seg_bytes;
   rc = sspd_compact_reports(sorted, z0, keep, C, out_ip, out_z0, counts + 1, s8 + o_seg, &cb, stream);
   if (rc) return rc;
   return check_launch();

@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(256) ldca_window_or_kernel(const uint32_t* __r
 // 32 have been seen.
 __global__ void __launch_bounds__(256) ldca_fold_ring_kernel(uint16_t* __restrict__ pool, uint64_t base,
                                                              uint64_t nwords, const uint32_t* __restrict__ ring,
-                                                             uint32_t ring_slots, uint64_t lo, uint64_t hi) {
+                                                             uint64_t slot_words, uint32_t ring_slots, uint64_t lo,
+                                                             uint64_t hi) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t slot_hi = (uint32_t)(hi % ring_slots);
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) {
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(256) ldca_fold_ring_kernel(uint16_t* __restric
     bool loaded = false;
     uint32_t slot = slot_hi;
     for (uint64_t e = hi + 1; e-- > lo && seen != 0xFFFFFFFFu;) {
-      const uint32_t d = __ldcg(ring + (uint64_t)slot * nwords + q);
+      const uint32_t d = __ldcg(ring + (uint64_t)slot * slot_words + q);
       slot = slot == 0 ? ring_slots - 1 : slot - 1;
       const uint32_t m = d & ~seen;
       if (!m) continue;
@@ -513,20 +514,24 @@ extern "C" int sspd_ldca_window_or(const uint32_t* cur, uint32_t* acc, const uin
 }
 
 extern "C" int sspd_ldca_fold_ring(void* pool, uint32_t ts_bytes, const sspd_params* p, const uint32_t* ring,
-                                   uint32_t ring_slots, uint64_t slice_lo, uint64_t slice_hi, void* stream) {
+                                   uint64_t slot_stride_bytes, uint32_t ring_slots, uint64_t slice_lo,
+                                   uint64_t slice_hi, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
   if (!pool || !ring || ring_slots == 0) return SSPD_ERR_DATA;
   if (ts_bytes != 2 || (p->ldca_bytes & 3u) || (p->slot_ldca_base & 7u) || (reinterpret_cast<uintptr_t>(pool) & 15u) ||
       (reinterpret_cast<uintptr_t>(ring) & 3u))
     return SSPD_ERR_CONFIG;
+  // consecutive slices' bitmaps are slot_stride_bytes apart (>= the LDCA
+  // bytes, a multiple of 4: the Python ring pads them to 16 B)
+  if ((slot_stride_bytes & 3u) || slot_stride_bytes < p->ldca_bytes) return SSPD_ERR_CONFIG;
   if (slice_hi < slice_lo) return SSPD_OK;
   if (slice_hi - slice_lo >= ring_slots) return SSPD_ERR_DATA;  // the ring holds R slices at most
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t nwords = p->ldca_bytes >> 2;
   const int grid = grid_for(ldca_fold_ring_kernel, 256, nwords);
-  ldca_fold_ring_kernel<<<grid, 256, 0, st>>>((uint16_t*)pool, p->slot_ldca_base, nwords, ring, ring_slots, slice_lo,
-                                              slice_hi);
+  ldca_fold_ring_kernel<<<grid, 256, 0, st>>>((uint16_t*)pool, p->slot_ldca_base, nwords, ring,
+                                              slot_stride_bytes >> 2, ring_slots, slice_lo, slice_hi);
   return check_launch();
 }
 

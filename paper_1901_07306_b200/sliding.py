@@ -280,7 +280,7 @@ class _DeferredLdca:
 
         if self.ring is not None:
             call("sspd_ldca_fold_ring", pool._buf.data_ptr(), pool.ts_bytes, self.params, self.ring.data_ptr(),
-                 self.slots, self.fold_lo, self.cur, stream_ptr())
+                 self.stride, self.slots, self.fold_lo, self.cur, stream_ptr())
             self.fold_lo = self.cur  # the current slice may gather more bits: folded again next time
             self.pending = False
             return False

@@ -222,12 +222,13 @@ class DeviceFinalize:
         self.list_ref = None  # weakref to the ReportList that still has to fetch its arrays
         self._launch(max(1024, seav._cand_cap))
 
-    def _enqueue(self, cap: int, out, h_tail):
+    def _enqueue(self, cap: int, out, h_tail, table=None):
         """sspd_finalize into `out` + the pinned copy of its counts/flags."""
         from ._device import call, stream_ptr
 
         seav = self.seav
-        table = device_keep_table(self.k, self.cutoff)
+        if table is None:
+            table = device_keep_table(self.k, self.cutoff)
         base = out.data_ptr()
         need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
         scratch = seav._scratch(need)
@@ -249,23 +250,33 @@ class DeviceFinalize:
         if self.graphs is not None:
             # per view set: the whole finalize (~12 launches, memsets and the
             # D2H copy of the counts) captured once per capacity / sort mode
-            # and replayed as ONE graph launch; buffers belong to the graph
-            key = (cap, seav._radix_sort, self.ldca.data_ptr(), self.cutoff, seav.restore_cap)
-            g = self.graphs.get(key)
-            if g is None:
+            # and replayed as ONE graph launch; buffers belong to the graph.
+            # Only the newest graph is kept (a new capacity, sort mode or
+            # scratch buffer replaces it: the old one may hold freed scratch
+            # pointers).  The keep table is a device INPUT of the graph: the
+            # view set owns one (k+1)-byte buffer, refreshed on the stream
+            # when beta*theta changes, so the cutoff is not part of the key.
+            need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
+            scratch = seav._scratch(need)  # allocated outside the capture
+            key = (cap, seav._radix_sort, self.ldca.data_ptr(), seav.restore_cap, scratch.data_ptr(), self.k)
+            keep = self.graphs.get("keep")
+            if keep is None or keep[0].numel() != self.k + 1:
+                keep = self.graphs["keep"] = [torch.empty(self.k + 1, dtype=torch.uint8, device=dev), None]
+            g = self.graphs.get("graph")
+            if g is None or g[0] != key:
+                self.graphs.pop("graph", None)
                 out = torch.empty(shape, dtype=torch.int32, device=dev)
                 h_tail = torch.empty(4 + nflag_words, dtype=torch.int32, pin_memory=True)
-                # allocations outside the capture: scratch size, scratch, keep table
-                need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
-                seav._scratch(need)
-                device_keep_table(self.k, self.cutoff)
                 graph = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(graph, stream=self.stream, capture_error_mode="thread_local"):
-                    self._enqueue(cap, out, h_tail)
-                g = self.graphs[key] = (graph, out, h_tail)
-            graph, self.out, self.h_tail = g
+                    self._enqueue(cap, out, h_tail, table=keep[0])
+                g = self.graphs["graph"] = (key, graph, out, h_tail)
+            _, graph, self.out, self.h_tail = g
             self.shared = True
             with torch.cuda.stream(self.stream):
+                if keep[1] != self.cutoff:  # stream-ordered after every earlier replay's reads
+                    keep[0].copy_(device_keep_table(self.k, self.cutoff), non_blocking=True)
+                    keep[1] = self.cutoff
                 graph.replay()
                 self.event = torch.cuda.Event()
                 self.event.record(self.stream)

@@ -240,9 +240,10 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case):
     assert st.ldca.payload_bytes() == ldca.tobytes()
 
 
-@pytest.mark.parametrize("n", [1, 1000, 8192, 8193, 100_003])
+@pytest.mark.parametrize("n", [1, 1000, 8192, 8193, 100_003, 1024 * 1024 + 1, 3_000_017])
 def test_compaction_is_stable(cuda, n):
-    """sspd_compact_reports (multi-segment and single-CTA forms) keeps order."""
+    """sspd_compact_reports (multi-segment and single-CTA forms) keeps order;
+    above 1,024 segments the multi-segment form scans the segment counts."""
     import ctypes
 
     import torch

@@ -464,16 +464,20 @@ def test_deferred_ldca_stamps_equal_direct_stamps(cuda):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("async_detect", [False, True])
-def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect):
+@pytest.mark.parametrize("geom", [(4096, 4, 256), (64, 3, 37)], ids=["ldca16B", "ldca_pad8"])
+def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom):
     """Ring mode of the deferred LDCA stamps (the LDCA view as a two-stack
     sliding-window OR of per-slice bitmaps, stamps folded lazily) against
     direct u16 stores over 2.7 windows from a pristine pool: detect at every
     slide across two block ends (suffix passes) with expiring slots, pool
     reads mid-block, a write around the detector (restart: stamps-based view
-    for one block, then the ring again), and reset."""
+    for one block, then the ring again), and reset.  `ldca_pad8`: 888 LDCA
+    bytes, so the ring pads each slice's bitmap to 896 B (the fold must step
+    by the padded stride, not the LDCA size)."""
     from paper_1901_07306_b200 import DetectorParams, SlidingDetector
 
-    params = DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5)
+    k, lr, lc = geom
+    params = DetectorParams(theta=256, r=8, k=k, lr=lr, lc=lc, design_n=2e5)
     w = 129
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
@@ -481,6 +485,7 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect):
         b = SlidingDetector(params, window_slices=w)
     b.defer_ldca_stamps = False
     assert a._deferred().ring is not None and a._deferred().valid()
+    assert (a._deferred().stride == a._params.ldca_bytes) == (a._params.ldca_bytes % 16 == 0)
     rng = np.random.default_rng(7)
     heavy = rng.integers(0, 2**32, size=3, dtype=np.uint64)
     base = a.layout.ldca_base
@@ -553,3 +558,38 @@ def test_detect_async_lists_outlive_their_view_set(cuda):
         b.advance_slice()
     assert {s: rep_list(x) for s, x in held.items()} == {s: want[s] for s in held}
     assert sum(len(want[s]) for s in held) > 0
+
+
+@pytest.mark.gpu
+def test_detect_async_graph_cache_varying_beta(cuda):
+    """detect_async with beta changing from slide to slide: each view set
+    keeps ONE finalize graph (the keep table is a device input refreshed on
+    the stream, not part of the graph key), and every list equals the
+    synchronous detect(beta) of a twin detector."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    params = DetectorParams(theta=256, r=12, k=4096, lr=4, lc=256, design_n=2e5)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = SlidingDetector(params, window_slices=8)
+        b = SlidingDetector(params, window_slices=8)
+    rng = np.random.default_rng(11)
+    heavy = rng.integers(0, 2**32, size=6, dtype=np.uint64)
+    betas = [0.8, 0.3, 1.5, 0.8, 0.05]
+    pend = []
+    for s in range(25):
+        n = int(rng.integers(5_000, 30_000))
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        hips[: n // 2] = heavy[rng.integers(0, 6, size=n // 2)]
+        a.observe_batch(hips, oips)
+        b.observe_batch(hips, oips)
+        beta = betas[s % len(betas)]
+        pend.append((s, a.detect_async(beta), rep_list(b.detect(beta))))
+        a.advance_slice()
+        b.advance_slice()
+    for s, x, want in pend:
+        assert rep_list(x) == want, s
+    assert sum(len(w) for _, _, w in pend) > 0
+    for vset in a._async["sets"]:
+        assert vset is not None and set(vset[3]) <= {"graph", "keep"}
