@@ -104,18 +104,25 @@ SSPD_API int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, uint
                        const sspd_params* p, uint8_t* seav, uint8_t* ldca,
                        void* stream);
 
-/* ---- K1p partitioned scan (same result as sspd_scan_discrete) -----------
- * The LDCA is partitioned across the SMs' shared memory for the duration of
- * the launch (one persistent CTA per SM, cooperative launch); updates are
- * routed through per-partition buckets in `scratch` (size from
- * sspd_scan_partitioned_scratch(p, chunk)).  Returns SSPD_ERR_CONFIG when the
- * LDCA does not fit in shared memory (use sspd_scan_discrete), and
- * SSPD_ERR_CAPACITY when scratch is too small.  ldca must be non-NULL. */
+/* ---- K1b / K1p partitioned scan (same result as sspd_scan_discrete) -----
+ * Replaces the same reference call as sspd_scan_discrete
+ * (window_detector.py:100-103).  The LDCA is partitioned across the SMs'
+ * shared memory for the duration of the launch (one persistent CTA per SM,
+ * cooperative launch); updates are routed through per-partition buckets in
+ * `scratch` (size from sspd_scan_partitioned_scratch(p, chunk)).  K1b cuts
+ * the LDCA along its b axis (one 16-byte entry per packet; LR = 8, k and lc
+ * powers of two) and is used whenever it applies; K1p cuts it into word
+ * ranges (any geometry whose LDCA fits).  sspd_scan_partitioned_variant
+ * tells which one runs: 2 = K1b, 1 = K1p, 0 = neither.  Returns
+ * SSPD_ERR_CONFIG when the LDCA does not fit in shared memory (use
+ * sspd_scan_discrete), and SSPD_ERR_CAPACITY when scratch is too small.
+ * ldca must be non-NULL. */
 SSPD_API int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                    const sspd_params* p, uint8_t* seav, uint8_t* ldca,
                                    void* scratch, uint64_t scratch_bytes, uint64_t chunk,
                                    void* stream);
 SSPD_API uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t chunk);
+SSPD_API int sspd_scan_partitioned_variant(const sspd_params* p, uint64_t chunk);
 
 /* ---- K2 sliding scan ---------------------------------------------------
  * Replaces SlidingDetector.observe_batch (sliding.py:156-185) with

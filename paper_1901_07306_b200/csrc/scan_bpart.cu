@@ -1,0 +1,481 @@
+// K1b: the partitioned scan with the LDCA cut along its b axis.
+//
+// Same result as K1 (scan.cu) and K1p (scan_smem.cu): bit (i*lc + c_i)*k + b
+// of the LDCA with c_i = LH_i(hip) % lc and b = H3(oip) % k
+// (long_sketch.py:125-135), plus the SEAV update of short_sketch.py:300-318.
+//
+// Like K1p, the LDCA lives in the SMs' shared memory for the whole launch
+// (one persistent 1,024-thread CTA per SM, cooperative launch, one grid
+// barrier per chunk, double-buffered buckets in L2).  The difference is the
+// cut.  K1p gives partition q a contiguous word range, so the LR = 8 bits of
+// one packet land in 8 different partitions: 8 staged u32 updates, 8 shared
+// atomicAdd slot reservations and 32 B of bucket traffic per packet.  K1b
+// gives partition q the b range [q*bw, (q+1)*bw) of EVERY cell
+// (bw = k / P bits, P = 128 partitions at k = 8192: 64 KB each).  All LR bits
+// of a packet share its b, so the packet goes to exactly ONE partition
+// q = b / bw as one 16-byte entry:
+//
+//   eight u16 halves, half_i = c_i << HB | (b % bw) >> 5   (HB = log2(bw/32))
+//   half_0 additionally carries b & 31 in bits [log2(lc)+HB, +5)
+//
+// which the owner of q turns into 8 shared-memory atomicOr (word
+// i*(lc << HB) + half_i of its partition, bit b & 31).  Per packet: one
+// shared atomicAdd instead of 8, one 16-byte staging store instead of 8
+// scalar ones, 16 B of bucket writes + 16 B of reads instead of 32 + 32.
+//
+// Anything that does not fit (a destination's staging row or bucket region
+// full, e.g. one opposite IP sending a large share of the window) is applied
+// as direct L2 `red.or` on the global LDCA -- exact, because OR is
+// commutative and idempotent.  SEAV updates (0.78 % of packets at tau = 7)
+// are queued per tile and applied by all lanes as direct reds (as K1p).
+#include <algorithm>
+#include <cooperative_groups.h>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include "sspd_common.cuh"
+#include "launch.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sspd {
+namespace bpart {
+
+constexpr uint32_t kThreads = 1024;
+constexpr uint32_t kPkt = 4;  // packets per thread per tile (one uint4 of hips + oips)
+constexpr uint32_t kTile = kThreads * kPkt;
+constexpr uint32_t kLR = 8;
+constexpr uint32_t kSeavQueue = 128;  // sampled packets per tile parity
+
+struct Plan {
+  uint32_t nparts;       // partitions = consumer CTAs 0 .. nparts-1 (power of two)
+  uint32_t nsrc;         // producers = gridDim.x (>= nparts)
+  uint32_t bshift;       // log2(bw): partition of b = b >> bshift
+  uint32_t row_words;    // lc << HB: words of one LDCA row inside a partition
+  uint32_t part_words;   // kLR * row_words
+  uint32_t lowm;         // mask of half 0 without the bit position
+  uint32_t bsh_shift;    // log2(lc) + HB: where half 0 keeps b & 31
+  uint32_t stage_slots;  // 16-B entries per destination per tile
+  uint32_t region_cap;   // entries per (src, dst) region per chunk
+  uint32_t w_owner, w_other;  // producer slice weights (owners vs pure producers)
+  uint64_t chunk;        // packets per chunk
+  uint64_t n;            // packets
+  uint4* buckets;        // [2][dst][src][region_cap]
+  uint32_t* counts;      // [2][dst][src]
+  uint32_t k_mask, lc_mask, log2k, lc;
+  uint32_t kw;           // k / 32: words per cell in the global LDCA
+  uint32_t s_lo[10], s_hg[10];  // split seeds (mix64_lo_split): H3, H1, LH0..7
+  uint32_t vec_ok;       // hips/oips 16-byte aligned and chunk % 4 == 0
+  uint32_t qstride;      // nsrc * region_cap: bucket entries per destination
+  uint32_t gshift;       // log2 of the flush group (threads per destination)
+  uint32_t tau_mask;
+};
+
+__device__ __forceinline__ void red_or_g(uint32_t* addr, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+// SEAV update of one sampled packet (short_sketch.py:300-318): SR direct reds.
+__device__ __forceinline__ void seav_update(const sspd_params& p, uint32_t hip, uint32_t oip, uint32_t* seav) {
+  const uint32_t sbit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+  const uint64_t rp = hip & ((1u << p.r) - 1u);
+  const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+    const uint64_t abs_bit = (p.seav_row_off[i] + (rp * p.sc[i] + col) * p.reg_bytes) * 8 + sbit;
+    red_or_g(seav + (abs_bit >> 5), 1u << (abs_bit & 31));
+  }
+}
+__device__ __noinline__ void seav_update_ool(const sspd_params& p, uint32_t hip, uint32_t oip, uint32_t* seav) {
+  seav_update(p, hip, oip, seav);
+}
+
+// Staging row full (rare): the packet's LR bits as direct L2 reds (exact).
+__device__ __noinline__ void direct_packet(const Plan& P, uint32_t hip, uint32_t b, uint32_t* ldca) {
+  for (uint32_t i = 0; i < kLR; ++i) {
+    const uint32_t c = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
+    const uint32_t bit = ((i * P.lc + c) << P.log2k) | b;
+    red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
+  }
+}
+
+// Bucket region full (rare): decode a staged entry of partition q back to
+// its LR bits and apply them as direct L2 reds (exact).
+template <int HB>
+__device__ __noinline__ void direct_entry(const Plan& P, uint32_t q, uint4 e, uint32_t* ldca) {
+  const uint32_t bsh = (e.x >> P.bsh_shift) & 31u;
+  const uint32_t h[kLR] = {e.x & P.lowm, e.x >> 16, e.y & 0xFFFFu, e.y >> 16,
+                           e.z & 0xFFFFu, e.z >> 16, e.w & 0xFFFFu, e.w >> 16};
+  for (uint32_t i = 0; i < kLR; ++i) {
+    const uint32_t c = h[i] >> HB;
+    const uint32_t b = (q << P.bshift) | ((h[i] & ((1u << HB) - 1u)) << 5) | bsh;
+    const uint32_t bit = ((i * P.lc + c) << P.log2k) | b;
+    red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
+  }
+}
+
+// Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
+// take w_other/w_owner as much as owners; boundaries are 4-aligned.
+__device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint64_t c1, uint32_t s) {
+  if (s >= P.nsrc) return c1;
+  const uint64_t tw = (uint64_t)P.nparts * P.w_owner + (uint64_t)(P.nsrc - P.nparts) * P.w_other;
+  const uint64_t cw =
+      (uint64_t)min(s, P.nparts) * P.w_owner + (uint64_t)(s > P.nparts ? s - P.nparts : 0) * P.w_other;
+  const uint64_t off = (((c1 - c0) * cw) / tw) & ~3ull;
+  return min(c1, c0 + off);
+}
+
+// Shared memory: [part_words | nparts*stage_slots uint4 staging | nparts cnt |
+//                 nparts cursor | 4 sq_cnt | 2*kSeavQueue (hip, oip)]
+template <bool kSeav, int HB>
+__global__ void __launch_bounds__(kThreads, 1)
+    scan_bpart_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
+                      const __grid_constant__ sspd_params p, const __grid_constant__ Plan P, uint32_t* seav,
+                      uint32_t* ldca) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* part = smem;
+  uint4* stage = reinterpret_cast<uint4*>(smem + P.part_words);  // part_words % 4 == 0
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
+  uint32_t* cursor = cnt + P.nparts;
+  uint32_t* sq_cnt = cursor + P.nparts;                     // [2] (+2 pad)
+  uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [2][kSeavQueue]
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t self = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = kThreads >> 5;
+  const uint32_t np = P.nparts, ns = P.nsrc;
+  const bool owner = self < np;
+  constexpr uint32_t kHMask = (1u << HB) - 1u;
+
+  for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
+  for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = cursor[i] = 0;
+  if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+  __syncthreads();
+
+  const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
+  for (uint64_t t = 0; t <= nchunks; ++t) {
+    // ---------------- consume chunk t-1 into the shared partition --------
+    if (t >= 1 && owner) {
+      const uint32_t bb = (uint32_t)((t - 1) & 1);
+      const uint32_t* cnts = P.counts + ((size_t)bb * np + self) * ns;
+      const uint4* regions = P.buckets + ((size_t)bb * np + self) * (size_t)P.qstride;
+      const uint32_t rw = P.row_words, lowm = P.lowm, bss = P.bsh_shift;
+      // warp w drains sources w, w+W, ...: lane j holds the run length of
+      // source w+W*j, fetched at once so no region waits on its count
+      const uint32_t my_src = warp + nwarps * lane;
+      const uint32_t my_cnt = my_src < ns ? min(__ldcg(cnts + my_src), P.region_cap) : 0u;
+      for (uint32_t src = warp, j = 0; src < ns; src += nwarps, ++j) {
+        const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
+        const uint4* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
+        for (uint32_t j0 = lane; j0 < m; j0 += 128) {  // 4 independent 16-B loads in flight per lane
+          uint4 u[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (j0 + 32 * g < m) u[g] = __ldcg(reg + j0 + 32 * g);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (j0 + 32 * g < m) {
+              const uint4 e = u[g];
+              const uint32_t bit = 1u << ((e.x >> bss) & 31u);
+              atomicOr(part + (e.x & lowm), bit);
+              atomicOr(part + rw + (e.x >> 16), bit);
+              atomicOr(part + 2 * rw + (e.y & 0xFFFFu), bit);
+              atomicOr(part + 3 * rw + (e.y >> 16), bit);
+              atomicOr(part + 4 * rw + (e.z & 0xFFFFu), bit);
+              atomicOr(part + 5 * rw + (e.z >> 16), bit);
+              atomicOr(part + 6 * rw + (e.w & 0xFFFFu), bit);
+              atomicOr(part + 7 * rw + (e.w >> 16), bit);
+            }
+          }
+        }
+        // the region is dead once read: drop its L2 lines without write-back
+        // so the bucket exchange stays on chip
+        __syncwarp();
+        for (uint32_t line = lane; line * 8 < m; line += 32)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(reg + line * 8) : "memory");
+      }
+    }
+    // ---------------- produce chunk t ------------------------------------
+    if (t < nchunks) {
+      const uint32_t bb = (uint32_t)(t & 1);
+      const uint64_t c0 = t * P.chunk;
+      const uint64_t c1 = min(P.n, c0 + P.chunk);
+      const uint64_t lo = slice_start(P, c0, c1, self);
+      const uint64_t hi = slice_start(P, c0, c1, self + 1);
+      // thread tid owns packets base + 4 tid + e, fetched one tile ahead
+      // with one 16-byte streaming load per array when aligned
+      auto fetch = [&](uint64_t first, uint32_t* h, uint32_t* o) {
+        if (P.vec_ok && first + kPkt <= hi) {
+          const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(hips + first));
+          const uint4 ov = __ldcs(reinterpret_cast<const uint4*>(oips + first));
+          h[0] = hv.x, h[1] = hv.y, h[2] = hv.z, h[3] = hv.w;
+          o[0] = ov.x, o[1] = ov.y, o[2] = ov.z, o[3] = ov.w;
+        } else {
+#pragma unroll
+          for (uint32_t e = 0; e < kPkt; ++e) {
+            h[e] = first + e < hi ? __ldcs(hips + first + e) : 0u;
+            o[e] = first + e < hi ? __ldcs(oips + first + e) : 0u;
+          }
+        }
+      };
+      uint32_t nh[kPkt], no[kPkt];
+      fetch(lo + (uint64_t)tid * kPkt, nh, no);
+      uint32_t par = 0;  // tile parity: selects the sampled-packet queue
+      for (uint64_t base = lo; base < hi; base += kTile, par ^= 1u) {
+        uint32_t ch[kPkt], co[kPkt];
+#pragma unroll
+        for (uint32_t e = 0; e < kPkt; ++e) {
+          ch[e] = nh[e];
+          co[e] = no[e];
+        }
+        fetch(base + kTile + (uint64_t)tid * kPkt, nh, no);
+#pragma unroll
+        for (uint32_t e = 0; e < kPkt; ++e) {
+          const uint64_t j = base + (uint64_t)tid * kPkt + e;
+          const uint32_t hip = ch[e], oip = co[e];
+          if (j < hi) {
+            const uint32_t b = mix64_lo_split(oip, P.s_lo[0], P.s_hg[0]) & P.k_mask;
+            const uint32_t q = b >> P.bshift;
+            const uint32_t bhi = (b >> 5) & kHMask;
+            const uint32_t both = bhi | (bhi << 16);
+            uint32_t c[kLR];
+#pragma unroll
+            for (uint32_t i = 0; i < kLR; ++i) c[i] = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
+            uint4 ent;
+            ent.x = both | (c[0] << HB) | (c[1] << (16 + HB)) | ((b & 31u) << P.bsh_shift);
+            ent.y = both | (c[2] << HB) | (c[3] << (16 + HB));
+            ent.z = both | (c[4] << HB) | (c[5] << (16 + HB));
+            ent.w = both | (c[6] << HB) | (c[7] << (16 + HB));
+            const uint32_t slot = atomicAdd(&cnt[q], 1u);
+            if (slot < P.stage_slots)
+              stage[q * P.stage_slots + slot] = ent;
+            else
+              direct_packet(P, hip, b, ldca);  // staging row full: direct (exact)
+            if (kSeav && (mix64_lo_split(oip, P.s_lo[1], P.s_hg[1]) & P.tau_mask) == 0u) {
+              const uint32_t qs = atomicAdd(sq_cnt + par, 1u);
+              if (qs < kSeavQueue)
+                sq_base[par * kSeavQueue + qs] = make_uint2(hip, oip);
+              else
+                seav_update_ool(p, hip, oip, seav);  // queue full (a skewed tile): apply now
+            }
+          }
+        }
+        __syncthreads();
+        if (kSeav) {  // the tile's sampled packets, all lanes busy
+          const uint32_t nq = min(sq_cnt[par], kSeavQueue);
+          const uint2* sq = sq_base + par * kSeavQueue;
+          for (uint32_t i = tid; i < nq; i += kThreads) seav_update(p, sq[i].x, sq[i].y, seav);
+          // the previous tile's queue was fully read before this barrier
+          if (tid == 0) sq_cnt[par ^ 1u] = 0;
+        }
+        // flush: G = 2^gshift threads per destination copy its run of 16-B
+        // entries into this CTA's own region of the destination's bucket
+        // (no global atomics); the loop is warp-uniform
+        {
+          const uint32_t gs = P.gshift, G = 1u << gs, gl = tid & (G - 1u);
+          const size_t boff = (size_t)bb * np * P.qstride + (size_t)self * P.region_cap;
+          for (uint32_t q0 = 0; q0 < np; q0 += (kThreads >> gs)) {
+            const uint32_t q = q0 + (tid >> gs);
+            if (q < np) {
+              const uint32_t m = min(cnt[q], P.stage_slots);
+              if (m) {
+                const uint32_t pos = cursor[q];
+                const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
+                uint4* dst = P.buckets + boff + (size_t)q * P.qstride + pos;
+                const uint4* src = stage + q * P.stage_slots;
+                uint32_t s = gl;
+                for (; s + 3u * G < fit; s += 4u * G) {  // 4 shared loads in flight, then 4 stores
+                  const uint4 a0 = src[s], a1 = src[s + G], a2 = src[s + 2u * G], a3 = src[s + 3u * G];
+                  __stcg(dst + s, a0);
+                  __stcg(dst + s + G, a1);
+                  __stcg(dst + s + 2u * G, a2);
+                  __stcg(dst + s + 3u * G, a3);
+                }
+                for (; s < fit; s += G) __stcg(dst + s, src[s]);
+                for (s = fit + gl; s < m; s += G) direct_entry<HB>(P, q, src[s], ldca);  // region full (exact)
+                if (gl == 0) {
+                  cursor[q] = pos + fit;
+                  cnt[q] = 0;
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (kSeav) {  // queues restart at parity 0 with the next chunk's slice
+        __syncthreads();
+        if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+      }
+      // publish this CTA's run lengths for chunk t and reset the cursors
+      for (uint32_t q = tid; q < np; q += kThreads) {
+        __stcg(P.counts + ((size_t)bb * np + q) * ns + self, cursor[q]);
+        cursor[q] = 0;
+      }
+    }
+    grid.sync();  // chunk t produced everywhere; chunk t-1 consumed everywhere
+  }
+  // fold the partition into the global LDCA: word (row, cell, j) of
+  // partition q is global word (row*lc + cell)*k/32 + q*2^HB + j.  After the
+  // last barrier no direct reds are in flight and the partitions are
+  // disjoint, so a plain read-modify-write is exact.
+  if (!owner) return;
+  __syncthreads();
+  const uint32_t rshift = 31 - __clz(P.row_words);  // row_words is a power of two
+  for (uint32_t i = tid; i < P.part_words; i += kThreads) {
+    const uint32_t v = part[i];
+    if (v) {
+      const uint32_t row = i >> rshift, within = i & (P.row_words - 1u);
+      const uint64_t cell = (uint64_t)row * P.lc + (within >> HB);
+      ldca[cell * P.kw + ((uint64_t)self << HB) + (within & kHMask)] |= v;
+    }
+  }
+}
+
+static uint32_t ilog2_exact(uint64_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  return l;
+}
+
+// Plan for the b-axis partitioned scan; false when the geometry or device
+// cannot host it (the caller then uses K1p or K1).
+static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int max_smem, Plan& P, uint64_t& smem,
+                 uint64_t& scratch, int& hb) {
+  const bool pow2 = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0;
+  if (p->lr != kLR || !pow2 || (uint64_t)p->lr * p->lc * p->k > 0xFFFFFFFFull) return false;
+  if (getenv("SSPD_PART_LEGACY") != nullptr) return false;
+  uint32_t np = 1;
+  while ((uint64_t)np * 2 <= (uint64_t)sms) np *= 2;
+  while (np > 1 && p->k / np < 32) np >>= 1;  // >= one word of b per cell and partition
+  if (np < 16 || p->k / np < 32) return false;
+  const uint32_t bw = p->k / np;
+  hb = (int)ilog2_exact(bw / 32);
+  if (hb > 3) return false;  // kernels are instantiated for 32..256 b values per cell
+  const uint32_t log2lc = ilog2_exact(p->lc);
+  if (log2lc + hb + 5 > 16) return false;  // half 0 holds the cell, the word and b & 31
+  P.nparts = np;
+  P.nsrc = (uint32_t)sms;
+  P.bshift = ilog2_exact(bw);
+  P.row_words = p->lc << hb;
+  P.part_words = kLR * P.row_words;
+  P.bsh_shift = log2lc + hb;
+  P.lowm = (1u << P.bsh_shift) - 1u;
+  {  // staging per destination per tile: mean kTile/np + 4 sigma + 8
+    const double mean = (double)kTile / np;
+    P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
+  }
+  smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 8ull * np + 16 + 16ull * kSeavQueue;
+  if ((int64_t)smem > max_smem) return false;
+  P.w_owner = 64;
+  P.w_other = 80;
+  if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
+  uint32_t tiles = 4;  // producer tiles per chunk (the bucket exchange of 2 chunks stays in L2)
+  if (const char* e = getenv("SSPD_BPART_TILES")) tiles = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 4;
+  P.chunk = chunk ? ((chunk + 3) & ~3ull) : (uint64_t)P.nsrc * kTile * tiles;
+  const double share =
+      (double)std::max(P.w_owner, P.w_other) / ((double)np * P.w_owner + (double)(P.nsrc - np) * P.w_other);
+  const double rmean = (double)P.chunk * share / np;  // largest producer -> one destination
+  P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
+  P.region_cap = (P.region_cap + 7u) & ~7u;  // regions start on 128-B lines
+  P.qstride = P.nsrc * P.region_cap;
+  if (2ull * np * P.qstride >= (1ull << 32)) return false;
+  P.gshift = 0;
+  while ((2u << P.gshift) <= 32u && ((kThreads >> (P.gshift + 1)) >= np)) ++P.gshift;
+  P.n = n;
+  scratch = 16ull * 2 * np * P.qstride + 4ull * 2 * np * P.nsrc;
+  P.k_mask = p->k - 1;
+  P.lc_mask = p->lc - 1;
+  P.log2k = ilog2_exact(p->k);
+  P.lc = p->lc;
+  P.kw = p->k / 32;
+  P.tau_mask = tau_mask(p->tau);
+  const uint64_t seeds[10] = {p->seed_h3,    p->seed_h1,    p->seed_lh[0], p->seed_lh[1], p->seed_lh[2],
+                              p->seed_lh[3], p->seed_lh[4], p->seed_lh[5], p->seed_lh[6], p->seed_lh[7]};
+  for (int i = 0; i < 10; ++i) {
+    P.s_lo[i] = (uint32_t)seeds[i];
+    P.s_hg[i] = (uint32_t)(seeds[i] >> 32) + (uint32_t)(kGolden >> 32);
+  }
+  return true;
+}
+
+template <bool kSeav>
+static void* kernel_for(int hb) {
+  switch (hb) {
+    case 0: return (void*)scan_bpart_kernel<kSeav, 0>;
+    case 1: return (void*)scan_bpart_kernel<kSeav, 1>;
+    case 2: return (void*)scan_bpart_kernel<kSeav, 2>;
+    default: return (void*)scan_bpart_kernel<kSeav, 3>;
+  }
+}
+
+static void device_limits(int& dev, int& sms, int& max_smem) {
+  dev = 0;
+  sms = 148;
+  max_smem = 232448;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+    max_smem = 232448;
+  }
+}
+
+}  // namespace bpart
+
+// Scratch bytes of the b-axis partitioned scan (0 = not applicable).
+uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk) {
+  int dev, sms, max_smem;
+  bpart::device_limits(dev, sms, max_smem);
+  bpart::Plan P;
+  uint64_t smem = 0, need = 0;
+  int hb = 0;
+  if (!bpart::plan(p, 1, chunk, sms, max_smem, P, smem, need, hb)) return 0;
+  return need;
+}
+
+// Launch; SSPD_ERR_CONFIG when not applicable (the caller tries K1p).
+int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
+                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream) {
+  int dev, sms, max_smem, coop = 0;
+  bpart::device_limits(dev, sms, max_smem);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return SSPD_ERR_CONFIG;
+  bpart::Plan P;
+  uint64_t smem = 0, need = 0;
+  int hb = 0;
+  if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb)) return SSPD_ERR_CONFIG;
+  if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  P.buckets = static_cast<uint4*>(scratch);
+  P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
+  P.vec_ok = (((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) == 0 &&
+              (P.chunk & 3u) == 0)
+                 ? 1u
+                 : 0u;
+  void* kern = seav ? bpart::kernel_for<true>(hb) : bpart::kernel_for<false>(hb);
+  // attribute/occupancy answers only change with (kernel, smem, device)
+  static void* c_kern = nullptr;
+  static uint64_t c_smem = 0;
+  static int c_dev = -1, c_per_sm = 0;
+  if (kern != c_kern || smem != c_smem || dev != c_dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bpart::kThreads, smem);
+    c_kern = kern, c_smem = smem, c_dev = dev, c_per_sm = per_sm;
+  }
+  if (c_per_sm < 1) return SSPD_ERR_CONFIG;
+  const uint32_t* h = hips;
+  const uint32_t* o = oips;
+  sspd_params pv = *p;
+  uint32_t* sv = reinterpret_cast<uint32_t*>(seav);
+  uint32_t* lv = reinterpret_cast<uint32_t*>(ldca);
+  void* args[] = {(void*)&h, (void*)&o, (void*)&pv, (void*)&P, (void*)&sv, (void*)&lv};
+  if (cudaLaunchCooperativeKernel(kern, dim3(P.nsrc), dim3(bpart::kThreads), args, smem,
+                                  static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    cudaGetLastError();
+    return SSPD_ERR_CUDA;
+  }
+  return check_launch();
+}
+
+}  // namespace sspd

@@ -504,6 +504,12 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   return true;
 }
 
+// K1b (scan_bpart.cu): the LDCA cut along its b axis, one 16-B entry per
+// packet; preferred whenever its plan applies.
+uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk);
+int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
+                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream);
+
 }  // namespace sspd
 
 using namespace sspd;
@@ -517,6 +523,8 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
   if (rc) return rc;
   if (n == 0) return SSPD_OK;
   if (!hips || !oips || !ldca) return SSPD_ERR_DATA;
+  if (scan_bpart_scratch(p, chunk) != 0)
+    return scan_bpart_launch(hips, oips, n, p, seav, ldca, scratch, scratch_bytes, chunk, stream);
   int dev = 0, sms = 0, max_smem = 0, coop = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -571,8 +579,29 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
 
 // Scratch bytes the partitioned scan needs for a given chunk size (0 when
 // the LDCA cannot be partitioned into shared memory on this device).
+// Which partitioned scan sspd_scan_partitioned runs for this geometry:
+// 2 = K1b (b-axis partitions), 1 = K1p (word-range partitions), 0 = none
+// (the LDCA does not fit the SMs' shared memory: SSPD_ERR_CONFIG).
+extern "C" int sspd_scan_partitioned_variant(const sspd_params* p, uint64_t chunk) {
+  if (!p || validate_params(p)) return 0;
+  if (scan_bpart_scratch(p, chunk) != 0) return 2;
+  int dev = 0, sms = 148, max_smem = 232448;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+    max_smem = 232448;
+  }
+  PartPlan P;
+  uint64_t smem = 0, need = 0;
+  int mode = 0;
+  return plan_partitioned(p, 1, chunk, sms, max_smem, P, smem, need, mode) ? 1 : 0;
+}
+
 extern "C" uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t chunk) {
   if (!p) return 0;
+  if (const uint64_t b = scan_bpart_scratch(p, chunk)) return b;
   int dev = 0, sms = 148, max_smem = 232448;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||

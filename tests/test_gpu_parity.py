@@ -211,27 +211,53 @@ def test_reset_replay_and_merge(cuda):
     assert shards[0].seav.payload_bytes() == a and shards[0].ldca.payload_bytes() == b
 
 
-@pytest.mark.parametrize("case", ["uniform", "skewed", "nonpow2", "tiny_chunks"])
-def test_partitioned_scan_vs_oracle(cuda, oracle, case):
-    """K1p (LDCA in shared memory, bucketed exchange) is bit-identical to the
-    oracle, including the overflow fallbacks a skewed stream triggers."""
-    from paper_1901_07306_b200 import DetectorParams
+PART_CASES = {
+    # case: (geometry, expected variant: 2 = K1b b-axis partitions, 1 = K1p word ranges)
+    "uniform": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    "skewed": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    "skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    "tiny_chunks": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    "k4096_hb0": (dict(theta=1024, r=12, k=4096, lr=8, lc=512), 2),
+    "k16384_hb2": (dict(theta=1024, r=12, k=16384, lr=8, lc=512), 2),
+    "k32768_hb3": (dict(theta=1024, r=16, k=32768, lr=8, lc=256), 2),
+    "nonpow2": (dict(theta=512, r=8, k=1000, lr=7, lc=333), 1),
+    "legacy_pow2": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 1),
+    "legacy_skewed": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 1),
+}
 
-    geom = dict(theta=1024, r=12, k=8192, lr=8, lc=1024)
-    if case == "nonpow2":
-        geom = dict(theta=512, r=8, k=1000, lr=7, lc=333)
+
+@pytest.mark.parametrize("case", list(PART_CASES))
+def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
+    """The partitioned scans are bit-identical to the oracle: K1b (LDCA cut
+    along b in shared memory, one 16-B entry per packet) and K1p (word-range
+    partitions; forced with SSPD_PART_LEGACY for pow2 geometries), including
+    the overflow fallbacks a skewed stream triggers -- one host (K1p: its
+    8 cells take half of all updates) or one opposite IP (K1b: half of all
+    packets go to ONE partition, overflowing its staging row and regions)."""
+    from paper_1901_07306_b200 import DetectorParams
+    from paper_1901_07306_b200._abi import lib
+
+    geom, variant = PART_CASES[case]
+    if case.startswith("legacy"):
+        monkeypatch.setenv("SSPD_PART_LEGACY", "1")
     dp = DetectorParams(design_n=1e6, **geom)
     _, _, p = params_block(dp)
     rng = np.random.default_rng(77)
     n = 3_000_017
     hips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
     oips = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
-    if case == "skewed":
+    if case in ("skewed", "legacy_skewed"):
         hips[: n // 2] = 0xC0A80001  # one host: its 8 cells take half of all updates
         hips[n // 2: n // 2 + 100_000] = 0x0A000001
+    if case == "skewed_oip":
+        oips[: n // 2] = 0x08080808  # one opposite IP: one b, so one K1b partition
+        oips[n // 2: n // 2 + 100_000] = 0x01010101
+        perm = rng.permutation(n)
+        hips, oips = hips[perm], oips[perm]
     seav, ldca = oracle.scan(p, hips, oips, threads=8)
     st = make_state(dp)
     st.scan_mode = "partitioned"
+    assert lib().sspd_scan_partitioned_variant(st.seav._params, 0) == variant
     if case == "tiny_chunks":
         st.partitioned_chunk = 1 << 14
     st.process_batch(hips[: n // 3], oips[: n // 3])
