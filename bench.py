@@ -241,6 +241,25 @@ def cpu_baseline_quick(scale: int) -> dict:
             "sample": f"{len(hips)} pkts of the config-2 law (1/{scale} scale), scan+restore+filter, best of 2"}
 
 
+def merge_summary(merger, merge_ms: list[float], dist, dev, args) -> dict:
+    """Per-window OR-merge cost (multigpu.OrMerger.merge_to_root), max over
+    ranks of each rank's median, with the bytes it moves over NVLink."""
+    import torch
+
+    med = statistics.median(merge_ms) if merge_ms else 0.0
+    t = torch.tensor([med, max(merge_ms) if merge_ms else 0.0], dtype=torch.float64,
+                     device=dev if args.backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    med, worst = float(t[0]), float(t[1])
+    tr = merger.traffic()
+    moved = tr["peer_read_bytes_this_rank"] + tr["root_gather_bytes"]
+    return {"merge_ms_median": round(med, 4), "merge_ms_max": round(worst, 4), **tr,
+            "achieved_gbs": round(moved / (med * 1e-3) / 1e9, 2) if med > 0 else None,
+            "note": "host wall time of merge_to_root after the post-scan barrier: reduce-scatter of the "
+                    "SEAV||LDCA block by stripes over CUDA-IPC peer reads, gather onto rank 0, three barriers; "
+                    "achieved_gbs = (this rank's peer reads + root gather) / median"}
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_gpu(args) -> dict | None:
     import torch
@@ -256,14 +275,7 @@ def run_gpu(args) -> dict | None:
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group("gloo")
+    dist = init_ranks(args, local)
     lib()
 
     from dataclasses import replace
@@ -293,6 +305,7 @@ def run_gpu(args) -> dict | None:
 
     stream = torch.cuda.current_stream()
     scan_ev = []
+    merge_ms: list[float] = []
 
     def step(reports_out=None, time_scan=False):
         if time_scan:
@@ -304,6 +317,8 @@ def run_gpu(args) -> dict | None:
             scan_ev.append((a, b))
         if merger is not None:
             merger.merge_to_root()
+            if time_scan:
+                merge_ms.append(merger.last_merge_ms)
         if rank != 0:
             st.reset()
             return []
@@ -413,7 +428,10 @@ def run_gpu(args) -> dict | None:
                                "frac": round(h2d[0] / (e2e_ms * 1e-3) / 1e9 / h2d_gbs, 4)}
         del dst
 
+    merge = merge_summary(merger, merge_ms, dist, dev, args) if merger is not None else None
     if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
         return None
 
     # roofline: the dominant kernel is K1 (scan).  Algorithmic bytes = 8 B
@@ -486,6 +504,7 @@ def run_gpu(args) -> dict | None:
                                    "rate measured live; K1p keeps the LDCA in shared memory so it is not bound "
                                    "by L2 atomics -- see issue_roofline")},
         "issue_roofline": issue,
+        "merge": merge,
         "clocks": clk,
         "detect": {"reports_per_window": counts[0] if counts else None,
                    "planted_supers_found": planted_found, "planted": len(supers)},
@@ -692,14 +711,7 @@ def run_sharded(args) -> dict | None:
     local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group("gloo")
+    dist = init_ranks(args, local)
     lib()
     spec = CONFIG3
     if args.packets:
@@ -725,11 +737,15 @@ def run_sharded(args) -> dict | None:
         merger = OrMerger(st, dist)
     stream = torch.cuda.current_stream()
 
+    merge_ms: list[float] = []
+
     def step(out=None):
         for h, o in shards:
             st.process_batch(h, o)
         if merger is not None:
             merger.merge_to_root()
+            if out is None:
+                merge_ms.append(merger.last_merge_ms)
         reps = st.finalize_window() if rank == 0 else []
         st.reset()
         if out is not None:
@@ -761,6 +777,9 @@ def run_sharded(args) -> dict | None:
         t = torch.tensor([ms], device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    merge = merge_summary(merger, merge_ms, dist, dev, args) if merger is not None else None
+    if dist is not None:
+        dist.destroy_process_group()
     if rank != 0:
         return None
     value = n_total / (ms * 1e-3) / 1e6
@@ -775,6 +794,7 @@ def run_sharded(args) -> dict | None:
                    "parallelism": f"dp{world} (shards folded onto ranks, OR-merge to rank 0)",
                    "l2": "inputs (8 GiB) exceed the 126 MB L2; no flush needed"},
         "e2e": None, "gpu_launches": args.steps * (len(mine) + 6 + (2 if merger else 0)),
+        "merge": merge,
         "clocks": clk,
         "detect": {"reports_per_window": len(first[0]), "planted_supers_found": len(set(supers.tolist()) & found),
                    "planted": len(supers),
@@ -870,6 +890,79 @@ def run_streaming(args) -> dict:
     }
 
 
+# ------------------------------------------------------------ rank launcher
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_cmd(argv: list[str], nproc: int, port: int) -> list[str]:
+    """torchrun command that re-runs this script as `nproc` ranks (one process
+    per GPU) on this node, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+
+
+def self_launch(args, argv: list[str]) -> int | None:
+    """`--gpus N` (N > 1) without a torchrun environment: spawn the N ranks
+    ourselves so the run really times N GPUs (rank 0 prints the line)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if not args.launcher_selftest and not args.same_device:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible "
+                             "(use --same-device to run the ranks on GPU 0 as a protocol test)")
+    print(f"[bench] launching {args.gpus} ranks via torch.distributed.run", file=sys.stderr, flush=True)
+    return subprocess.call(launch_cmd(argv, args.gpus, _free_port()))
+
+
+def init_ranks(args, local: int):
+    """Process group of the torchrun ranks (None at N = 1); logs the
+    communicator so the driver can check ranks and backend."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    if args.same_device:  # NCCL refuses two ranks on one GPU: protocol runs use gloo
+        args.backend = "gloo"
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    dev = f"cuda:{local}" if args.backend == "nccl" or torch.cuda.is_available() else "cpu"
+    print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()} backend={dist.get_backend()} device={dev} "
+          f"nccl={'.'.join(map(str, torch.cuda.nccl.version())) if args.backend == 'nccl' else '-'}",
+          file=sys.stderr, flush=True)
+    return dist
+
+
+def run_launcher_selftest(args) -> dict | None:
+    """CPU check of the launcher: every rank joins a gloo group and
+    all-reduces its rank; rank 0 reports the world it saw."""
+    import torch
+
+    args.backend = "gloo"
+    dist = init_ranks(args, 0)
+    world = dist.get_world_size() if dist else 1
+    rank = dist.get_rank() if dist else 0
+    t = torch.tensor([rank + 1], dtype=torch.int64)
+    if dist:
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {"selftest": "launcher", "n_gpus": world, "rank_sum": int(t.item()),
+            "world_env": int(os.environ.get("WORLD_SIZE", "1"))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -897,7 +990,17 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="2 = headline discrete window; 3 = 8 router shards OR-merged (strong scaling); "
                          "4 = sliding window, detect every slide; 5 = 2^32 pkts streamed from host")
+    ap.add_argument("--launcher-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.impl != "reference":
+        rc = self_launch(args, sys.argv[1:])
+        if rc is not None:
+            sys.exit(rc)
+    if args.launcher_selftest:
+        line = run_launcher_selftest(args)
+        if line is not None:
+            print(json.dumps(line))
+        return
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return

@@ -175,7 +175,8 @@ SSPD_API int sspd_materialize_seav_if(const void* pool, uint32_t ts_bytes, const
  * instead record the slot in an LDCA-shaped dirty bitmap (ldca_bytes):
  *   sspd_scan_sliding_deferred = sspd_scan_sliding_tracked (seav_view may be
  *       NULL: no tracking) whose LDCA stamps go to `ldca_dirty` (may be
- *       NULL: stored directly; also when the u16 fast path does not apply);
+ *       NULL: stored directly) -- for every geometry and input alignment
+ *       (a generic u16 kernel when the fast path does not apply);
  *   sspd_ldca_fold             = stamp now_wrapped into every dirty slot and
  *       clear the bitmap; with ldca_view != NULL also write the packed
  *       active-bit LDCA (as sspd_materialize_ldca after the fold) in the

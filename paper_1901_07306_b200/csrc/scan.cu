@@ -265,6 +265,60 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
   for (uint64_t j = head + (nq << 2) + tid; j < n; j += stride) one(hips[j], oips[j]);
 }
 
+// K2 for u16 stamps when the fast path does not apply (k or lc not a power
+// of two, or hips/oips misaligned relative to each other): scalar loads and
+// the exact 64-bit modulo, with the same optional SEAV tracking and deferred
+// LDCA stamps as the fast kernel (dirty bit = the LDCA bit index
+// (i*lc + c)*k + b), so every u16 scan honours the caller's deferred state.
+template <bool kTrack, bool kDefer>
+__global__ void __launch_bounds__(256) scan_sliding_u16_generic_kernel(const uint32_t* __restrict__ hips,
+                                                                       const uint32_t* __restrict__ oips, uint64_t n,
+                                                                       const __grid_constant__ sspd_params p,
+                                                                       uint16_t* pool, uint16_t now, SeavTracker tr,
+                                                                       uint32_t* dirty) {
+  const uint32_t tmask = tau_mask(p.tau);
+  uint16_t* const lpool = pool + p.slot_ldca_base;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    const uint32_t hip = hips[j], oip = oips[j];
+    if (sampled(oip, p.seed_h1, tmask)) {
+      const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+      const uint64_t rp = hip & ((1u << p.r) - 1u);
+      const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+      unsigned long long pos = 0;
+      if (kTrack) {
+        cg::coalesced_group g = cg::coalesced_threads();
+        unsigned long long base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(tr.log_head, (unsigned long long)g.size() * p.sr);
+        pos = g.shfl(base, 0) + (unsigned long long)g.thread_rank() * p.sr;
+      }
+      for (uint32_t i = 0; i < p.sr; ++i) {
+        const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+        const uint64_t reg = rp * p.sc[i] + col;
+        const uint64_t slot = p.slot_row_base[i] + reg * p.g + bit;
+        pool[slot] = now;
+        if (kTrack) {
+          const uint64_t vbit = (p.seav_row_off[i] + reg * p.reg_bytes) * 8 + bit;
+          atomicOr(tr.view + (vbit >> 5), 1u << (vbit & 31));
+          tr.log[(pos + i) & tr.log_mask] = (uint32_t)slot;
+        }
+      }
+    }
+    const uint64_t b = hash_range(oip, p.seed_h3, p.div_k);
+    const uint64_t k = p.k;
+    uint64_t cell = 0;
+    for (uint32_t i = 0; i < p.lr; ++i) {
+      const uint64_t c = hash_range(hip, p.seed_lh[i], p.div_lc);
+      const uint64_t slot = (cell + c) * k + b;
+      if (kDefer)
+        red_or(dirty + (slot >> 5), 1u << (slot & 31));
+      else
+        lpool[slot] = now;
+      cell += p.lc;
+    }
+  }
+}
+
 template <bool S, bool L>
 static int launch_discrete(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params& p,
                            uint8_t* seav, uint8_t* ldca, cudaStream_t st) {
@@ -323,8 +377,9 @@ extern "C" int sspd_scan_sliding_tracked(const uint32_t* hips, const uint32_t* o
 }
 
 // Tracked (optional: seav_view may be null) scan with deferred LDCA stamps
-// (optional: ldca_dirty may be null).  When the u16 fast path does not apply
-// the stamps are stored directly -- the same result.
+// (optional: ldca_dirty may be null).  u16 stamps only; when the fast path
+// does not apply (geometry, alignment) the generic u16 kernel keeps the same
+// tracked / deferred semantics (the ring of dirty bitmaps depends on it).
 extern "C" int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                           const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
                                           uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
@@ -351,7 +406,8 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
                              SeavTracker tracker, uint32_t* dirty, void* stream) {
   int rc = validate_params(p);
   if (rc) return rc;
-  if (tracker.view && ts_bytes != 2) return SSPD_ERR_CONFIG;  // tracking exists only on the u16 fast path
+  // tracking and deferred LDCA stamps exist for u16 stamps only
+  if ((tracker.view || dirty) && ts_bytes != 2) return SSPD_ERR_CONFIG;
   if (n == 0) return SSPD_OK;
   if (!hips || !oips || !pool) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -386,7 +442,15 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
         kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker, dirty);
         break;
       }
-      if (tracker.view) return SSPD_ERR_CONFIG;  // tracking exists only on the fast path
+      if (tracker.view || dirty) {  // the caller's tracked / deferred state must be honoured
+        if (p->slot_total >= (1ull << 32) && tracker.view) return SSPD_ERR_CONFIG;  // 32-bit log entries
+        auto kern = tracker.view
+                        ? (dirty ? scan_sliding_u16_generic_kernel<true, true> : scan_sliding_u16_generic_kernel<true, false>)
+                        : scan_sliding_u16_generic_kernel<false, true>;
+        const int grid = grid_for(kern, 256, n);
+        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, tracker, dirty);
+        break;
+      }
       const int grid = grid_for(scan_sliding_kernel<uint16_t>, 256, n);
       scan_sliding_kernel<uint16_t><<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped);
       break;

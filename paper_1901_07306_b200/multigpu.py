@@ -148,15 +148,38 @@ class OrMerger:
         if self.transport == "nccl" and not allow_fallback:
             raise RuntimeError("CUDA IPC peer mapping failed on some rank")
         self.stripes = stripes(self.nbytes, self.world)
+        self.last_merge_ms = 0.0
+
+    def traffic(self) -> dict:
+        """Bytes one merge moves: each rank reads its stripe of every peer's
+        block (reduce-scatter) and the root reads every other stripe back
+        (gather)."""
+        lo, hi = self.stripes[self.rank]
+        peer_reads = (self.world - 1) * (hi - lo) if self.transport == "ipc" else (self.world - 1) * self.nbytes
+        root_ingress = sum(h - l for r, (l, h) in enumerate(self.stripes) if r != 0)
+        return {"block_bytes": self.nbytes, "peer_read_bytes_this_rank": peer_reads,
+                "root_gather_bytes": root_ingress, "transport": self.transport}
 
     @traced("merge")
     def merge_to_root(self):
-        """After every rank finished scanning: rank 0's block = OR of all blocks."""
+        """After every rank finished scanning: rank 0's block = OR of all blocks.
+
+        `last_merge_ms` = host wall time from the barrier that follows this
+        rank's scan to the end of the merge (both data phases, their device
+        syncs and the two further barriers)."""
+        import time
+
         if self.transport == "nccl":
-            return self._merge_nccl()
+            self.ops.sync()
+            self.dist.barrier(group=self.group)
+            t0 = time.perf_counter()
+            self._merge_nccl()
+            self.last_merge_ms = (time.perf_counter() - t0) * 1e3
+            return
         d = self.dist
         self.ops.sync()
         d.barrier(group=self.group)              # all scans complete
+        t0 = time.perf_counter()
         lo, hi = self.stripes[self.rank]
         if hi > lo:                               # reduce-scatter: my stripe of every block
             self.ops.merge_or([p + lo for p in self.peers], self.base + lo, hi - lo)
@@ -169,6 +192,7 @@ class OrMerger:
                     self.ops.copy(self.base + lo, self.peers[r] + lo, hi - lo)
             self.ops.sync()
         d.barrier(group=self.group)              # root done reading peers
+        self.last_merge_ms = (time.perf_counter() - t0) * 1e3
 
     def _merge_nccl(self):
         import torch

@@ -464,7 +464,8 @@ def test_deferred_ldca_stamps_equal_direct_stamps(cuda):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("async_detect", [False, True])
-@pytest.mark.parametrize("geom", [(4096, 4, 256), (64, 3, 37)], ids=["ldca16B", "ldca_pad8"])
+@pytest.mark.parametrize("geom", [(4096, 4, 256), (64, 3, 37), (4096, 4, 256, "misaligned")],
+                         ids=["ldca16B", "ldca_pad8_nonpow2", "misaligned_inputs"])
 def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom):
     """Ring mode of the deferred LDCA stamps (the LDCA view as a two-stack
     sliding-window OR of per-slice bitmaps, stamps folded lazily) against
@@ -473,10 +474,15 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom):
     reads mid-block, a write around the detector (restart: stamps-based view
     for one block, then the ring again), and reset.  `ldca_pad8`: 888 LDCA
     bytes, so the ring pads each slice's bitmap to 896 B (the fold must step
-    by the padded stride, not the LDCA size)."""
+    by the padded stride, not the LDCA size) and lc = 37 (the generic u16
+    scan must fill the dirty bitmaps).  `misaligned_inputs`: device hips /
+    oips at different 16-B offsets (no fast path either)."""
+    import torch
+
     from paper_1901_07306_b200 import DetectorParams, SlidingDetector
 
-    k, lr, lc = geom
+    k, lr, lc = geom[:3]
+    misaligned = len(geom) > 3
     params = DetectorParams(theta=256, r=8, k=k, lr=lr, lc=lc, design_n=2e5)
     w = 129
     with warnings.catch_warnings():
@@ -497,7 +503,13 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom):
         oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
         if s < 40 or 150 <= s < 175:  # bursts that expire inside the run
             hips[: n // 2] = heavy[s % 3]
-        a.observe_batch(hips, oips)
+        if misaligned and n:
+            hd = torch.from_numpy(hips.astype(np.uint32).view(np.int32)).cuda()
+            od = torch.zeros(n + 1, dtype=torch.int32, device="cuda")
+            od[1:] = torch.from_numpy(oips.astype(np.uint32).view(np.int32)).cuda()
+            a.observe_batch(hd, od[1:])
+        else:
+            a.observe_batch(hips, oips)
         b.observe_batch(hips, oips)
         if s == 200:  # a write around the detector: restart, stamps-based view for one block
             for det in (a, b):

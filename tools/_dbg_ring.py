@@ -1,3 +1,4 @@
+import sys; sys.path.insert(0, ".")
 import warnings
 import numpy as np
 from paper_1901_07306_b200 import DetectorParams, SlidingDetector
