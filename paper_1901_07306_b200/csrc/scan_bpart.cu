@@ -15,11 +15,13 @@
 // of a packet share its b, so the packet goes to exactly ONE partition
 // q = b / bw as one 16-byte entry:
 //
-//   eight u16 halves, half_i = c_i << HB | (b % bw) >> 5   (HB = log2(bw/32))
-//   half_0 additionally carries b & 31 in bits [log2(lc)+HB, +5)
+//   eight u16 halves; with w_i = c_i << HB | (b % bw) >> 5 (HB = log2(bw/32))
+//   the word of row i inside the partition (rows of rw = lc << HB words):
+//     half_0 = w_0 | (b & 31) << log2(rw)        (a word index + the bit)
+//     half_i = 4 * (i * rw + w_i), i = 1..7      (shared-memory byte offsets)
 //
-// which the owner of q turns into 8 shared-memory atomicOr (word
-// i*(lc << HB) + half_i of its partition, bit b & 31).  Per packet: one
+// which the owner of q turns into 8 shared-memory atomicOr (bit b & 31 of
+// word i*rw + w_i of its partition; 8*rw*4 <= 2^16 by plan).  Per packet: one
 // shared atomicAdd instead of 8, one 16-byte staging store instead of 8
 // scalar ones, 16 B of bucket writes + 16 B of reads instead of 32 + 32.
 //
@@ -45,15 +47,17 @@ constexpr uint32_t kPkt = 4;  // packets per thread per tile (one uint4 of hips 
 constexpr uint32_t kTile = kThreads * kPkt;
 constexpr uint32_t kLR = 8;
 constexpr uint32_t kSeavQueue = 128;  // sampled packets per tile parity
+constexpr uint32_t kMaxSrc = 256;     // producer CTAs (SMs) the plan supports
 
 struct Plan {
   uint32_t nparts;       // partitions = consumer CTAs 0 .. nparts-1 (power of two)
   uint32_t nsrc;         // producers = gridDim.x (>= nparts)
   uint32_t bshift;       // log2(bw): partition of b = b >> bshift
-  uint32_t row_words;    // lc << HB: words of one LDCA row inside a partition
+  uint32_t row_words;    // rw = lc << HB: words of one LDCA row inside a partition (<= 2048)
   uint32_t part_words;   // kLR * row_words
-  uint32_t lowm;         // mask of half 0 without the bit position
-  uint32_t bsh_shift;    // log2(lc) + HB: where half 0 keeps b & 31
+  uint32_t lowm;         // rw - 1: half 0 without the bit position
+  uint32_t bsh_shift;    // log2(rw): where half 0 keeps b & 31
+  uint32_t rowc[4];      // per entry word: the row byte offsets of its halves (4*i*rw << 16*(i&1))
   uint32_t stage_slots;  // 16-B entries per destination per tile
   uint32_t region_cap;   // entries per (src, dst) region per chunk
   uint32_t w_owner, w_other;  // producer slice weights (owners vs pure producers)
@@ -68,6 +72,7 @@ struct Plan {
   uint32_t qstride;      // nsrc * region_cap: bucket entries per destination
   uint32_t gshift;       // log2 of the flush group (threads per destination)
   uint32_t tau_mask;
+  uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
 };
 
 __device__ __forceinline__ void red_or_g(uint32_t* addr, uint32_t v) {
@@ -106,17 +111,20 @@ __device__ __noinline__ void direct_entry(const Plan& P, uint32_t q, uint4 e, ui
   const uint32_t h[kLR] = {e.x & P.lowm, e.x >> 16, e.y & 0xFFFFu, e.y >> 16,
                            e.z & 0xFFFFu, e.z >> 16, e.w & 0xFFFFu, e.w >> 16};
   for (uint32_t i = 0; i < kLR; ++i) {
-    const uint32_t c = h[i] >> HB;
-    const uint32_t b = (q << P.bshift) | ((h[i] & ((1u << HB) - 1u)) << 5) | bsh;
+    const uint32_t w = (i ? h[i] >> 2 : h[i]) & (P.row_words - 1u);  // strip the row offset
+    const uint32_t c = w >> HB;
+    const uint32_t b = (q << P.bshift) | ((w & ((1u << HB) - 1u)) << 5) | bsh;
     const uint32_t bit = ((i * P.lc + c) << P.log2k) | b;
     red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
   }
 }
 
 // Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
-// take w_other/w_owner as much as owners; boundaries are 4-aligned.
+// take w_other/w_owner as much as owners; boundaries are 4-aligned.  Full
+// chunks read the host-computed table (no 64-bit division per chunk).
 __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint64_t c1, uint32_t s) {
   if (s >= P.nsrc) return c1;
+  if (c1 - c0 == P.chunk) return c0 + P.slice_off[s];
   const uint64_t tw = (uint64_t)P.nparts * P.w_owner + (uint64_t)(P.nsrc - P.nparts) * P.w_other;
   const uint64_t cw =
       (uint64_t)min(s, P.nparts) * P.w_owner + (uint64_t)(s > P.nparts ? s - P.nparts : 0) * P.w_other;
@@ -125,7 +133,7 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 }
 
 // Shared memory: [part_words | nparts*stage_slots uint4 staging | nparts cnt |
-//                 nparts cursor | 4 sq_cnt | 2*kSeavQueue (hip, oip)]
+//                 4 sq_cnt | 2*kSeavQueue (hip, oip)]
 template <bool kSeav, int HB>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_bpart_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
@@ -135,8 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* part = smem;
   uint4* stage = reinterpret_cast<uint4*>(smem + P.part_words);  // part_words % 4 == 0
   uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
-  uint32_t* cursor = cnt + P.nparts;
-  uint32_t* sq_cnt = cursor + P.nparts;                     // [2] (+2 pad)
+  uint32_t* sq_cnt = cnt + P.nparts;                        // [2] (+2 pad); nparts % 4 == 0
   uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [2][kSeavQueue]
   cg::grid_group grid = cg::this_grid();
   const uint32_t self = blockIdx.x;
@@ -147,7 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kHMask = (1u << HB) - 1u;
 
   for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
-  for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = cursor[i] = 0;
+  for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = 0;
+  // flush role, fixed for the launch: group q = tid >> gshift of G threads
+  // copies destination q's staging row (one pass covers every destination)
+  const uint32_t gs = P.gshift, G = 1u << gs, gl = tid & (G - 1u), fq = tid >> gs;
+  const bool flusher = fq < np;
   if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
   __syncthreads();
 
@@ -158,7 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bb = (uint32_t)((t - 1) & 1);
       const uint32_t* cnts = P.counts + ((size_t)bb * np + self) * ns;
       const uint4* regions = P.buckets + ((size_t)bb * np + self) * (size_t)P.qstride;
-      const uint32_t rw = P.row_words, lowm = P.lowm, bss = P.bsh_shift;
+      const uint32_t lowm = P.lowm, bss = P.bsh_shift;
+      char* const pb = reinterpret_cast<char*>(part);
       // warp w drains sources w, w+W, ...: lane j holds the run length of
       // source w+W*j, fetched at once so no region waits on its count
       const uint32_t my_src = warp + nwarps * lane;
@@ -177,13 +189,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint4 e = u[g];
               const uint32_t bit = 1u << ((e.x >> bss) & 31u);
               atomicOr(part + (e.x & lowm), bit);
-              atomicOr(part + rw + (e.x >> 16), bit);
-              atomicOr(part + 2 * rw + (e.y & 0xFFFFu), bit);
-              atomicOr(part + 3 * rw + (e.y >> 16), bit);
-              atomicOr(part + 4 * rw + (e.z & 0xFFFFu), bit);
-              atomicOr(part + 5 * rw + (e.z >> 16), bit);
-              atomicOr(part + 6 * rw + (e.w & 0xFFFFu), bit);
-              atomicOr(part + 7 * rw + (e.w >> 16), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.x >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.y & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.y >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.z & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.z >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.w & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (e.w >> 16)), bit);
             }
           }
         }
@@ -217,6 +229,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       };
+      // this thread's flush destination: region (self -> fq) of bucket bb,
+      // filled up to `pos` (identical in the G lanes of the group)
+      uint4* const dstq = P.buckets + ((size_t)bb * np + fq) * P.qstride + (size_t)self * P.region_cap;
+      const uint4* const srcq = stage + fq * P.stage_slots;
+      uint32_t pos = 0;
       uint32_t nh[kPkt], no[kPkt];
       fetch(lo + (uint64_t)tid * kPkt, nh, no);
       uint32_t par = 0;  // tile parity: selects the sampled-packet queue
@@ -236,15 +253,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b = mix64_lo_split(oip, P.s_lo[0], P.s_hg[0]) & P.k_mask;
             const uint32_t q = b >> P.bshift;
             const uint32_t bhi = (b >> 5) & kHMask;
-            const uint32_t both = bhi | (bhi << 16);
+            // the word bits shared by all halves (half 0: word index, 1..7: byte offsets)
+            const uint32_t both = (bhi << 2) * 0x10001u;
             uint32_t c[kLR];
 #pragma unroll
             for (uint32_t i = 0; i < kLR; ++i) c[i] = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
             uint4 ent;
-            ent.x = both | (c[0] << HB) | (c[1] << (16 + HB)) | ((b & 31u) << P.bsh_shift);
-            ent.y = both | (c[2] << HB) | (c[3] << (16 + HB));
-            ent.z = both | (c[4] << HB) | (c[5] << (16 + HB));
-            ent.w = both | (c[6] << HB) | (c[7] << (16 + HB));
+            ent.x = (c[0] << HB) + bhi + ((b & 31u) << P.bsh_shift) + c[1] * (1u << (18 + HB)) + (both & 0xFFFF0000u) +
+                    P.rowc[0];
+            ent.y = c[2] * (1u << (2 + HB)) + c[3] * (1u << (18 + HB)) + (both + P.rowc[1]);
+            ent.z = c[4] * (1u << (2 + HB)) + c[5] * (1u << (18 + HB)) + (both + P.rowc[2]);
+            ent.w = c[6] * (1u << (2 + HB)) + c[7] * (1u << (18 + HB)) + (both + P.rowc[3]);
             const uint32_t slot = atomicAdd(&cnt[q], 1u);
             if (slot < P.stage_slots)
               stage[q * P.stage_slots + slot] = ent;
@@ -267,38 +286,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           // the previous tile's queue was fully read before this barrier
           if (tid == 0) sq_cnt[par ^ 1u] = 0;
         }
-        // flush: G = 2^gshift threads per destination copy its run of 16-B
-        // entries into this CTA's own region of the destination's bucket
-        // (no global atomics); the loop is warp-uniform
-        {
-          const uint32_t gs = P.gshift, G = 1u << gs, gl = tid & (G - 1u);
-          const size_t boff = (size_t)bb * np * P.qstride + (size_t)self * P.region_cap;
-          for (uint32_t q0 = 0; q0 < np; q0 += (kThreads >> gs)) {
-            const uint32_t q = q0 + (tid >> gs);
-            if (q < np) {
-              const uint32_t m = min(cnt[q], P.stage_slots);
-              if (m) {
-                const uint32_t pos = cursor[q];
-                const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
-                uint4* dst = P.buckets + boff + (size_t)q * P.qstride + pos;
-                const uint4* src = stage + q * P.stage_slots;
-                uint32_t s = gl;
-                for (; s + 3u * G < fit; s += 4u * G) {  // 4 shared loads in flight, then 4 stores
-                  const uint4 a0 = src[s], a1 = src[s + G], a2 = src[s + 2u * G], a3 = src[s + 3u * G];
-                  __stcg(dst + s, a0);
-                  __stcg(dst + s + G, a1);
-                  __stcg(dst + s + 2u * G, a2);
-                  __stcg(dst + s + 3u * G, a3);
-                }
-                for (; s < fit; s += G) __stcg(dst + s, src[s]);
-                for (s = fit + gl; s < m; s += G) direct_entry<HB>(P, q, src[s], ldca);  // region full (exact)
-                if (gl == 0) {
-                  cursor[q] = pos + fit;
-                  cnt[q] = 0;
-                }
-              }
-            }
+        // flush: the G = 2^gshift threads of group fq copy destination fq's
+        // run of 16-B entries into this CTA's own region of that bucket (no
+        // global atomics); `pos` lives in registers, identical in the group
+        if (flusher) {
+          const uint32_t m = min(cnt[fq], P.stage_slots);
+          const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
+          uint4* dst = dstq + pos;
+          uint32_t s = gl;
+          for (; s + G < fit; s += 2u * G) {  // 2 shared loads in flight, then 2 stores
+            const uint4 a0 = srcq[s], a1 = srcq[s + G];
+            __stcg(dst + s, a0);
+            __stcg(dst + s + G, a1);
           }
+          if (s < fit) __stcg(dst + s, srcq[s]);
+          for (s = fit + gl; s < m; s += G) direct_entry<HB>(P, fq, srcq[s], ldca);  // region full (exact)
+          pos += fit;
+          __syncwarp();  // the group's lanes read cnt[fq] before it is reset
+          if (gl == 0) cnt[fq] = 0;
         }
         __syncthreads();
       }
@@ -306,11 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
       }
-      // publish this CTA's run lengths for chunk t and reset the cursors
-      for (uint32_t q = tid; q < np; q += kThreads) {
-        __stcg(P.counts + ((size_t)bb * np + q) * ns + self, cursor[q]);
-        cursor[q] = 0;
-      }
+      // publish this CTA's run lengths for chunk t
+      if (flusher && gl == 0) __stcg(P.counts + ((size_t)bb * np + fq) * ns + self, pos);
     }
     grid.sync();  // chunk t produced everywhere; chunk t-1 consumed everywhere
   }
@@ -352,7 +354,8 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   hb = (int)ilog2_exact(bw / 32);
   if (hb > 3) return false;  // kernels are instantiated for 32..256 b values per cell
   const uint32_t log2lc = ilog2_exact(p->lc);
-  if (log2lc + hb + 5 > 16) return false;  // half 0 holds the cell, the word and b & 31
+  if (log2lc + hb > 11) return false;  // 8 rows of rw <= 2048 words: byte offsets fit a u16 half
+  if (sms > (int)kMaxSrc) return false;
   P.nparts = np;
   P.nsrc = (uint32_t)sms;
   P.bshift = ilog2_exact(bw);
@@ -360,18 +363,23 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   P.part_words = kLR * P.row_words;
   P.bsh_shift = log2lc + hb;
   P.lowm = (1u << P.bsh_shift) - 1u;
+  for (uint32_t w = 0; w < 4; ++w)
+    P.rowc[w] = (w ? (4u * (2 * w) * P.row_words) : 0u) | ((4u * (2 * w + 1) * P.row_words) << 16);
   {  // staging per destination per tile: mean kTile/np + 4 sigma + 8
     const double mean = (double)kTile / np;
     P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
   }
-  smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 8ull * np + 16 + 16ull * kSeavQueue;
+  smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 16ull * kSeavQueue;
   if ((int64_t)smem > max_smem) return false;
   P.w_owner = 64;
   P.w_other = 80;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
-  uint32_t tiles = 4;  // producer tiles per chunk (the bucket exchange of 2 chunks stays in L2)
-  if (const char* e = getenv("SSPD_BPART_TILES")) tiles = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 4;
+  // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
+  // outweigh the part of the bucket exchange that then spills from L2)
+  uint32_t tiles = 16;
+  if (const char* e = getenv("SSPD_BPART_TILES")) tiles = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 16;
   P.chunk = chunk ? ((chunk + 3) & ~3ull) : (uint64_t)P.nsrc * kTile * tiles;
+  if (P.chunk >= (1ull << 32)) return false;  // slice offsets are 32-bit
   const double share =
       (double)std::max(P.w_owner, P.w_other) / ((double)np * P.w_owner + (double)(P.nsrc - np) * P.w_other);
   const double rmean = (double)P.chunk * share / np;  // largest producer -> one destination
@@ -379,8 +387,15 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   P.region_cap = (P.region_cap + 7u) & ~7u;  // regions start on 128-B lines
   P.qstride = P.nsrc * P.region_cap;
   if (2ull * np * P.qstride >= (1ull << 32)) return false;
-  P.gshift = 0;
+  P.gshift = 0;  // one pass of the flush covers every destination: np << gshift <= kThreads
   while ((2u << P.gshift) <= 32u && ((kThreads >> (P.gshift + 1)) >= np)) ++P.gshift;
+  {  // producer slice offsets inside a full chunk (slice_start)
+    const uint64_t tw = (uint64_t)np * P.w_owner + (uint64_t)(P.nsrc - np) * P.w_other;
+    for (uint32_t sidx = 0; sidx <= P.nsrc; ++sidx) {
+      const uint64_t cw = (uint64_t)std::min(sidx, np) * P.w_owner + (uint64_t)(sidx > np ? sidx - np : 0) * P.w_other;
+      P.slice_off[sidx] = (uint32_t)std::min<uint64_t>(P.chunk, ((P.chunk * cw) / tw) & ~3ull);
+    }
+  }
   P.n = n;
   scratch = 16ull * 2 * np * P.qstride + 4ull * 2 * np * P.nsrc;
   P.k_mask = p->k - 1;

@@ -193,6 +193,7 @@ def device_keep_table(k: int, cutoff: float):
 
 
 _FINALIZE_SCRATCH: dict = {}  # capacity -> sspd_finalize work-space bytes
+_SM_COUNT: dict = {}  # device -> SMs
 
 
 class DeviceFinalize:
@@ -459,6 +460,20 @@ class DetectorState:
     partitioned_min_packets = 1 << 22
     partitioned_chunk = 0  # 0: library default (8 whole 4096-packet tiles per SM per chunk)
 
+    @staticmethod
+    def _default_chunk() -> int:
+        """Packets per chunk of the partitioned scan's default plan (16 tiles
+        of 4,096 packets per SM)."""
+        import torch
+
+        from ._abi import lib
+
+        dev = torch.cuda.current_device()
+        sms = _SM_COUNT.get(dev)
+        if sms is None:
+            sms = _SM_COUNT[dev] = int(lib().sspd_device_sm_count(dev))
+        return 16 * 4096 * (sms if sms > 0 else 148)
+
     def _scan(self, h_ptr: int, o_ptr: int, n: int):
         from ._abi import ERR_CONFIG, check, lib
         from ._device import call, stream_ptr
@@ -468,14 +483,17 @@ class DetectorState:
         ldca_p = self.ldca.device_buffer().data_ptr()
         if mode == "partitioned" or (mode == "auto" and n >= self.partitioned_min_packets):
             scratch = getattr(self, "_part_scratch", None)
-            need = int(lib().sspd_scan_partitioned_scratch(self.seav._params, self.partitioned_chunk))
+            # a batch smaller than the library's default chunk is ONE chunk of
+            # its own size (smaller bucket scratch, same result)
+            chunk = self.partitioned_chunk or (-(-n // 4) * 4 if n < self._default_chunk() else 0)
+            need = int(lib().sspd_scan_partitioned_scratch(self.seav._params, chunk))
             if scratch is None or scratch.numel() < need:
                 import torch
 
                 scratch = torch.empty(need, dtype=torch.uint8, device=self.ldca.device_buffer().device)
                 self._part_scratch = scratch
             rc = lib().sspd_scan_partitioned(h_ptr, o_ptr, n, self.seav._params, seav_p, ldca_p,
-                                             scratch.data_ptr(), need, self.partitioned_chunk, stream_ptr())
+                                             scratch.data_ptr(), scratch.numel(), chunk, stream_ptr())
             if rc != ERR_CONFIG or mode == "partitioned":
                 check(rc, "sspd_scan_partitioned")
                 self.last_scan = "partitioned"

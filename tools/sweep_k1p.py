@@ -49,7 +49,7 @@ def main():
         st.scan_mode = "direct" if setting == "direct" else "partitioned"
         env = {} if setting == "direct" else dict(kv.split("=", 1) for kv in setting.split(",") if kv)
         st.partitioned_chunk = int(env.pop("chunk", 0))  # packets per chunk (0 = library default)
-        for k in [k for k in os.environ if k.startswith("SSPD_PART_")]:
+        for k in [k for k in os.environ if k.startswith(("SSPD_PART_", "SSPD_BPART_"))]:
             del os.environ[k]
         os.environ.update(env)
         st.reset()
