@@ -434,42 +434,66 @@ def run_gpu(args) -> dict | None:
             dist.destroy_process_group()
         return None
 
-    # roofline: the dominant kernel is K1 (scan).  Algorithmic bytes = 8 B
-    # input per packet; the binding term is the L2 RED rate,
-    # measured live with the scan's own instruction.
+    # roofline of the dominant kernel, the scan.  Algorithmic bytes = the 8 B
+    # input per packet.  Bounds measured live in this
+    # process: the hash floor (every per-packet index hash, no sketch
+    # update: the work K1b is issue-bound on), and the SURVEY's L2-red term.
     import ctypes
 
     peaks = measured_peaks()
+    p_blk = st.seav._params
     buf = torch.empty(8 << 20, dtype=torch.uint8, device=dev)
     red = ctypes.c_double(0.0)
     lib().sspd_microbench_red(buf.data_ptr(), 8 << 20, 8, 256, ctypes.byref(red), stream.cuda_stream)
     red_per_s = red.value
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.empty(2048 * sms, dtype=torch.int32, device=dev)
+    hash_pps = {}
+    for bps in (1, 2):
+        v = ctypes.c_double(0.0)
+        rc = lib().sspd_microbench_hash(hips.data_ptr(), oips.data_ptr(), n, p_blk, bps, sink.data_ptr(),
+                                        ctypes.byref(v), stream.cuda_stream)
+        hash_pps[bps] = v.value if rc == 0 else None
+    del buf, sink
     reds_per_pkt = dp.ldca_config().lr + dp.seav_config().sr / (1 << dp.seav_config().tau)
     scan_pps = n / (scan_ms * 1e-3)
     hbm_gbs = peaks.get("hbm_gbs", 6650.0)
     achieved_gbs = 8 * n / (scan_ms * 1e-3) / 1e9
     roof_pps = min(hbm_gbs * 1e9 / 8, red_per_s / reds_per_pkt)
     kernel = getattr(st, "last_scan", "direct")
-    kname = ("scan_partitioned_kernel<true, kPow2> (K1p, LDCA in shared memory)" if kernel == "partitioned"
-             else "scan_discrete_kernel<true,true> (K1, L2 red.or)")
+    variant = int(lib().sspd_scan_partitioned_variant(p_blk, 0)) if kernel == "partitioned" else 0
+    kkey = {2: "bpart", 1: "partitioned"}.get(variant, "direct")
+    kname = {"bpart": "scan_bpart_kernel<true, 1> (K1b: LDCA in shared memory, cut along b)",
+             "partitioned": "scan_partitioned_kernel<true, kPow2> (K1p, LDCA in shared memory)",
+             "direct": "scan_discrete_kernel<true,true> (K1, L2 red.or)"}[kkey]
     # per-kernel ncu evidence committed under profiles/ (bytes and issue slots per packet)
     prof = {}
     pf = ROOT / "profiles" / "scan_ncu_summary.json"
     if pf.exists():
         try:
-            prof = json.loads(pf.read_text()).get(kernel, {})
+            prof = json.loads(pf.read_text()).get(kkey, {})
         except ValueError:
             prof = {}
     traffic = prof.get("dram_bytes_per_packet")
     traffic = round(traffic * n) if traffic else None
     issue = None
     if prof.get("warp_inst_per_packet"):
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
         clk_hz = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
         issue_pps = sms * 4 * clk_hz / prof["warp_inst_per_packet"]  # 4 schedulers x 1 warp-inst/clk
-        issue = {"bound": "sm_issue", "warp_inst_per_packet": prof["warp_inst_per_packet"],
+        issue = {"bound": "sm_issue", "warp_inst_per_packet": round(prof["warp_inst_per_packet"], 3),
                  "roofline_gpps": round(issue_pps / 1e9, 3), "frac": round(scan_pps / issue_pps, 4),
+                 "issue_slots_busy_pct": prof.get("issue_active_pct"),
                  "source": prof.get("source")}
+    ceiling = hash_pps.get(2) or hash_pps.get(1)
+    binding = None
+    if ceiling:
+        binding = {"bound": "sm_issue: per-packet index hashes (sspd_microbench_hash, live)",
+                   "ceiling_gpps": round(ceiling / 1e9, 3),
+                   "ceiling_gpps_scan_launch_shape": round(hash_pps[1] / 1e9, 3) if hash_pps.get(1) else None,
+                   "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / ceiling, 4),
+                   "note": ("streaming the same pairs and computing H3 % k, the H1 test and the LR row hashes "
+                            "(10 SplitMix64 per packet) with no sketch update, at full occupancy (2 x 1,024 "
+                            "threads per SM); the scan adds the shared-memory partition exchange to this floor")}
 
     value = world * n / (ms * 1e-3) / 1e6
     line = {
@@ -491,18 +515,21 @@ def run_gpu(args) -> dict | None:
                      "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback",
                      "kernel": kname, "algorithmic_bytes_per_packet": 8,
+                     "binding": binding,
                      "note": ("the packet stream is 8 B/pkt, so HBM is far from binding; the scan is bound by "
-                              "SM instruction issue (ten SplitMix64 hashes per packet on the ALU pipe) -- "
-                              "see issue_roofline, and scan_roofline for the SURVEY's L2-atomic roofline; `traffic` is "
-                              "the 8 B/pkt input plus the part of the 32 B/pkt shared-memory bucket exchange that "
-                              "spills from L2 with the default 8-tile chunks (DESIGN.md §3)")},
+                              "SM instruction issue on the ten SplitMix64 index hashes per packet -- `binding` "
+                              "is that floor measured live in this process; `traffic` (ncu, per launch) is the "
+                              "8 B/pkt input plus the part of the 16 B/pkt shared-memory bucket exchange that "
+                              "spills from L2 with 16-tile chunks (DESIGN.md §3)")},
         "scan_roofline": {"bound": "l2_red", "l2_red_ops_per_s": round(red_per_s / 1e9, 2),
                           "reds_per_packet": round(reds_per_pkt, 4), "roofline_gpps": round(roof_pps / 1e9, 3),
                           "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / roof_pps, 4),
                           "scan_ms": round(scan_ms, 4), "scan_share_of_step": round(scan_share, 4),
+                          "l2_red_requests_per_packet_ncu": prof.get("l2_red_requests_per_packet"),
                           "note": ("SURVEY.md §8d roofline min(HBM 8 B/pkt, L2 red.or rate / reds per pkt), red "
-                                   "rate measured live; K1p keeps the LDCA in shared memory so it is not bound "
-                                   "by L2 atomics -- see issue_roofline")},
+                                   "rate measured live -- the bound of the L2-atomic scan K1; the partitioned "
+                                   "scan keeps the LDCA in shared memory and issues only the SEAV reds to L2 "
+                                   "(~0.03 per packet), so this term does not bind it")},
         "issue_roofline": issue,
         "merge": merge,
         "clocks": clk,

@@ -333,6 +333,16 @@ SSPD_API int sspd_route_pairs(const uint32_t* hips, const uint32_t* oips, uint64
  * bench.py for the L2-atomic term of the scan roofline. */
 SSPD_API int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
                         int iters, double* ops_per_s, void* stream);
+/* The scans' compute floor: packets/s of streaming the caller's (16-B
+ * aligned) pairs and evaluating every per-packet hash the partitioned scans
+ * evaluate (H3 % k, the H1 sampling test, LR row hashes % lc; k and lc
+ * powers of two), with no sketch update -- at blocks_per_sm = 1 or 2
+ * CTAs of 1,024 threads per SM (1 = the scans' launch shape, 2 = full
+ * occupancy).  sink: >= 2048 x SMs
+ * words.  The binding roofline of K1b (bench.py `roofline.binding`). */
+SSPD_API int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                  const sspd_params* p, int blocks_per_sm, uint32_t* sink,
+                                  double* pkts_per_s, void* stream);
 /* Random st.global.u16 rate over a `bytes` (power of two) footprint -- the
  * measured roofline term of the sliding scan K2. */
 SSPD_API int sspd_microbench_store16(void* buf, uint64_t bytes, int blocks_per_sm,

@@ -46,6 +46,8 @@ def lib():
             "or_scan": (C.c_int, [P, vp, vp, u64, vp, vp, C.c_int]),
             "or_restore": (C.c_int64, [P, vp, u32, u32, u64, vp, vp, u64, vp]),
             "or_filter": (None, [P, vp, vp, u64, vp]),
+            "or_restore_mt": (C.c_int64, [P, vp, u32, u32, u64, vp, vp, u64, vp, C.c_int]),
+            "or_filter_mt": (None, [P, vp, vp, u64, vp, C.c_int]),
             "or_observe": (None, [P, vp, vp, u64, vp, u32, u64]),
             "or_sweep": (None, [vp, u64, u32, u64, u64, u64]),
             "or_materialize_seav": (None, [P, vp, u32, u64, u64, vp]),
@@ -96,8 +98,10 @@ def scan(params, hips, oips, seav: np.ndarray | None = None, ldca: np.ndarray | 
     return seav, ldca
 
 
-def restore(params, seav: np.ndarray, cap: int, rp_begin: int = 0, rp_count: int | None = None):
-    """(ips, rps, weights, overflow[rp]) sorted by ip (short_sketch.py:347-408)."""
+def restore(params, seav: np.ndarray, cap: int, rp_begin: int = 0, rp_count: int | None = None,
+            threads: int = 1):
+    """(ips, rps, weights, overflow[rp]) sorted by ip (short_sketch.py:347-408);
+    `threads` > 1 restores ranges of SEAs concurrently (same result)."""
     if rp_count is None:
         rp_count = 1 << params.r
     seav = np.ascontiguousarray(seav, dtype=np.uint8)
@@ -106,17 +110,18 @@ def restore(params, seav: np.ndarray, cap: int, rp_begin: int = 0, rp_count: int
     while True:
         ips = np.zeros(capacity, dtype=np.uint32)
         aux = np.zeros(capacity, dtype=np.uint32)
-        n = lib().or_restore(params, _p(seav), rp_begin, rp_count, cap, _p(ips), _p(aux), capacity, _p(over))
+        n = lib().or_restore_mt(params, _p(seav), rp_begin, rp_count, cap, _p(ips), _p(aux), capacity, _p(over),
+                                threads)
         if n <= capacity:
             break
         capacity = n
     return ips[:n], aux[:n] >> 8, aux[:n] & 0xFF, over[:rp_count]
 
 
-def filter_z0(params, ldca: np.ndarray, ips) -> np.ndarray:
+def filter_z0(params, ldca: np.ndarray, ips, threads: int = 1) -> np.ndarray:
     ips = _u32(ips)
     z0 = np.zeros(max(1, len(ips)), dtype=np.uint32)
-    lib().or_filter(params, _p(np.ascontiguousarray(ldca, dtype=np.uint8)), _p(ips), len(ips), _p(z0))
+    lib().or_filter_mt(params, _p(np.ascontiguousarray(ldca, dtype=np.uint8)), _p(ips), len(ips), _p(z0), threads)
     return z0[: len(ips)]
 
 

@@ -96,55 +96,46 @@ void or_ldca_update(const sspd_params* p, const uint32_t* hips, const uint32_t* 
 /* DetectorState.process_batch (window_detector.py:100-103) on nthreads.
  * Work is split by SKETCH ROW (LDCA row i, or the whole SEAV) so each
  * thread's working set is one 1 MiB row that stays in its private cache;
- * when there are more threads than row tasks the packet range is split too
- * and those threads OR with relaxed atomics (exact: OR is monotone). */
+ * the (row task x packet) space is cut into nthreads equal ranges, and a
+ * task shared by several threads is OR-ed with relaxed atomics (exact: OR
+ * is monotone). */
 typedef struct {
   const sspd_params* p;
   const uint32_t* hips;
   const uint32_t* oips;
   uint64_t lo, hi;
   int row;      /* LDCA row, or -1 for the SEAV task */
-  int atomic;
-  uint8_t* seav;
-  uint8_t* ldca;
+  uint8_t* out; /* the LDCA row / the SEAV, or a private zeroed copy of it */
+  uint8_t* dst; /* where a private copy is OR-ed after the join (NULL: out is dst) */
+  uint64_t bytes;
 } or_job;
 
 static void* or_scan_job(void* arg) {
   or_job* j = (or_job*)arg;
   const sspd_params* p = j->p;
   if (j->row < 0) {
-    if (!j->atomic) {
-      for (uint64_t t = j->lo; t < j->hi; ++t) or_seav_pair(p, j->hips[t], j->oips[t], j->seav);
-      return NULL;
-    }
-    for (uint64_t t = j->lo; t < j->hi; ++t) {
-      uint64_t oip = j->oips[t], hip = j->hips[t];
-      uint32_t h1 = (uint32_t)(or_mix64(oip ^ p->seed_h1) & 0xFFFFFFFFull);
-      if (or_lsb32(h1) < (int)p->tau) continue;
-      uint64_t bit = or_hash_range(oip, p->seed_h2, p->g);
-      uint64_t rp = hip & ((1ull << p->r) - 1ull);
-      uint64_t lp = (hip >> p->r) & ((1ull << p->lp_bits) - 1ull);
-      for (uint32_t i = 0; i < p->sr; ++i) {
-        uint64_t col = or_index_of(p, i, lp);
-        uint64_t byte = p->seav_row_off[i] + (rp * p->sc[i] + col) * p->reg_bytes + (bit >> 3);
-        __atomic_fetch_or(&j->seav[byte], (uint8_t)(1u << (bit & 7)), __ATOMIC_RELAXED);
-      }
-    }
+    for (uint64_t t = j->lo; t < j->hi; ++t) or_seav_pair(p, j->hips[t], j->oips[t], j->out);
     return NULL;
   }
   const uint64_t kb = p->k / 8;
-  uint8_t* row = j->ldca + (uint64_t)j->row * p->lc * kb;
   const uint64_t seed = p->seed_lh[j->row];
   for (uint64_t t = j->lo; t < j->hi; ++t) {
     uint64_t b = or_hash_range(j->oips[t], p->seed_h3, p->k);
     uint64_t c = or_hash_range(j->hips[t], seed, p->lc);
-    uint8_t* cell = row + c * kb + (b >> 3);
-    uint8_t m = (uint8_t)(1u << (b & 7));
-    if (j->atomic)
-      __atomic_fetch_or(cell, m, __ATOMIC_RELAXED);
-    else
-      *cell |= m;
+    j->out[c * kb + (b >> 3)] |= (uint8_t)(1u << (b & 7));
   }
+  return NULL;
+}
+
+/* one thread's jobs (at most a few), run in order */
+typedef struct {
+  or_job* jobs;
+  int count;
+} or_run;
+
+static void* or_run_jobs(void* a) {
+  or_run* r = (or_run*)a;
+  for (int i = 0; i < r->count; ++i) or_scan_job(&r->jobs[i]);
   return NULL;
 }
 
@@ -157,32 +148,63 @@ int or_scan(const sspd_params* p, const uint32_t* hips, const uint32_t* oips, ui
     }
     return 0;
   }
-  int tasks = (ldca ? (int)p->lr : 0) + (seav ? 1 : 0);
-  int parts = nthreads / tasks;
-  if (parts < 1) parts = 1;
-  int total = tasks * parts;
-  pthread_t* th = (pthread_t*)calloc(total, sizeof(pthread_t));
-  or_job* jobs = (or_job*)calloc(total, sizeof(or_job));
-  int q = 0;
-  for (int t = 0; t < tasks; ++t) {
-    for (int part = 0; part < parts; ++part, ++q) {
-      jobs[q].p = p;
-      jobs[q].hips = hips;
-      jobs[q].oips = oips;
-      jobs[q].lo = n * part / parts;
-      jobs[q].hi = n * (part + 1) / parts;
-      jobs[q].row = (ldca && t < (int)p->lr) ? t : -1;
-      jobs[q].atomic = parts > 1;
-      jobs[q].seav = seav;
-      jobs[q].ldca = ldca;
+  /* the (task, packet) work space is cut into nthreads equal contiguous
+   * ranges, so every thread is busy; a task covered by several ranges is
+   * scanned into private zeroed copies that are OR-ed in after the join
+   * (exact: OR is commutative and idempotent) */
+  const int tasks = (ldca ? (int)p->lr : 0) + (seav ? 1 : 0);
+  if (tasks == 0) return 0;
+  const uint64_t units = (uint64_t)tasks * n;
+  const uint64_t row_bytes = (uint64_t)p->lc * (p->k / 8);
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  or_job* jobs = (or_job*)calloc((size_t)nthreads + (size_t)tasks + 1, sizeof(or_job));  /* pieces <= tasks + nthreads - 1 */
+  int* first = (int*)calloc((size_t)nthreads + 1, sizeof(int));
+  int nj = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    const uint64_t u0 = units * (uint64_t)t / (uint64_t)nthreads, u1 = units * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    first[t] = nj;
+    for (uint64_t u = u0; u < u1;) {
+      const int task = (int)(u / n);
+      const uint64_t lo = u - (uint64_t)task * n;
+      const uint64_t hi = (u1 - (uint64_t)task * n) < n ? (u1 - (uint64_t)task * n) : n;
+      or_job* j = &jobs[nj++];
+      j->p = p;
+      j->hips = hips;
+      j->oips = oips;
+      j->lo = lo;
+      j->hi = hi;
+      j->row = (ldca && task < (int)p->lr) ? task : -1;
+      uint8_t* target = j->row >= 0 ? ldca + (uint64_t)j->row * row_bytes : seav;
+      j->bytes = j->row >= 0 ? row_bytes : p->seav_bytes;
+      if (lo == 0 && hi == n) {
+        j->out = target;
+        j->dst = NULL;
+      } else {
+        j->out = (uint8_t*)calloc(j->bytes, 1);
+        j->dst = target;
+      }
+      u = (uint64_t)task * n + hi;
     }
   }
-  /* more threads than tasks x parts would idle; fewer run in waves */
-  for (int base = 0; base < total; base += nthreads) {
-    int end = base + nthreads < total ? base + nthreads : total;
-    for (int t = base; t < end; ++t) pthread_create(&th[t], NULL, or_scan_job, &jobs[t]);
-    for (int t = base; t < end; ++t) pthread_join(th[t], NULL);
+  first[nthreads] = nj;
+  or_run* runs = (or_run*)calloc((size_t)nthreads, sizeof(or_run));
+  for (int t = 0; t < nthreads; ++t) {
+    runs[t].jobs = &jobs[first[t]];
+    runs[t].count = first[t + 1] - first[t];
   }
+  for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, or_run_jobs, &runs[t]);
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  for (int q = 0; q < nj; ++q) {
+    if (!jobs[q].dst) continue;
+    uint64_t* d = (uint64_t*)jobs[q].dst;
+    const uint64_t* s8 = (const uint64_t*)jobs[q].out;
+    uint64_t words = jobs[q].bytes / 8, tail = jobs[q].bytes % 8;
+    for (uint64_t i = 0; i < words; ++i) d[i] |= s8[i];
+    for (uint64_t i = 0; i < tail; ++i) jobs[q].dst[words * 8 + i] |= jobs[q].out[words * 8 + i];
+    free(jobs[q].out);
+  }
+  free(runs);
+  free(first);
   free(th);
   free(jobs);
   return 0;
@@ -333,17 +355,116 @@ int64_t or_restore(const sspd_params* p, const uint8_t* seav, uint32_t rp_begin,
 void or_filter(const sspd_params* p, const uint8_t* ldca, const uint32_t* ips, uint64_t n, uint32_t* z0) {
   uint64_t kb = p->k / 8;
   for (uint64_t j = 0; j < n; ++j) {
+    uint64_t cell[SSPD_MAX_LR];
+    for (uint32_t i = 0; i < p->lr; ++i) cell[i] = (uint64_t)i * p->lc + or_hash_range(ips[j], p->seed_lh[i], p->lc);
     uint32_t pop = 0;
     for (uint64_t by = 0; by < kb; ++by) {
       uint8_t acc = 0xFF;
-      for (uint32_t i = 0; i < p->lr; ++i) {
-        uint64_t c = or_hash_range(ips[j], p->seed_lh[i], p->lc);
-        acc &= ldca[((uint64_t)i * p->lc + c) * kb + by];
-      }
+      for (uint32_t i = 0; i < p->lr; ++i) acc &= ldca[cell[i] * kb + by];
       pop += (uint32_t)__builtin_popcount(acc);
     }
     z0[j] = p->k - pop;
   }
+}
+
+/* ---- the same restore / filter on nthreads (CPU baseline) --------------
+ * Restore: SEAs are independent, so the rp range is cut into nthreads
+ * contiguous pieces restored concurrently, then the candidates are merged
+ * and sorted by ip exactly as or_restore does.  Filter: candidates cut into
+ * nthreads pieces. */
+typedef struct {
+  const sspd_params* p;
+  const uint8_t* seav;
+  uint32_t rp_begin, rp_count;
+  uint64_t cap;
+  uint8_t* overflow;
+  uint32_t* ip;
+  uint32_t* w;
+  int64_t n;
+} or_restore_job;
+
+static void* or_restore_run(void* a) {
+  or_restore_job* j = (or_restore_job*)a;
+  uint64_t capacity = 1024;
+  for (;;) {
+    j->ip = (uint32_t*)realloc(j->ip, sizeof(uint32_t) * capacity);
+    j->w = (uint32_t*)realloc(j->w, sizeof(uint32_t) * capacity);
+    j->n = or_restore(j->p, j->seav, j->rp_begin, j->rp_count, j->cap, j->ip, j->w, capacity, j->overflow);
+    if ((uint64_t)j->n <= capacity) break;
+    capacity = (uint64_t)j->n;
+  }
+  return NULL;
+}
+
+int64_t or_restore_mt(const sspd_params* p, const uint8_t* seav, uint32_t rp_begin, uint32_t rp_count, uint64_t cap,
+                      uint32_t* out_ip, uint32_t* out_w, uint64_t out_cap, uint8_t* overflow, int nthreads) {
+  if (nthreads <= 1 || rp_count < 2 * (uint32_t)nthreads)
+    return or_restore(p, seav, rp_begin, rp_count, cap, out_ip, out_w, out_cap, overflow);
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  or_restore_job* jobs = (or_restore_job*)calloc((size_t)nthreads, sizeof(or_restore_job));
+  for (int t = 0; t < nthreads; ++t) {
+    const uint32_t a = (uint32_t)((uint64_t)rp_count * t / nthreads), b = (uint32_t)((uint64_t)rp_count * (t + 1) / nthreads);
+    jobs[t].p = p;
+    jobs[t].seav = seav;
+    jobs[t].rp_begin = rp_begin + a;
+    jobs[t].rp_count = b - a;
+    jobs[t].cap = cap;
+    jobs[t].overflow = overflow ? overflow + a : NULL;
+    pthread_create(&th[t], NULL, or_restore_run, &jobs[t]);
+  }
+  uint64_t nall = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    pthread_join(th[t], NULL);
+    nall += (uint64_t)jobs[t].n;
+  }
+  uint64_t* all = (uint64_t*)malloc(sizeof(uint64_t) * (nall ? nall : 1));
+  uint64_t q = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    for (int64_t i = 0; i < jobs[t].n; ++i) all[q++] = ((uint64_t)jobs[t].ip[i] << 32) | jobs[t].w[i];
+    free(jobs[t].ip);
+    free(jobs[t].w);
+  }
+  qsort(all, nall, sizeof(uint64_t), cmp_u64);
+  for (uint64_t t = 0; t < nall && t < out_cap; ++t) {
+    out_ip[t] = (uint32_t)(all[t] >> 32);
+    out_w[t] = (uint32_t)(all[t] & 0xFFFFFFFFu);
+  }
+  free(all);
+  free(jobs);
+  free(th);
+  return (int64_t)nall;
+}
+
+typedef struct {
+  const sspd_params* p;
+  const uint8_t* ldca;
+  const uint32_t* ips;
+  uint64_t n;
+  uint32_t* z0;
+} or_filter_job;
+
+static void* or_filter_run(void* a) {
+  or_filter_job* j = (or_filter_job*)a;
+  or_filter(j->p, j->ldca, j->ips, j->n, j->z0);
+  return NULL;
+}
+
+void or_filter_mt(const sspd_params* p, const uint8_t* ldca, const uint32_t* ips, uint64_t n, uint32_t* z0,
+                  int nthreads) {
+  if (nthreads <= 1 || n < 64) {
+    or_filter(p, ldca, ips, n, z0);
+    return;
+  }
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  or_filter_job* jobs = (or_filter_job*)calloc((size_t)nthreads, sizeof(or_filter_job));
+  for (int t = 0; t < nthreads; ++t) {
+    const uint64_t a = n * (uint64_t)t / (uint64_t)nthreads, b = n * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    jobs[t] = (or_filter_job){p, ldca, ips + a, b - a, z0 + a};
+    pthread_create(&th[t], NULL, or_filter_run, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(jobs);
+  free(th);
 }
 
 /* ---- sliding (sliding.py:24-248) -------------------------------------- */

@@ -36,9 +36,98 @@ __global__ void __launch_bounds__(256) microbench_store16_kernel(uint16_t* buf, 
   }
 }
 
+// The scan's compute floor: stream (hip, oip) pairs with the scan's 16-byte
+// loads and evaluate exactly the hashes the partitioned scans evaluate per
+// packet -- H3 % k, the H1 sampling test and LR row hashes % lc (split-seed
+// SplitMix64, sspd_common.cuh) -- with no sketch update at all.  The packets/s
+// it reaches bound any scan that must compute these indexes (SURVEY.md
+// §8(a) a1-a2): K1b is issue-bound on exactly this work.
+struct HashSeeds {
+  uint32_t s_lo[2 + SSPD_MAX_LR], s_hg[2 + SSPD_MAX_LR];
+  uint32_t lr, k_mask, lc_mask, tmask;
+};
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(1024, kMinBlocks)
+    microbench_hash_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips, uint64_t nq,
+                           const __grid_constant__ HashSeeds S, uint32_t* sink) {
+  uint32_t acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(hips) + q);
+    const uint4 ov = __ldcs(reinterpret_cast<const uint4*>(oips) + q);
+    const uint32_t h[4] = {hv.x, hv.y, hv.z, hv.w}, o[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t v = mix64_lo_split(o[e], S.s_lo[0], S.s_hg[0]) & S.k_mask;
+      v ^= (mix64_lo_split(o[e], S.s_lo[1], S.s_hg[1]) & S.tmask) == 0u ? 0x80000000u : 0u;
+#pragma unroll 8
+      for (uint32_t i = 0; i < S.lr; ++i) v += (mix64_lo_split(h[e], S.s_lo[2 + i], S.s_hg[2 + i]) & S.lc_mask) << i;
+      acc ^= v;
+    }
+  }
+  sink[(uint64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 }  // namespace sspd
 
 using namespace sspd;
+
+// Hash-floor packets/s of the scans over the caller's packets (n % 4 == 0
+// used, 16-byte aligned), at `blocks_per_sm` CTAs of 1,024 threads per SM
+// (1 = the partitioned scans' launch shape, 2 = full occupancy: 32
+// registers per thread); sink: >= 2048 * SMs words.  Best of 5 after one
+// warm-up.
+extern "C" int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                                    int blocks_per_sm, uint32_t* sink, double* pkts_per_s, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!hips || !oips || !sink || !pkts_per_s || n < 4) return SSPD_ERR_DATA;
+  if (((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) != 0) return SSPD_ERR_DATA;
+  if ((p->k & (p->k - 1)) || (p->lc & (p->lc - 1))) return SSPD_ERR_CONFIG;  // masks, as the scans' fast modes
+  if (blocks_per_sm != 1 && blocks_per_sm != 2) return SSPD_ERR_CONFIG;
+  HashSeeds S;
+  const uint64_t seeds[2] = {p->seed_h3, p->seed_h1};
+  for (int i = 0; i < 2 + (int)p->lr; ++i) {
+    const uint64_t sd = i < 2 ? seeds[i] : p->seed_lh[i - 2];
+    S.s_lo[i] = (uint32_t)sd;
+    S.s_hg[i] = (uint32_t)(sd >> 32) + (uint32_t)(kGolden >> 32);
+  }
+  S.lr = p->lr;
+  S.k_mask = p->k - 1;
+  S.lc_mask = p->lc - 1;
+  S.tmask = tau_mask(p->tau);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t nq = n / 4;
+  const int threads = 1024, grid = sms * blocks_per_sm;
+  auto launch = [&]() {
+    if (blocks_per_sm == 1)
+      microbench_hash_kernel<1><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+    else
+      microbench_hash_kernel<2><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+  };
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  launch();  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(a, st);
+    launch();
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *pkts_per_s = (double)(nq * 4) / (best * 1e-3);
+  return check_launch();
+}
 
 extern "C" int sspd_abi_version(void) { return SSPD_ABI_VERSION; }
 
