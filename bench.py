@@ -165,21 +165,71 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- reference arm
+def reference_python(hips, oips, dp) -> dict | None:
+    """The reference package itself (baseline/_ref, pure Python + numpy) on
+    the host: one process over a 2^20-pair prefix, and P = host-core
+    processes, each a watch point over 1/P of the sample, merged with
+    serialize -> merge_frames -> finalize_window."""
+    from oracle import oracle
+    from tools import reference_cpu
+
+    if not reference_cpu.available():
+        return None
+    geom = dict(theta=dp.theta, r=dp.r, k=dp.k, lr=dp.lr, lc=dp.lc, design_n=dp.design_n)
+    n1 = min(len(hips), 1 << 20)
+    single = reference_cpu.time_single(geom, hips[:n1], oips[:n1])
+    procs = max(1, min(oracle.cpu_threads(), 64))
+    n = len(hips) - len(hips) % procs
+    per = n // procs
+    multi = reference_cpu.time_multi(geom, [(hips[i * per:(i + 1) * per], oips[i * per:(i + 1) * per])
+                                            for i in range(procs)], procs)
+    return {"single_process": single, "processes": multi,
+            "source": "baseline/_ref: the reference sspd package (pip-installed from its source), "
+                      "DetectorState.process_batch in 65,536-pair buffers + finalize_window; "
+                      "P processes: serialize -> merge_frames -> finalize_window",
+            "sample": f"config-2 law, single: first {n1} pairs; processes: {procs} x {per} pairs"}
+
+
+def _config2_host(scale: int):
+    """The config-2 stream at 1/scale on the host (generated on the GPU when
+    one is present -- the torch and numpy generators are bit-identical --
+    because the numpy generator needs ~80 s for the full window)."""
+    import numpy as np
+
+    from tools.workloads import CONFIG2, generate, scaled
+
+    spec = scaled(CONFIG2, scale) if scale > 1 else CONFIG2
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            h, o, _ = generate(spec, "torch", torch.device("cuda", 0))
+            out = h.cpu().numpy().view(np.uint32).copy(), o.cpu().numpy().view(np.uint32).copy()
+            del h, o
+            torch.cuda.empty_cache()
+            return spec, out[0], out[1]
+    except Exception:  # noqa: BLE001 - no usable GPU: numpy generator
+        pass
+    h, o, _ = generate(spec)
+    return spec, h, o
+
+
 def run_reference(args) -> dict:
-    """The reference path on the host: oracle port, all host threads."""
+    """The reference path on the host: the oracle port (C restatement of the
+    reference's algorithm, oracle/sspd_oracle.c) on all host threads over
+    the FULL config-2 window (same workload as the GPU arm), plus the
+    reference package itself timed on a bounded prefix (reference_python)."""
     import numpy as np
 
     from oracle import oracle
     from paper_1901_07306_b200._abi import build_params
     from paper_1901_07306_b200.hashing import SeedFamily
-    from tools.workloads import CONFIG2, generate, scaled
 
     dp = detector_params()
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         p = build_params(dp.seav_config(), dp.ldca_config(), SeedFamily(dp.master_seed))
-    spec = scaled(CONFIG2, args.cpu_scale)
-    hips, oips, _ = generate(spec)
+    spec, hips, oips = _config2_host(args.ref_scale)
     threads = oracle.cpu_threads()
     seav = np.zeros(p.seav_bytes, dtype=np.uint8)
     ldca = np.zeros(p.ldca_bytes, dtype=np.uint8)
@@ -188,8 +238,8 @@ def run_reference(args) -> dict:
         seav.fill(0)
         ldca.fill(0)
         oracle.scan(p, hips, oips, seav, ldca, threads=threads)
-        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
-        oracle.filter_z0(p, ldca, ips)
+        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap, threads=threads)
+        oracle.filter_z0(p, ldca, ips, threads=threads)
 
     for _ in range(args.warmup):
         step()
@@ -198,34 +248,37 @@ def run_reference(args) -> dict:
         step()
     dt = (time.perf_counter() - t0) / args.steps
     mpps = len(hips) / dt / 1e6
-    sample = f"{spec.name}: {len(hips)} pkts of the config-2 law (1/{args.cpu_scale} scale), scan+restore+filter"
+    full = args.ref_scale <= 1
+    sample = (f"the full config-2 window ({len(hips)} pairs) per step" if full else
+              f"{len(hips)} pairs of the config-2 law (1/{args.ref_scale}) per step") + \
+        ", scan + restore + filter, oracle port on all host threads"
     return {
         "metric": METRIC, "value": round(mpps, 3), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u8 (integer)",
         "data": "synthetic (seeded, tools/workloads.py)",
-        "config": {"workload": WORKLOAD, "global_batch": len(hips), "parallelism": "host threads"},
+        "config": {"workload": WORKLOAD, "global_batch": len(hips), "parallelism": "host threads",
+                   "same_config": full},
         "cpu_baseline": {"value": round(mpps, 3), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "reference_python": reference_python(hips, oips, dp)},
         "e2e": {"value": round(mpps, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
 def cpu_baseline_quick(scale: int) -> dict:
-    """Bounded CPU sample for the b200 line's cpu_baseline (rank 0, N=1)."""
+    """Bounded CPU sample for the b200 line's cpu_baseline (rank 0, N=1):
+    the oracle port on all host threads, plus the reference package itself."""
     import numpy as np
 
     from oracle import oracle
     from paper_1901_07306_b200._abi import build_params
     from paper_1901_07306_b200.hashing import SeedFamily
-    from tools.workloads import CONFIG2, generate, scaled
 
     dp = detector_params()
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         p = build_params(dp.seav_config(), dp.ldca_config(), SeedFamily(dp.master_seed))
-    spec = scaled(CONFIG2, scale)
-    hips, oips, _ = generate(spec)
+    spec, hips, oips = _config2_host(scale)
     threads = oracle.cpu_threads()
     best = None
     for _ in range(2):
@@ -233,12 +286,14 @@ def cpu_baseline_quick(scale: int) -> dict:
         ldca = np.zeros(p.ldca_bytes, dtype=np.uint8)
         t0 = time.perf_counter()
         oracle.scan(p, hips, oips, seav, ldca, threads=threads)
-        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
-        oracle.filter_z0(p, ldca, ips)
+        ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap, threads=threads)
+        oracle.filter_z0(p, ldca, ips, threads=threads)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     return {"value": round(len(hips) / best / 1e6, 3), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{len(hips)} pkts of the config-2 law (1/{scale} scale), scan+restore+filter, best of 2"}
+            "sample": f"{len(hips)} pkts of the config-2 law (1/{scale} scale), scan+restore+filter on "
+                      f"{threads} threads, best of 2",
+            "reference_python": reference_python(hips, oips, dp)}
 
 
 def merge_summary(merger, merge_ms: list[float], dist, dev, args) -> dict:
@@ -999,6 +1054,8 @@ def main():
     ap.add_argument("--packets", type=int, default=0, help="override packets per window (debug)")
     ap.add_argument("--chunk", type=int, default=1 << 23, help="e2e staging chunk (pairs)")
     ap.add_argument("--cpu-scale", type=int, default=32, help="CPU sample = config 2 / scale")
+    ap.add_argument("--ref-scale", type=int, default=1,
+                    help="--impl reference: config 2 / scale per step (1 = the full window)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "direct", "partitioned"])
