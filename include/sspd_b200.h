@@ -93,6 +93,16 @@ SSPD_API int sspd_device_sm_count(int device);   /* -1 when no device is availab
 SSPD_API uint64_t sspd_hash_range_host(uint64_t key, uint64_t seed, const sspd_divisor* d);
 SSPD_API uint64_t sspd_mix64_host(uint64_t x);                   /* hashing.py:48-53 */
 
+/* ---- host staging of caller key arrays (no device work) ----------------
+ * DetectorState.process_batch from host memory (the reference's own call
+ * pattern: 65,536-pair numpy buffers, cli.py:215-217) stages the keys in
+ * pinned memory and scans them in large batches.  sspd_host_check_u32 =
+ * SSPD_ERR_DATA if any of n keys (elem_bytes 1/2/4/8, signed or not) lies
+ * outside [0, 2^32) -- the IPv4-only contract, checked before anything is
+ * staged; sspd_host_pack_u32 = narrow n checked keys into dst (u32). */
+SSPD_API int sspd_host_check_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed);
+SSPD_API int sspd_host_pack_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed, uint32_t* dst);
+
 /* ---- K1 discrete scan --------------------------------------------------
  * Replaces DetectorState.process_batch (window_detector.py:100-103) =
  * SeavSketch.update_batch (short_sketch.py:300-318) +

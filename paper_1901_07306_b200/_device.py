@@ -81,3 +81,26 @@ def ips_to_device(a, name: str = "ips"):
 
 def call(name: str, *args):
     check(getattr(lib(), name)(*args), name)
+
+
+class PreReadHook:
+    """Mixin for the device-resident sketches: reading `_buf` (every access
+    path to the payload -- device_buffer(), rows/data, payload_bytes, merge,
+    restore, finalize, ...) first runs `_pre_read`, a weak reference to the
+    owning DetectorState's flush of host batches it has staged but not yet
+    scanned, so no reader ever sees a sketch missing staged packets."""
+
+    _pre_read = None
+
+    @property
+    def _buf(self):
+        hook = self._pre_read
+        if hook is not None:
+            fn = hook()
+            if fn is not None:
+                fn()
+        return self.__dict__["_buf_t"]
+
+    @_buf.setter
+    def _buf(self, value):
+        self.__dict__["_buf_t"] = value

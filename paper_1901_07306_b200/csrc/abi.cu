@@ -129,6 +129,53 @@ extern "C" int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, 
   return check_launch();
 }
 
+// ---- host staging of caller arrays (DetectorState.process_batch from host
+// memory): IPv4 keys of any integer width narrowed to u32 in one pass, so a
+// 65,536-pair numpy batch costs one read + one write of host memory.
+template <typename T>
+static int check_u32_range(const T* s, uint64_t n) {
+  uint64_t bad = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t v = (uint64_t)s[i];  // negative values wrap to >= 2^63
+    bad |= v >> 32;
+  }
+  return bad ? SSPD_ERR_DATA : SSPD_OK;
+}
+
+extern "C" int sspd_host_check_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed) {
+  if (n == 0) return SSPD_OK;
+  if (!src) return SSPD_ERR_DATA;
+  switch (elem_bytes * 2 + (is_signed ? 1 : 0)) {
+    case 2: case 4: return SSPD_OK;                              // u8 / u16
+    case 3: return check_u32_range(static_cast<const int8_t*>(src), n);
+    case 5: return check_u32_range(static_cast<const int16_t*>(src), n);
+    case 8: return SSPD_OK;                                      // u32
+    case 9: return check_u32_range(static_cast<const int32_t*>(src), n);
+    case 16: return check_u32_range(static_cast<const uint64_t*>(src), n);
+    case 17: return check_u32_range(static_cast<const int64_t*>(src), n);
+    default: return SSPD_ERR_CONFIG;
+  }
+}
+
+template <typename T>
+static void pack_u32(const T* s, uint64_t n, uint32_t* d) {
+  for (uint64_t i = 0; i < n; ++i) d[i] = (uint32_t)s[i];
+}
+
+extern "C" int sspd_host_pack_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed, uint32_t* dst) {
+  if (n == 0) return SSPD_OK;
+  if (!src || !dst) return SSPD_ERR_DATA;
+  switch (elem_bytes) {
+    case 1: pack_u32(static_cast<const uint8_t*>(src), n, dst); break;
+    case 2: pack_u32(static_cast<const uint16_t*>(src), n, dst); break;
+    case 4: memcpy(dst, src, n * 4); break;
+    case 8: pack_u32(static_cast<const uint64_t*>(src), n, dst); break;
+    default: return SSPD_ERR_CONFIG;
+  }
+  (void)is_signed;  // the bit pattern of a checked key is the same either way
+  return SSPD_OK;
+}
+
 extern "C" int sspd_abi_version(void) { return SSPD_ABI_VERSION; }
 
 extern "C" size_t sspd_params_size(void) { return sizeof(sspd_params); }

@@ -24,6 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._abi import build_params
+from ._device import PreReadHook
 from .errors import ConfigError, SeaOverflowError
 from .hashing import SeedFamily, hash_full, hash_range, lsb
 
@@ -222,7 +223,7 @@ class CandidateHost:
 
 
 # ------------------------------------------------------------------ sketch
-class SeavSketch:
+class SeavSketch(PreReadHook):
     """Device-resident SEAV with the reference's API (short_sketch.py:259-408).
 
     Updates are monotone bit-sets (device `red.or`), so permutation,

@@ -632,6 +632,19 @@ class SlidingDetector:
              stream_ptr())
         return ldc_estimate(int(z0.item()) & 0xFFFFFFFF, self.ldca_config.k)
 
+    def views_into(self, seav_sketch, ldca_view):
+        """Write the current active-bit views -- SEAV registers into
+        `seav_sketch` (a SeavSketch of this geometry) and the packed LDCA
+        into `ldca_view` (device bytes) -- as detect() builds them (the
+        multi-GPU SlidingMerger ORs these across ranks)."""
+        self._ldca_view_into(ldca_view)
+        sv = self._seav_view()
+        if sv is not seav_sketch:
+            dst = seav_sketch.device_buffer()
+            src = sv.device_buffer()
+            n = min(dst.numel(), src.numel())
+            dst[:n].copy_(src[:n])
+
     @traced("detect")
     def detect(self, beta: float | None = None) -> list[DetectionReport]:
         """Materialise (K4: SEAV registers + packed LDCA) -> fused finalize

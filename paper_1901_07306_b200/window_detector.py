@@ -443,16 +443,121 @@ class DetectorState:
 
     @traced("scan")
     def process_batch(self, hips, oips):
-        """K1: one fused pass updating both sketches (window_detector.py:100-103)."""
-        from ._device import call, ips_to_device, stream_ptr
+        """K1: one fused pass updating both sketches (window_detector.py:100-103).
+
+        Host arrays (the reference's own call pattern: 65,536-pair numpy
+        buffers, cli.py:215-217, distributed.py:225-227) are staged in pinned
+        memory and scanned in batches of `host_stage_pairs` by the
+        partitioned scan (see `_stage_host`); device tensors are scanned at
+        once."""
+        from ._device import ips_to_device
         from .errors import ConfigError
 
+        if self.coalesce_host_batches and _is_host(hips) and _is_host(oips):
+            self._stage_host(hips, oips)
+            return
         h = ips_to_device(hips, "hips")
         o = ips_to_device(oips, "oips")
         if h.numel() != o.numel():
             raise ConfigError("hips and oips differ in length")
         self._scan(h.data_ptr(), o.data_ptr(), int(h.numel()))
         self.pair_count += int(h.numel())
+
+    # host-array batches are staged in pinned memory and scanned together
+    # (class attributes, not dataclass fields)
+    coalesce_host_batches = True
+    host_stage_pairs = 1 << 23
+
+    def _stage_host(self, hips, oips):
+        """Append a host batch to the pinned staging buffer (one narrowing
+        copy, keys checked first: nothing is staged from a rejected batch);
+        a full buffer is copied to the device on a copy stream and scanned
+        there while the host fills the other buffer.  Every read of either
+        sketch (PreReadHook), reset and finalize apply or drop what is
+        pending first, so the state any reader sees is exactly the
+        reference's after the same process_batch calls (OR commutes)."""
+        from ._abi import check, lib
+        from .errors import ConfigError, DataError
+
+        h, o = _host_array(hips, "hips"), _host_array(oips, "oips")
+        n = int(h.shape[0])
+        if n != int(o.shape[0]):
+            raise ConfigError("hips and oips differ in length")
+        L = lib()
+        for a, name in ((h, "hips"), (o, "oips")):
+            if L.sspd_host_check_u32(a.ctypes.data, n, a.dtype.itemsize, 1 if a.dtype.kind == "i" else 0):
+                raise DataError(f"{name}: IPv4 keys must lie in [0, 2^32)")
+        hs = self._host_stage_state()
+        pos = 0
+        while pos < n:
+            take = min(hs["cap"] - hs["fill"], n - pos)
+            b, off = hs["b"], 4 * hs["fill"]
+            for a, dst in ((h, hs["ph"][b]), (o, hs["po"][b])):
+                check(L.sspd_host_pack_u32(a.ctypes.data + pos * a.dtype.itemsize, take, a.dtype.itemsize,
+                                           1 if a.dtype.kind == "i" else 0, dst.data_ptr() + off),
+                      "sspd_host_pack_u32")
+            hs["fill"] += take
+            pos += take
+            if hs["fill"] == hs["cap"]:
+                self._flush_host()
+        self.pair_count += n
+
+    def _host_stage_state(self):
+        import weakref
+
+        import torch
+
+        from ._device import device
+
+        hs = getattr(self, "_hstage", None)
+        if hs is None or hs["cap"] != self.host_stage_pairs:
+            if hs is not None:
+                self._flush_host()
+            cap, dev = int(self.host_stage_pairs), device()
+            pin = lambda: torch.empty(cap, dtype=torch.int32, pin_memory=True)  # noqa: E731
+            dbuf = lambda: torch.empty(cap, dtype=torch.int32, device=dev)  # noqa: E731
+            hs = self._hstage = {"cap": cap, "fill": 0, "b": 0, "ph": [pin(), pin()], "po": [pin(), pin()],
+                                 "dh": [dbuf(), dbuf()], "do": [dbuf(), dbuf()],
+                                 "copied": [None, None], "free": [None, None],
+                                 "stream": torch.cuda.Stream(device=dev)}
+        hook = weakref.WeakMethod(self._flush_host)
+        if self.seav._pre_read is None or self.seav._pre_read() != self._flush_host:
+            self.seav._pre_read = hook
+        if self.ldca._pre_read is None or self.ldca._pre_read() != self._flush_host:
+            self.ldca._pre_read = hook
+        return hs
+
+    def _flush_host(self):
+        """Scan the staged host pairs (H2D on the copy stream, scan on the
+        caller's stream); the host may refill the other buffer meanwhile."""
+        import torch
+
+        hs = getattr(self, "_hstage", None)
+        if hs is None or hs["fill"] == 0:
+            return
+        m, b = hs["fill"], hs["b"]
+        hs["fill"] = 0  # first: the scan below reads the sketches (re-entrant hook)
+        compute = torch.cuda.current_stream()
+        cs = hs["stream"]
+        if hs["free"][b] is not None:
+            cs.wait_event(hs["free"][b])  # the scan that last read device buffer b is done
+        with torch.cuda.stream(cs):
+            hs["dh"][b][:m].copy_(hs["ph"][b][:m], non_blocking=True)
+            hs["do"][b][:m].copy_(hs["po"][b][:m], non_blocking=True)
+            ev = hs["copied"][b] = torch.cuda.Event()
+            ev.record(cs)
+        compute.wait_event(ev)
+        self._scan(hs["dh"][b].data_ptr(), hs["do"][b].data_ptr(), m)
+        fr = hs["free"][b] = torch.cuda.Event()
+        fr.record(compute)
+        hs["b"] = b ^ 1
+        if hs["copied"][b ^ 1] is not None:
+            hs["copied"][b ^ 1].synchronize()  # its pinned buffers are written next
+
+    def _drop_host(self):
+        hs = getattr(self, "_hstage", None)
+        if hs is not None:
+            hs["fill"] = 0
 
     # "auto": the shared-memory partitioned scan (K1p) for large batches when
     # the LDCA fits in the SMs' shared memory, else the direct L2 scan (K1).
@@ -593,10 +698,37 @@ class DetectorState:
         return PendingReports(lambda: fin.reports(wid, source))
 
     def reset(self):
+        self._drop_host()  # staged pairs of the window being cleared need no scan
         self.seav.clear()
         self.ldca.clear()
         self.window_id += 1
         self.pair_count = 0
+
+
+def _is_host(a) -> bool:
+    """A host array argument (numpy, a sequence, or a CPU torch tensor)."""
+    import torch
+
+    if isinstance(a, torch.Tensor):
+        return a.device.type == "cpu"
+    return isinstance(a, (np.ndarray, list, tuple))
+
+
+def _host_array(a, name: str) -> np.ndarray:
+    """Contiguous 1-D integer numpy view of a host key array (no copy when
+    it already is one)."""
+    import torch
+
+    from .errors import DataError
+
+    if isinstance(a, torch.Tensor):
+        a = a.contiguous().numpy()
+        if a.dtype == np.int32:  # torch int32 carries the uint32 bit pattern (ips_to_device)
+            a = a.view(np.uint32)
+    arr = np.ascontiguousarray(np.asarray(a)).reshape(-1)
+    if arr.dtype.kind not in "ui":
+        raise DataError(f"{name}: integer array expected, got {arr.dtype}")
+    return arr
 
 
 def _host_u32_tensor(a, name: str):

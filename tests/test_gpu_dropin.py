@@ -339,3 +339,69 @@ def test_detect_after_everything_expired_is_empty(cuda):  # :199-207
     for _ in range(4):
         det.advance_slice()
     assert det.detect() == []
+
+
+# --- the reference's own call pattern: 65,536-pair host buffers (cli.py:215-217)
+@pytest.mark.parametrize("stage", [1 << 23, 100_003])
+def test_host_batches_staged_bit_exact_vs_oracle(cuda, oracle, stage):
+    """process_batch fed host arrays the way `sspd detect` and
+    simulate_window feed it (65,536-pair buffers; uint64 like the
+    reference's astype, plus uint32 and CPU-tensor batches) is staged in
+    pinned memory and scanned in large batches.  Reads in the middle
+    (payload_bytes, rows, finalize), device-tensor batches interleaved, a
+    rejected batch (nothing of it staged) and reset (staged pairs dropped)
+    all see exactly the reference's state; `stage` = 100,003 forces many
+    flushes through both staging buffers."""
+    import torch
+
+    from conftest import params_block
+    from paper_1901_07306_b200 import DetectorParams
+    from paper_1901_07306_b200.errors import DataError
+
+    dp = DetectorParams(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=2e6)
+    _, _, p = params_block(dp)
+    rng = np.random.default_rng(31)
+    n = 1_500_000
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    hips[:300_000] = rng.integers(0, 2**32, size=40, dtype=np.uint64)[rng.integers(0, 40, size=300_000)]
+    st = fresh(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=2e6)
+    st.host_stage_pairs = stage
+    seav = np.zeros(p.seav_bytes, dtype=np.uint8)
+    ldca = np.zeros(p.ldca_bytes, dtype=np.uint8)
+    B = 65_536
+    for i, lo in enumerate(range(0, n, B)):
+        h, o = hips[lo:lo + B], oips[lo:lo + B]
+        if i % 5 == 1:
+            h, o = h.astype(np.uint32), o.astype(np.uint32)
+        elif i % 5 == 2:
+            h = torch.from_numpy(h.astype(np.uint32).view(np.int32))
+            o = torch.from_numpy(o.astype(np.uint32).view(np.int32))
+        elif i % 5 == 3:
+            h = torch.from_numpy(h.astype(np.uint32).view(np.int32)).cuda()  # device batch, scanned at once
+            o = torch.from_numpy(o.astype(np.uint32).view(np.int32)).cuda()
+        st.process_batch(h, o)
+        oracle.scan(p, hips[lo:lo + B], oips[lo:lo + B], seav, ldca, threads=4)
+        if i == 7:  # a read mid-stream sees every staged pair
+            assert st.seav.payload_bytes() == seav.tobytes()
+            assert st.ldca.payload_bytes() == ldca.tobytes()
+        if i == 9:
+            bad = hips[lo:lo + B].copy()
+            bad[-1] = 1 << 32
+            with pytest.raises(DataError):
+                st.process_batch(bad, oips[lo:lo + B])
+    assert st.pair_count == n
+    assert st.seav.payload_bytes() == seav.tobytes()
+    assert st.ldca.payload_bytes() == ldca.tobytes()
+    reps = st.finalize_window()
+    ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+    z0 = oracle.filter_z0(p, ldca, ips)
+    k = dp.k
+    want = [int(ip) for ip, z in zip(ips, z0) if z == 0 or -k * math.log(z / k) >= dp.beta * dp.theta]
+    assert [r.ip for r in reps] == want and len(want) > 0
+    st.process_batch(hips[:1000], oips[:1000])  # staged, then dropped by reset
+    st.reset()
+    assert st.seav.total_set_bits() == 0 and not st.ldca.data.any()
+    st.process_pair(int(hips[0]), int(oips[0]))
+    s1, l1 = oracle.scan(p, hips[:1], oips[:1])
+    assert st.seav.payload_bytes() == s1.tobytes() and st.ldca.payload_bytes() == l1.tobytes()
