@@ -643,6 +643,10 @@ def run_sliding(args) -> dict:
     from paper_1901_07306_b200 import DetectorParams, SlidingDetector
     from tools.workloads import CONFIG4, CONFIG4_TIMING, TimingSpec, generate, scaled
 
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return run_sliding_ranks(args)
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     spec, timing = CONFIG4, CONFIG4_TIMING
@@ -806,6 +810,107 @@ def run_sliding(args) -> dict:
     }
 
 
+def run_sliding_ranks(args) -> dict | None:
+    """Config 4 on N ranks: N routers share the one sliding window; every
+    slice's packets are split into N contiguous parts (rank r observes part
+    r, slices advanced in lockstep) and every slide is detected through
+    multigpu.SlidingMerger (the ranks' active-bit views OR-merged onto rank
+    0 over peer memory, finalized there).  Strong scaling: the trace is
+    fixed.  The value is packets / (max over ranks of the trace time)."""
+    import torch
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+    from paper_1901_07306_b200.multigpu import SlidingMerger
+    from tools.workloads import CONFIG4, CONFIG4_TIMING, TimingSpec, generate, scaled
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_ranks(args, local)
+    spec, timing = CONFIG4, CONFIG4_TIMING
+    if args.packets:
+        spec = scaled(CONFIG4, max(1, CONFIG4.n_packets // args.packets))
+        timing = TimingSpec(rate_pps=spec.n_packets / (CONFIG4.n_packets / CONFIG4_TIMING.rate_pps))
+    t_gen = time.perf_counter()
+    hips, oips, supers, ts = generate(spec, "torch", dev, timing=timing)
+    slices = ts // 1000
+    del ts
+    n_sl = int(slices[-1].item()) + 1
+    bounds = torch.searchsorted(slices, torch.arange(n_sl + 1, device=dev, dtype=slices.dtype)).cpu().tolist()
+    del slices
+    parts = []
+    for s_ in range(n_sl):  # this rank's contiguous part of every slice
+        lo, hi = bounds[s_], bounds[s_ + 1]
+        parts.append((lo + (hi - lo) * rank // world, lo + (hi - lo) * (rank + 1) // world))
+    t_gen = time.perf_counter() - t_gen
+    n = int(hips.numel())
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=1024, design_n=2.15e8),
+                              window_slices=300)
+    merger = SlidingMerger(det, dist)
+    stream = torch.cuda.current_stream()
+    counts = []
+    merge_ms: list[float] = []
+
+    def step(record=None):
+        det.reset()
+        total = 0
+        for s_ in range(n_sl):
+            lo, hi = parts[s_]
+            if hi > lo:
+                det.observe_batch(hips[lo:hi], oips[lo:hi])
+            total += len(merger.detect())
+            if record is not None:
+                merge_ms.append(merger.last_merge_ms)
+            det.advance_slice()
+        if record is not None:
+            record.append(total)
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    clocks.mark()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(counts)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev if args.backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    merge = merge_summary(merger, merge_ms, dist, dev, args)
+    dist.destroy_process_group()
+    if rank != 0:
+        return None
+    value = n / (ms * 1e-3) / 1e6
+    return {
+        "metric": "packets/sec (Mpps) sliding scan+detect at every slide", "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 keys / u16 stamps",
+        "data": "synthetic (seeded, tools/workloads.py CONFIG4)",
+        "config": {"workload": f"config4: {n} pkts, {n_sl} slices, w=300, r=16, LDCA 8x1024x8192, detect every slide",
+                   "parallelism": f"dp{world} (each slice split over {world} routers; per-slide OR of the "
+                                  "active-bit views onto rank 0, finalize there)",
+                   "detect": "SlidingMerger.detect() at every slide (synchronous)"},
+        "merge": merge, "clocks": clk,
+        "detect": {"reports_total": counts[0] if counts else None, "slides": n_sl, "planted": len(supers)},
+        "gen_s": round(t_gen, 2),
+    }
+
+
 def run_sharded(args) -> dict | None:
     """Config 3 (BASELINE configs[2]): 8 router shards x 2^27 packets over one
     33.5 M-source population; each of 1,024 planted super points has its
@@ -918,26 +1023,34 @@ def run_sharded(args) -> dict | None:
     }
 
 
-def run_streaming(args) -> dict:
+def run_streaming(args) -> dict | None:
     """Config 5 (BASELINE configs[4]): 2^32 packets streamed from pinned host
     memory in 2^26-packet batches (double-buffered H2D, process_host_stream);
     8 discrete windows x 8 router batches, LDCA 64 MiB (LR=8, LC=8192),
-    SEAV r=16, finalize once per window.  One GPU plays all 8 routers of a
-    window (the OR-merge is the sketch itself); the 8 router batches are
-    generated once and re-streamed by every window."""
+    SEAV r=16, finalize once per window.  At N ranks, rank r is the border
+    router(s) r, r+N, ... of every window: it streams only its own batches
+    over its own PCIe link, the per-rank sketches are OR-merged onto rank 0
+    (multigpu.OrMerger) and rank 0 finalizes each window.  At N = 1 one GPU
+    plays all 8 routers (the OR-merge is the sketch itself).  The router
+    batches are generated once and re-streamed by every window."""
     import torch
 
     from paper_1901_07306_b200 import DetectorParams, DetectorState
     from tools.workloads import CONFIG5_WINDOW, generate_shard, sharded_scaled
 
-    torch.cuda.set_device(0)
-    dev = torch.device("cuda", 0)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_ranks(args, local)
     spec = CONFIG5_WINDOW
     if args.packets:
         spec = sharded_scaled(spec, max(1, spec.packets_per_shard // args.packets))
+    mine = list(range(rank, spec.n_shards, world))
     t_gen = time.perf_counter()
     batches = []
-    for r in range(spec.n_shards):
+    for r in mine:
         h, o, _ = generate_shard(spec, r, "torch", dev)
         batches.append((h.cpu().pin_memory(), o.cpu().pin_memory()))
         del h, o
@@ -949,34 +1062,55 @@ def run_streaming(args) -> dict:
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         st = DetectorState.create(DetectorParams(theta=1024, r=16, k=8192, lr=8, lc=8192, design_n=1.6e8))
+    merger = None
+    if dist is not None:
+        from paper_1901_07306_b200.multigpu import OrMerger
+
+        merger = OrMerger(st, dist)
     stream = torch.cuda.current_stream()
     reps = []
+    merge_ms: list[float] = []
 
     def step(record=None):
         total = 0
         for _ in range(windows):
             for h, o in batches:
                 st.process_host_stream(h, o, chunk_pairs=args.chunk)
-            total += len(st.finalize_window())
+            if merger is not None:
+                merger.merge_to_root()
+                if record is not None:
+                    merge_ms.append(merger.last_merge_ms)
+            if rank == 0:
+                total += len(st.finalize_window())
             st.reset()
         if record is not None:
             record.append(total)
 
-    clocks = ClockSampler(0)
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
     clocks.start()
     for _ in range(args.warmup):
         step()
     clocks.mark()
-    torch.cuda.synchronize()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step(reps)
     e1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    # bound: the host link -- measured pinned H2D rate on one batch
+    if dist is not None:
+        t = torch.tensor([ms], device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # bound: the host links -- measured pinned H2D rate on one batch (per GPU)
     dst = torch.empty(per_batch, dtype=torch.int32, device=dev)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     best = None
@@ -987,19 +1121,29 @@ def run_streaming(args) -> dict:
         b.synchronize()
         best = a.elapsed_time(b) if best is None else min(best, a.elapsed_time(b))
     h2d = per_batch * 4 / (best * 1e-3) / 1e9
+    merge = merge_summary(merger, merge_ms, dist, dev, args) if merger is not None else None
+    if dist is not None:
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
     achieved = 8 * n / (ms * 1e-3) / 1e9
     value = n / (ms * 1e-3) / 1e6
     return {
         "metric": "packets/sec (Mpps) streamed scan+detect (pinned host batches)", "value": round(value, 3),
-        "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 keys / u8 bit arrays",
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 keys / u8 bit arrays",
         "data": "synthetic (seeded, tools/workloads.py CONFIG5_WINDOW)",
         "config": {"workload": f"config5: {windows} windows x {spec.n_shards} batches x {per_batch} pkts = {n}",
                    "ldca": "LR=8 LC=8192 k=8192 (64 MiB, L2 red.or scan)", "seav_r": 16,
+                   "routers_per_rank": len(mine),
+                   "parallelism": f"dp{world} (router batches over each GPU's own PCIe link, OR-merge to rank 0)",
                    "ingest": f"process_host_stream, {args.chunk}-pair double-buffered H2D chunks"},
-        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": None},
-        "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 2), "peak": round(h2d, 2), "unit": "GB/s",
-                     "frac": round(achieved / h2d, 4), "traffic": None, "peak_source": "measured pinned H2D copy"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": None},
+        "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 2), "peak": round(h2d * world, 2),
+                     "unit": "GB/s", "frac": round(achieved / (h2d * world), 4), "traffic": None,
+                     "peak_source": f"measured pinned H2D copy x {world} GPU link(s)"},
+        "merge": merge,
         "clocks": clk, "detect": {"reports_total": reps[0] if reps else None, "windows": windows},
         "gen_s": round(t_gen, 2),
     }

@@ -111,3 +111,77 @@ def test_host_stream_ingest_matches_device_batch(cuda):
     assert a.seav.payload_bytes() == b.seav.payload_bytes()
     assert a.ldca.payload_bytes() == b.ldca.payload_bytes()
     assert a.finalize_window() == b.finalize_window()
+
+
+def _sliding_worker(rank, world, port, out):
+    """Rank r = one router of a sliding window over the packets whose index
+    is r mod world; slices advanced in lockstep; detect via SlidingMerger at
+    every slice (views OR-merged onto rank 0) plus one full age-min pool
+    merge at the end."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+    from paper_1901_07306_b200.multigpu import SlidingMerger
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        det = SlidingDetector(DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5), window_slices=9)
+    m = SlidingMerger(det, dist)
+    out[f"transport{rank}"] = m.transport
+    for s, (hips, oips) in enumerate(_slides()):
+        det.observe_batch(hips[rank::world], oips[rank::world])
+        reps = m.detect()
+        if rank == 0:
+            out[f"rep{s}"] = [(r.ip, r.estimated_cardinality, r.saturated, r.window_id) for r in reps]
+        det.advance_slice()
+    merged = m.merge_pools_to_root()
+    if rank == 0:
+        out["pool"] = merged.ts.tobytes()
+    dist.barrier()
+    m.close()
+    dist.destroy_process_group()
+
+
+def _slides(n_slides=24):
+    rng = np.random.default_rng(44)
+    heavy = rng.integers(0, 2**32, size=4, dtype=np.uint64)
+    out = []
+    for s in range(n_slides):
+        n = int(rng.integers(10_000, 30_000))
+        hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+        if s < 6 or 12 <= s < 15:  # bursts that expire within the run (w = 9)
+            hips[: n // 2] = heavy[s % 4]
+        out.append((hips.astype(np.uint32), oips.astype(np.uint32)))
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sliding_merger_two_processes_one_gpu(cuda, world):
+    """N routers sharing one sliding window (north_star (4) in sliding mode):
+    per-slide reports from the OR of the ranks' active-bit views and the
+    age-min merged pool (merge_timestamp_pools across ranks) equal a single
+    detector's over all packets."""
+    from paper_1901_07306_b200 import DetectorParams, SlidingDetector
+
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_sliding_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    assert all(out[f"transport{r}"] == "ipc" for r in range(world))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = SlidingDetector(DetectorParams(theta=256, r=8, k=4096, lr=4, lc=256, design_n=2e5), window_slices=9)
+    total = 0
+    for s, (hips, oips) in enumerate(_slides()):
+        ref.observe_batch(hips, oips)
+        want = [(r.ip, r.estimated_cardinality, r.saturated, r.window_id) for r in ref.detect()]
+        assert out[f"rep{s}"] == want, s
+        total += len(want)
+        ref.advance_slice()
+    assert total > 0
+    assert out["pool"] == ref.pool.ts.tobytes()

@@ -61,6 +61,22 @@ class ShmOps:
     def copy(self, dst, src, n):
         self._view(dst, n)[:] = self._view(src, n)
 
+    def merge_age_min(self, srcs, dst, n_slots, ts_bytes, now):
+        """K8 restated: per slot the stamp with the smallest wrapped age."""
+        dt = np.dtype(f"u{ts_bytes}")
+        mask = (1 << (8 * ts_bytes)) - 1
+        stamps = [self._view(s, n_slots * ts_bytes).view(dt).astype(np.int64) for s in srcs]
+        ages = np.stack([(now - x) & mask for x in stamps])
+        best = np.min(ages, axis=0)
+        self._view(dst, n_slots * ts_bytes).view(dt)[:] = ((now - best) & mask).astype(dt)
+
+    def put_pool(self, ptr, pool):
+        raw = pool.ts.tobytes()
+        self._view(ptr, len(raw))[:] = np.frombuffer(raw, dtype=np.uint8)
+
+    def pool_from(self, ptr, pool):
+        return self._view(ptr, pool.n_slots * pool.ts_bytes).view(pool.ts.dtype).copy()
+
     def sync(self):
         pass
 
@@ -98,6 +114,53 @@ def _worker(rank, world, port, seav_bytes, ldca_bytes, results):
             results[window] = bool((ops._view(m.base, m.nbytes) == want).all())
         dist.barrier()
     dist.destroy_process_group()
+
+
+class _FakePool:
+    """A TimestampPool's protocol surface: u16 stamps, window, clock."""
+
+    def __init__(self, rank, n=4099, w=9, now=37):
+        rng = np.random.default_rng(77 + rank)
+        self.n_slots, self.ts_bytes, self.window_slices, self.now = n, 2, w, now
+        self.ts = ((now - rng.integers(0, 3 * w, n)) & 0xFFFF).astype(np.uint16)
+
+    def _wrapped_now(self):
+        return self.now & 0xFFFF
+
+
+def _pool_worker(rank, world, port, results):
+    import torch.distributed as dist
+
+    from paper_1901_07306_b200.multigpu import SlidingMerger
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ops = ShmOps()
+    det = types.SimpleNamespace(pool=_FakePool(rank), _params=types.SimpleNamespace(seav_bytes=4096, ldca_bytes=1000))
+    m = SlidingMerger(det, dist, ops=ops)
+    merged = m.merge_pools_to_root()
+    if rank == 0:
+        pools = [_FakePool(r).ts.astype(np.int64) for r in range(world)]
+        ages = np.stack([(37 - x) & 0xFFFF for x in pools])
+        want = ((37 - ages.min(axis=0)) & 0xFFFF).astype(np.uint16)
+        results["pool"] = bool((merged == want).all())
+    else:
+        results[f"none{rank}"] = merged is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sliding_pool_age_min_protocol_gloo(world):
+    """SlidingMerger.merge_pools_to_root (merge_timestamp_pools across ranks,
+    distributed.py:176-192): each rank age-min-merges one slot stripe of all
+    pools over peer memory, rank 0 gathers -- equals the per-slot minimum
+    wrapped age over all ranks' pools."""
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    mp.start_processes(_pool_worker, args=(world, _free_port(), results), nprocs=world, join=True,
+                       start_method="spawn")
+    assert results["pool"] and all(results[f"none{r}"] for r in range(1, world))
 
 
 @pytest.mark.parametrize("world", [2, 3])
