@@ -102,6 +102,12 @@ SSPD_API uint64_t sspd_mix64_host(uint64_t x);                   /* hashing.py:4
  * staged; sspd_host_pack_u32 = narrow n checked keys into dst (u32). */
 SSPD_API int sspd_host_check_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed);
 SSPD_API int sspd_host_pack_u32(const void* src, uint64_t n, uint32_t elem_bytes, int is_signed, uint32_t* dst);
+/* Both key arrays of a batch at once (widths hbytes/obytes), split over a
+ * persistent host worker pool (SSPD_HOST_COPY_THREADS, default min(cores/2, 8));
+ * sspd_host_copy_threads = the threads a pack uses (pool workers + caller). */
+SSPD_API int sspd_host_pack_pairs(const void* hips, const void* oips, uint64_t n, uint32_t hbytes,
+                                  uint32_t obytes, uint32_t* dst_h, uint32_t* dst_o);
+SSPD_API int sspd_host_copy_threads(void);
 
 /* ---- K1 discrete scan --------------------------------------------------
  * Replaces DetectorState.process_batch (window_detector.py:100-103) =

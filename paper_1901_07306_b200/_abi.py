@@ -105,6 +105,8 @@ _SIGS = {
     "sspd_scan_partitioned_variant": (C.c_int, [_PP, _U64]),
     "sspd_host_check_u32": (C.c_int, [_VP, _U64, _U32, C.c_int]),
     "sspd_host_pack_u32": (C.c_int, [_VP, _U64, _U32, C.c_int, _VP]),
+    "sspd_host_pack_pairs": (C.c_int, [_VP, _VP, _U64, _U32, _U32, _VP, _VP]),
+    "sspd_host_copy_threads": (C.c_int, []),
     "sspd_scan_sliding": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _VP]),
     "sspd_scan_sliding_capped": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP]),
     "sspd_scan_sliding_tracked": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP, _VP, _U64, _VP, _VP]),

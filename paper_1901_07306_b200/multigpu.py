@@ -184,6 +184,7 @@ class BlockMerger:
         syncs and the two further barriers)."""
         import time
 
+        self._before_merge()
         if self.transport == "nccl":
             self.ops.sync()
             self.dist.barrier(group=self.group)
@@ -208,6 +209,9 @@ class BlockMerger:
             self.ops.sync()
         d.barrier(group=self.group)              # root done reading peers
         self.last_merge_ms = (time.perf_counter() - t0) * 1e3
+
+    def _before_merge(self):
+        """Hook: make the block complete before peers read it."""
 
     def _merge_nccl(self):
         import torch
@@ -242,9 +246,17 @@ class OrMerger(BlockMerger):
         self.seav_off = 0
         self.ldca_off, nbytes = _two_part_layout(state.seav.nbytes, state.ldca.nbytes)
         super().__init__(nbytes, dist, group, ops, allow_fallback)
+        self._state = state
         if self._block is not None:
             state.seav._rebind(self._block[: self.ldca_off])
             state.ldca._rebind(self._block[self.ldca_off:])
+
+    def _before_merge(self):
+        # host batches the state has staged but not scanned yet (the pre-read
+        # hook of its sketches) must reach the block before peers read it
+        flush = getattr(self._state, "_flush_host", None)
+        if flush is not None:
+            flush()
 
 
 class SlidingMerger(BlockMerger):
