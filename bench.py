@@ -320,7 +320,26 @@ def run_dropin(st, h_host, o_host, args, timed, stream_value) -> dict:
     step()
     ms = timed(step, max(1, args.steps // 4))
     v = n / (ms * 1e-3) / 1e6
+    # the path's own bound: the host copy of every call's keys from pageable
+    # memory into the pinned staging buffers (sspd_host_pack_pairs on the
+    # staging pool), measured alone over the same window
+    from paper_1901_07306_b200._abi import lib
+
+    L = lib()
+    stage = st._hstage
+    pa, pb, cap = stage["ph_addr"][0], stage["po_addr"][0], stage["cap"]
+    t0 = time.perf_counter()
+    for lo in range(0, n, B):
+        off = 4 * (lo % cap)
+        L.sspd_host_pack_pairs(h_np.ctypes.data + 4 * lo, o_np.ctypes.data + 4 * lo, min(B, n - lo), 4, 4,
+                               pa + off, pb + off)
+    pack_s = time.perf_counter() - t0
+    pack_pps = n / pack_s
     return {"value": round(v, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "calls_per_step": -(-n // B),
+            "host_copy_bound": {"value": round(pack_pps / 1e6, 3), "unit": UNIT,
+                                "gbs": round(8 * n / pack_s / 1e9, 2), "threads": int(L.sspd_host_copy_threads()),
+                                "frac": round(v * 1e6 / pack_pps, 4),
+                                "note": "pageable -> pinned copy of the keys alone, same 65,536-pair calls"},
             "pairs_per_call": B, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * out[0] + 16,
             "frac_of_host_stream": round(v / stream_value, 4) if stream_value else None,
             "note": "process_batch(numpy uint32 views of 65,536 pairs) x calls + finalize_window + reset; "
