@@ -200,6 +200,14 @@ SSPD_API int sspd_materialize_seav_if(const void* pool, uint32_t ts_bytes, const
  *       read (SlidingDetector does; TimestampPool.flush).
  * SSPD_ERR_CONFIG when the stamps are not u16 / the layout is not 8-slot
  * aligned. */
+/* sspd_scan_sliding_seav = the SEAV half of sspd_scan_sliding_deferred
+ *       (SEAV stamps + optional tracking, no LDCA slot); with
+ *       sspd_scan_partitioned(seav = NULL, ldca = the slice's dirty bitmap)
+ *       for the LDCA half it records exactly what the deferred scan does. */
+SSPD_API int sspd_scan_sliding_seav(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                    const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                    uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
+                                    uint64_t log_entries, unsigned long long* log_head, void* stream);
 SSPD_API int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                         const sspd_params* p, void* pool, uint32_t ts_bytes,
                                         uint64_t now_wrapped, uint32_t max_blocks_per_sm,

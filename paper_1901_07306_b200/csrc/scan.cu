@@ -354,7 +354,7 @@ extern "C" int sspd_scan_discrete(const uint32_t* hips, const uint32_t* oips, ui
 
 static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                              void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
-                             SeavTracker tracker, uint32_t* dirty, void* stream);
+                             SeavTracker tracker, uint32_t* dirty, void* stream, bool seav_only = false);
 
 extern "C" int sspd_scan_sliding_capped(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                         const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
@@ -396,16 +396,44 @@ extern "C" int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* 
   return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm, tr, ldca_dirty, stream);
 }
 
+// SEAV half of the deferred scan: SEAV stamps (+ optional tracking) only.
+// The LDCA half of the same packets goes to the slice's dirty bitmap through
+// the partitioned scan (sspd_scan_partitioned with seav = NULL, ldca = the
+// bitmap) -- together exactly sspd_scan_sliding_deferred.
+extern "C" int sspd_scan_sliding_seav(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+                                      void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
+                                      uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
+                                      uint64_t log_entries, unsigned long long* log_head, void* stream) {
+  SeavTracker tr{nullptr, nullptr, nullptr, 0u};
+  if (seav_view) {
+    if (!log || !log_head || log_entries == 0 || (log_entries & (log_entries - 1)) || log_entries > (1ull << 32) ||
+        (reinterpret_cast<uintptr_t>(seav_view) & 3u))
+      return SSPD_ERR_DATA;
+    tr = SeavTracker{reinterpret_cast<uint32_t*>(seav_view), log, log_head, (uint32_t)(log_entries - 1)};
+  }
+  return scan_sliding_impl(hips, oips, n, p, pool, ts_bytes, now_wrapped, max_blocks_per_sm, tr, nullptr, stream,
+                           true);
+}
+
 extern "C" int sspd_scan_sliding(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
                                  void* pool, uint32_t ts_bytes, uint64_t now_wrapped, void* stream) {
   return sspd_scan_sliding_capped(hips, oips, n, p, pool, ts_bytes, now_wrapped, 0, stream);
 }
 
-static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p,
+static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p_in,
                              void* pool, uint32_t ts_bytes, uint64_t now_wrapped, uint32_t max_blocks_per_sm,
-                             SeavTracker tracker, uint32_t* dirty, void* stream) {
-  int rc = validate_params(p);
+                             SeavTracker tracker, uint32_t* dirty, void* stream, bool seav_only) {
+  int rc = validate_params(p_in);
   if (rc) return rc;
+  // seav_only: the SEAV stamps (and tracking) of the packets, no LDCA slot --
+  // the same kernels with zero LDCA rows (the LDCA side is then recorded by
+  // the partitioned scan into the dirty bitmap, sspd_scan_sliding_seav)
+  sspd_params pv = *p_in;
+  if (seav_only) {
+    pv.lr = 0;
+    dirty = nullptr;
+  }
+  const sspd_params* p = &pv;
   // tracking and deferred LDCA stamps exist for u16 stamps only
   if ((tracker.view || dirty) && ts_bytes != 2) return SSPD_ERR_CONFIG;
   if (n == 0) return SSPD_OK;

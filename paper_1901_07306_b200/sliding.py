@@ -13,6 +13,8 @@ view (K4), restores (K5) and filters straight from the pool (K6 sliding).
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -405,6 +407,9 @@ class SlidingDetector:
     # ((w+1) x LDCA bytes; 2.5 GB at config 4) and build the LDCA view as a
     # sliding-window OR instead of from the stamps
     ldca_ring_max_bytes = 8 << 30
+    # slices at least this large record their LDCA half with the partitioned
+    # scan K1b (0 = never); see _partitioned_dirty
+    partitioned_dirty_min_packets = 0
 
     def __init__(self, params: DetectorParams | None = None, window_slices: int = 300,
                  slice_seconds: float = 1.0):
@@ -569,7 +574,20 @@ class SlidingDetector:
         dfr = self._deferred()
         if dfr is not None and dfr.ring is not None:
             dfr.sync(pool)
-        if iv is not None or dfr is not None:
+        if dfr is not None and self._partitioned_dirty(h.numel()):
+            # large slices: the LDCA half into the slice's dirty bitmap with
+            # the shared-memory partitioned scan (K1b), the SEAV half (stamps
+            # + tracking) with K2 restricted to the sampled packets
+            if iv is not None:
+                self._iv_check(iv)
+            self._scan_dirty_partitioned(h, o, dfr.dirty_ptr())
+            call("sspd_scan_sliding_seav", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+                 pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
+                 None if iv is None else iv["view"].device_buffer().data_ptr(),
+                 None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
+                 None if iv is None else iv["meta"].data_ptr(), stream_ptr())
+            dfr.mark_scanned()
+        elif iv is not None or dfr is not None:
             if iv is not None:
                 self._iv_check(iv)
             # pool._buf: the scan itself needs no flush (pending and new
@@ -586,6 +604,39 @@ class SlidingDetector:
             call("sspd_scan_sliding_capped", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
                  pool.device_buffer().data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap, stream_ptr())
         self.pair_count += int(h.numel())
+
+    def _partitioned_dirty(self, n: int) -> bool:
+        """Record this slice's LDCA half with K1b? (env SSPD_SLIDE_PARTITIONED
+        = 1 / 0 forces it on / off; else `partitioned_dirty_min_packets`)."""
+        env = os.environ.get("SSPD_SLIDE_PARTITIONED")
+        if env is not None and env != "":
+            want = env != "0"
+        else:
+            want = self.partitioned_dirty_min_packets > 0 and n >= self.partitioned_dirty_min_packets
+        if not want:
+            return False
+        ok = getattr(self, "_k1b_ok", None)
+        if ok is None:
+            from ._abi import lib
+
+            ok = self._k1b_ok = int(lib().sspd_scan_partitioned_variant(self._params, 0)) > 0
+        return ok
+
+    def _scan_dirty_partitioned(self, h, o, dirty_ptr: int):
+        import torch
+
+        from ._abi import check, lib
+        from ._device import stream_ptr
+
+        n = int(h.numel())
+        chunk = -(-n // 4) * 4
+        need = int(lib().sspd_scan_partitioned_scratch(self._params, chunk))
+        buf = getattr(self, "_part_scratch", None)
+        if buf is None or buf.numel() < need:
+            buf = self._part_scratch = torch.empty(need, dtype=torch.uint8, device=h.device)
+        check(lib().sspd_scan_partitioned(h.data_ptr(), o.data_ptr(), n, self._params, None, dirty_ptr,
+                                          buf.data_ptr(), buf.numel(), chunk, stream_ptr()),
+              "sspd_scan_partitioned")
 
     def observe(self, hip: int, oip: int):
         self.observe_batch(np.array([hip], dtype=np.uint64), np.array([oip], dtype=np.uint64))
