@@ -72,6 +72,7 @@ struct Plan {
   uint32_t qstride;      // nsrc * region_cap: bucket entries per destination
   uint32_t gshift;       // log2 of the flush group (threads per destination)
   uint32_t tau_mask;
+  uint32_t cons_warps;   // kSpec: consumer warps of an owner CTA
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
 };
 
@@ -134,7 +135,14 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 
 // Shared memory: [part_words | nparts*stage_slots uint4 staging | nparts cnt |
 //                 4 sq_cnt | 2*kSeavQueue (hip, oip)]
-template <bool kSeav, int HB>
+// kSpec: warp-specialised owner CTAs -- P.cons_warps warps consume chunk t-1
+// (the bucket entries into the shared partition: LSU/shared-atomic work)
+// while the other warps hash and stage chunk t (ALU/FMA work), so the two
+// overlap instead of alternating; the producers synchronise on named
+// barrier 1.  Pure-producer CTAs (no partition) hash with all warps.
+constexpr uint32_t kConsWarps = 8;  // measured best (4: 5.48 ms, 6: 4.70, 8: 4.60, 10: 4.75 per config-2 window)
+
+template <bool kSeav, int HB, bool kSpec>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_bpart_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
                       const __grid_constant__ sspd_params p, const __grid_constant__ Plan P, uint32_t* seav,
@@ -152,20 +160,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t np = P.nparts, ns = P.nsrc;
   const bool owner = self < np;
   constexpr uint32_t kHMask = (1u << HB) - 1u;
+  // producer threads of this CTA and their tile (packets per tile barrier)
+  const uint32_t nprod = (kSpec && owner) ? kThreads - 32u * P.cons_warps : kThreads;
+  const bool producer = tid < nprod;
+  const uint32_t tile = nprod * kPkt;
+  auto pbar = [&]() {  // the producers' barrier
+    if (kSpec)
+      asm volatile("bar.sync 1, %0;" ::"r"(nprod) : "memory");
+    else
+      __syncthreads();
+  };
 
   for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
   for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = 0;
   // flush role, fixed for the launch: group q = tid >> gshift of G threads
   // copies destination q's staging row (one pass covers every destination)
-  const uint32_t gs = P.gshift, G = 1u << gs, gl = tid & (G - 1u), fq = tid >> gs;
-  const bool flusher = fq < np;
+  uint32_t gs = P.gshift;
+  while (gs && (nprod >> gs) < np) --gs;
+  const uint32_t G = 1u << gs, gl = tid & (G - 1u), fq = tid >> gs;
+  const bool flusher = producer && fq < np;
   if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
   __syncthreads();
 
   const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
   for (uint64_t t = 0; t <= nchunks; ++t) {
     // ---------------- consume chunk t-1 into the shared partition --------
-    if (t >= 1 && owner) {
+    if (t >= 1 && owner && (!kSpec || !producer)) {
+      const uint32_t cw = kSpec ? warp - nprod / 32u : warp;  // consumer warp index
+      const uint32_t ncw = kSpec ? P.cons_warps : nwarps;
       const uint32_t bb = (uint32_t)((t - 1) & 1);
       const uint32_t* cnts = P.counts + ((size_t)bb * np + self) * ns;
       const uint4* regions = P.buckets + ((size_t)bb * np + self) * (size_t)P.qstride;
@@ -173,9 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       char* const pb = reinterpret_cast<char*>(part);
       // warp w drains sources w, w+W, ...: lane j holds the run length of
       // source w+W*j, fetched at once so no region waits on its count
-      const uint32_t my_src = warp + nwarps * lane;
+      for (uint32_t src0 = cw; src0 < ns; src0 += 32u * ncw) {
+      const uint32_t my_src = src0 + ncw * lane;
       const uint32_t my_cnt = my_src < ns ? min(__ldcg(cnts + my_src), P.region_cap) : 0u;
-      for (uint32_t src = warp, j = 0; src < ns; src += nwarps, ++j) {
+      for (uint32_t src = src0, j = 0; src < ns && j < 32u; src += ncw, ++j) {
         const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
         const uint4* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
         for (uint32_t j0 = lane; j0 < m; j0 += 128) {  // 4 independent 16-B loads in flight per lane
@@ -205,9 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t line = lane; line * 8 < m; line += 32)
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(reg + line * 8) : "memory");
       }
+      }
     }
     // ---------------- produce chunk t ------------------------------------
-    if (t < nchunks) {
+    if (t < nchunks && producer) {
       const uint32_t bb = (uint32_t)(t & 1);
       const uint64_t c0 = t * P.chunk;
       const uint64_t c1 = min(P.n, c0 + P.chunk);
@@ -237,14 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t nh[kPkt], no[kPkt];
       fetch(lo + (uint64_t)tid * kPkt, nh, no);
       uint32_t par = 0;  // tile parity: selects the sampled-packet queue
-      for (uint64_t base = lo; base < hi; base += kTile, par ^= 1u) {
+      for (uint64_t base = lo; base < hi; base += tile, par ^= 1u) {
         uint32_t ch[kPkt], co[kPkt];
 #pragma unroll
         for (uint32_t e = 0; e < kPkt; ++e) {
           ch[e] = nh[e];
           co[e] = no[e];
         }
-        fetch(base + kTile + (uint64_t)tid * kPkt, nh, no);
+        fetch(base + tile + (uint64_t)tid * kPkt, nh, no);
 #pragma unroll
         for (uint32_t e = 0; e < kPkt; ++e) {
           const uint64_t j = base + (uint64_t)tid * kPkt + e;
@@ -278,11 +302,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        __syncthreads();
-        if (kSeav) {  // the tile's sampled packets, all lanes busy
+        pbar();
+        if (kSeav) {  // the tile's sampled packets, all producer lanes busy
           const uint32_t nq = min(sq_cnt[par], kSeavQueue);
           const uint2* sq = sq_base + par * kSeavQueue;
-          for (uint32_t i = tid; i < nq; i += kThreads) seav_update(p, sq[i].x, sq[i].y, seav);
+          for (uint32_t i = tid; i < nq; i += nprod) seav_update(p, sq[i].x, sq[i].y, seav);
           // the previous tile's queue was fully read before this barrier
           if (tid == 0) sq_cnt[par ^ 1u] = 0;
         }
@@ -305,10 +329,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();  // the group's lanes read cnt[fq] before it is reset
           if (gl == 0) cnt[fq] = 0;
         }
-        __syncthreads();
+        pbar();
       }
       if (kSeav) {  // queues restart at parity 0 with the next chunk's slice
-        __syncthreads();
+        pbar();
         if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
       }
       // publish this CTA's run lengths for chunk t
@@ -342,7 +366,7 @@ static uint32_t ilog2_exact(uint64_t d) {
 // Plan for the b-axis partitioned scan; false when the geometry or device
 // cannot host it (the caller then uses K1p or K1).
 static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int max_smem, Plan& P, uint64_t& smem,
-                 uint64_t& scratch, int& hb) {
+                 uint64_t& scratch, int& hb, bool& spec) {
   const bool pow2 = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0;
   if (p->lr != kLR || !pow2 || (uint64_t)p->lr * p->lc * p->k > 0xFFFFFFFFull) return false;
   if (getenv("SSPD_PART_LEGACY") != nullptr) return false;
@@ -371,8 +395,16 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   }
   smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 16ull * kSeavQueue;
   if ((int64_t)smem > max_smem) return false;
+  // warp-specialised owner CTAs (default; SSPD_BPART_SPEC=0: consume in line,
+  // 4.80 vs 4.60 ms per config-2 window)
+  spec = true;
+  if (const char* e = getenv("SSPD_BPART_SPEC")) spec = atoi(e) != 0;
+  P.cons_warps = kConsWarps;
+  if (const char* e = getenv("SSPD_BPART_CONS_WARPS")) P.cons_warps = (uint32_t)std::min(16, std::max(1, atoi(e)));
+  // producer slice weights: pure producers hash with all 32 warps; owners
+  // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;
-  P.w_other = 80;
+  P.w_other = spec ? 76 : 80;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
   // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
   // outweigh the part of the bucket exchange that then spills from L2)
@@ -413,13 +445,13 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   return true;
 }
 
-template <bool kSeav>
+template <bool kSeav, bool kSpec>
 static void* kernel_for(int hb) {
   switch (hb) {
-    case 0: return (void*)scan_bpart_kernel<kSeav, 0>;
-    case 1: return (void*)scan_bpart_kernel<kSeav, 1>;
-    case 2: return (void*)scan_bpart_kernel<kSeav, 2>;
-    default: return (void*)scan_bpart_kernel<kSeav, 3>;
+    case 0: return (void*)scan_bpart_kernel<kSeav, 0, kSpec>;
+    case 1: return (void*)scan_bpart_kernel<kSeav, 1, kSpec>;
+    case 2: return (void*)scan_bpart_kernel<kSeav, 2, kSpec>;
+    default: return (void*)scan_bpart_kernel<kSeav, 3, kSpec>;
   }
 }
 
@@ -445,7 +477,8 @@ uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk) {
   bpart::Plan P;
   uint64_t smem = 0, need = 0;
   int hb = 0;
-  if (!bpart::plan(p, 1, chunk, sms, max_smem, P, smem, need, hb)) return 0;
+  bool spec = false;
+  if (!bpart::plan(p, 1, chunk, sms, max_smem, P, smem, need, hb, spec)) return 0;
   return need;
 }
 
@@ -459,7 +492,8 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   bpart::Plan P;
   uint64_t smem = 0, need = 0;
   int hb = 0;
-  if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb)) return SSPD_ERR_CONFIG;
+  bool spec = false;
+  if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb, spec)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
@@ -467,7 +501,8 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
               (P.chunk & 3u) == 0)
                  ? 1u
                  : 0u;
-  void* kern = seav ? bpart::kernel_for<true>(hb) : bpart::kernel_for<false>(hb);
+  void* kern = seav ? (spec ? bpart::kernel_for<true, true>(hb) : bpart::kernel_for<true, false>(hb))
+                     : (spec ? bpart::kernel_for<false, true>(hb) : bpart::kernel_for<false, false>(hb));
   // attribute/occupancy answers only change with (kernel, smem, device)
   static void* c_kern = nullptr;
   static uint64_t c_smem = 0;
