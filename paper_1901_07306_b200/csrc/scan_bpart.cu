@@ -72,7 +72,7 @@ struct Plan {
   uint32_t qstride;      // nsrc * region_cap: bucket entries per destination
   uint32_t gshift;       // log2 of the flush group (threads per destination)
   uint32_t tau_mask;
-  uint32_t cons_warps;   // kSpec: consumer warps of an owner CTA
+  uint32_t cons_warps;   // kWarpLdg / kWarpTma: consumer warps of an owner CTA
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
 };
 
@@ -120,6 +120,45 @@ __device__ __noinline__ void direct_entry(const Plan& P, uint32_t q, uint4 e, ui
   }
 }
 
+// ---- TMA bulk-copy pipeline of the consumer warps (kWarpTma) -------------
+// One lane of the first consumer warp streams the chunk's bucket regions
+// into a ring of kRing shared-memory slots with cp.async.bulk (completion
+// on the slot's `full` mbarrier, transaction bytes); the other consumer
+// warps OR the entries out of shared memory and release the slot on its
+// `empty` mbarrier.  No consumer lane waits on a global load.
+constexpr uint32_t kRing = 4;
+constexpr uint32_t kSlot = 256;  // entries (16 B) per ring slot
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both 16-B aligned),
+// completing `bytes` transactions on mbarrier `b`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
 // Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
 // take w_other/w_owner as much as owners; boundaries are 4-aligned.  Full
 // chunks read the host-computed table (no 64-bit division per chunk).
@@ -134,15 +173,25 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 }
 
 // Shared memory: [part_words | nparts*stage_slots uint4 staging | nparts cnt |
-//                 4 sq_cnt | 2*kSeavQueue (hip, oip)]
-// kSpec: warp-specialised owner CTAs -- P.cons_warps warps consume chunk t-1
+//                 4 sq_cnt | 2*kSeavQueue (hip, oip) | kWarpTma: kRing*kSlot uint4
+//                 ring | 2*kRing mbarriers]
+// Warp-specialised owner CTAs (kWarpLdg / kWarpTma): P.cons_warps warps consume chunk t-1
 // (the bucket entries into the shared partition: LSU/shared-atomic work)
 // while the other warps hash and stage chunk t (ALU/FMA work), so the two
 // overlap instead of alternating; the producers synchronise on named
 // barrier 1.  Pure-producer CTAs (no partition) hash with all warps.
-constexpr uint32_t kConsWarps = 8;  // measured best (4: 5.48 ms, 6: 4.70, 8: 4.60, 10: 4.75 per config-2 window)
+// Consumer modes: kInline = every warp drains chunk t-1, then produces;
+// kWarpLdg = P.cons_warps warps drain with 16-B global loads (4 in flight
+// per lane) while the rest produce (default: 4.60 vs 4.80 ms per config-2
+// window); kWarpTma = the same split, fed by TMA bulk copies into a
+// shared-memory ring (1 issuing lane + draining warps; bit-exact but
+// measured slower on B200: 6.3-6.9 ms -- the 16 KB ring the shared-memory
+// budget leaves keeps too few bytes in flight).
+enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2 };
+constexpr uint32_t kConsWarpsLdg = 8;  // measured: 4 -> 5.48 ms, 6 -> 4.70, 8 -> 4.60, 10 -> 4.75
+constexpr uint32_t kConsWarpsTma = 6;
 
-template <bool kSeav, int HB, bool kSpec>
+template <bool kSeav, int HB, int kCons>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_bpart_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
                       const __grid_constant__ sspd_params p, const __grid_constant__ Plan P, uint32_t* seav,
@@ -153,6 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
   uint32_t* sq_cnt = cnt + P.nparts;                        // [2] (+2 pad); nparts % 4 == 0
   uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [2][kSeavQueue]
+  uint4* ring = reinterpret_cast<uint4*>(sq_base + 2 * kSeavQueue);  // kWarpTma: [kRing][kSlot]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(ring + kRing * kSlot);
+  uint64_t* empty_bar = full_bar + kRing;
   cg::grid_group grid = cg::this_grid();
   const uint32_t self = blockIdx.x;
   const uint32_t tid = threadIdx.x;
@@ -161,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool owner = self < np;
   constexpr uint32_t kHMask = (1u << HB) - 1u;
   // producer threads of this CTA and their tile (packets per tile barrier)
+  constexpr bool kSpec = kCons != kInline;
   const uint32_t nprod = (kSpec && owner) ? kThreads - 32u * P.cons_warps : kThreads;
   const bool producer = tid < nprod;
   const uint32_t tile = nprod * kPkt;
@@ -180,13 +233,77 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t G = 1u << gs, gl = tid & (G - 1u), fq = tid >> gs;
   const bool flusher = producer && fq < np;
   if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+  if (kCons == kWarpTma && tid == 0) {
+    for (uint32_t r = 0; r < kRing; ++r) {
+      mbar_init(full_bar + r, 1);                     // the issuing lane's expect_tx
+      mbar_init(empty_bar + r, P.cons_warps - 1u);    // every draining warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  uint32_t ring_s = 0, ring_ph = 0;  // consumer pipeline position (kept across chunks)
 
   const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
   for (uint64_t t = 0; t <= nchunks; ++t) {
     // ---------------- consume chunk t-1 into the shared partition --------
-    if (t >= 1 && owner && (!kSpec || !producer)) {
-      const uint32_t cw = kSpec ? warp - nprod / 32u : warp;  // consumer warp index
+    if (kCons == kWarpTma && t >= 1 && owner && !producer) {
+      // TMA-fed drain of chunk t-1: consumer warp 0 issues, warps 1.. OR
+      const uint32_t cw = warp - nprod / 32u, nk = P.cons_warps - 1u;
+      const uint32_t bb = (uint32_t)((t - 1) & 1);
+      const uint32_t* cnts = P.counts + ((size_t)bb * np + self) * ns;
+      const uint4* regions = P.buckets + ((size_t)bb * np + self) * (size_t)P.qstride;
+      const uint32_t lowm = P.lowm, bss = P.bsh_shift;
+      char* const pb = reinterpret_cast<char*>(part);
+      if (cw == 0) {
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' bucket stores -> TMA reads
+          for (uint32_t src = 0; src < ns; ++src) {
+            const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
+            const uint4* reg = regions + (size_t)src * P.region_cap;
+            for (uint32_t off = 0; off < m; off += kSlot) {
+              const uint32_t len = min(kSlot, m - off);
+              mbar_wait(empty_bar + ring_s, ring_ph ^ 1u);
+              mbar_expect_tx(full_bar + ring_s, len * 16u);
+              bulk_g2s(ring + ring_s * kSlot, reg + off, len * 16u, full_bar + ring_s);
+              if (++ring_s == kRing) ring_s = 0, ring_ph ^= 1u;
+            }
+          }
+        }
+        __syncwarp();
+      } else {
+        const uint32_t k = cw - 1u;
+        for (uint32_t src = 0; src < ns; ++src) {
+          const uint32_t m = min(__ldcg(cnts + src), P.region_cap);
+          for (uint32_t off = 0; off < m; off += kSlot) {
+            const uint32_t len = min(kSlot, m - off);
+            mbar_wait(full_bar + ring_s, ring_ph);
+            const uint4* slot = ring + ring_s * kSlot;
+            for (uint32_t e = k * 32u + lane; e < len; e += nk * 32u) {
+              const uint4 u = slot[e];
+              const uint32_t bit = 1u << ((u.x >> bss) & 31u);
+              atomicOr(part + (u.x & lowm), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.x >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.y & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.y >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.z & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.z >> 16)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.w & 0xFFFFu)), bit);
+              atomicOr(reinterpret_cast<uint32_t*>(pb + (u.w >> 16)), bit);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar + ring_s);
+            if (++ring_s == kRing) ring_s = 0, ring_ph ^= 1u;
+          }
+          if (k == 0) {  // the region is dead once read: drop its L2 lines without write-back
+            const uint4* reg = regions + (size_t)src * P.region_cap;
+            for (uint32_t line = lane; line * 8 < m; line += 32)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(reg + line * 8) : "memory");
+          }
+        }
+      }
+    }
+    if (kCons != kWarpTma && t >= 1 && owner && !producer == kSpec) {
+      const uint32_t cw = kSpec ? warp - nprod / 32u : warp;  // draining warp index
       const uint32_t ncw = kSpec ? P.cons_warps : nwarps;
       const uint32_t bb = (uint32_t)((t - 1) & 1);
       const uint32_t* cnts = P.counts + ((size_t)bb * np + self) * ns;
@@ -366,7 +483,7 @@ static uint32_t ilog2_exact(uint64_t d) {
 // Plan for the b-axis partitioned scan; false when the geometry or device
 // cannot host it (the caller then uses K1p or K1).
 static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int max_smem, Plan& P, uint64_t& smem,
-                 uint64_t& scratch, int& hb, bool& spec) {
+                 uint64_t& scratch, int& hb, int& cons) {
   const bool pow2 = (p->k & (p->k - 1)) == 0 && (p->lc & (p->lc - 1)) == 0;
   if (p->lr != kLR || !pow2 || (uint64_t)p->lr * p->lc * p->k > 0xFFFFFFFFull) return false;
   if (getenv("SSPD_PART_LEGACY") != nullptr) return false;
@@ -394,13 +511,17 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
     P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
   }
   smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 16ull * kSeavQueue;
+  // consumer mode (SSPD_BPART_CONS = 0 in line / 1 warp-specialised, global
+  // loads (default) / 2 warp-specialised, TMA ring)
+  cons = kWarpLdg;
+  if (const char* e = getenv("SSPD_BPART_CONS")) cons = std::min(2, std::max(0, atoi(e)));
+  P.cons_warps = cons == kWarpTma ? kConsWarpsTma : kConsWarpsLdg;
+  if (const char* e = getenv("SSPD_BPART_CONS_WARPS")) P.cons_warps = (uint32_t)std::min(16, std::max(2, atoi(e)));
+  const uint64_t ring_bytes = 16ull * kRing * kSlot + 16ull * kRing;  // TMA ring + full/empty mbarriers
+  if (cons == kWarpTma && (int64_t)(smem + ring_bytes) > max_smem) cons = kWarpLdg;  // no room for the ring
+  if (cons == kWarpTma) smem += ring_bytes;
   if ((int64_t)smem > max_smem) return false;
-  // warp-specialised owner CTAs (default; SSPD_BPART_SPEC=0: consume in line,
-  // 4.80 vs 4.60 ms per config-2 window)
-  spec = true;
-  if (const char* e = getenv("SSPD_BPART_SPEC")) spec = atoi(e) != 0;
-  P.cons_warps = kConsWarps;
-  if (const char* e = getenv("SSPD_BPART_CONS_WARPS")) P.cons_warps = (uint32_t)std::min(16, std::max(1, atoi(e)));
+  const bool spec = cons != kInline;
   // producer slice weights: pure producers hash with all 32 warps; owners
   // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;
@@ -445,14 +566,20 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   return true;
 }
 
-template <bool kSeav, bool kSpec>
-static void* kernel_for(int hb) {
+template <bool kSeav, int kCons>
+static void* kernel_hb(int hb) {
   switch (hb) {
-    case 0: return (void*)scan_bpart_kernel<kSeav, 0, kSpec>;
-    case 1: return (void*)scan_bpart_kernel<kSeav, 1, kSpec>;
-    case 2: return (void*)scan_bpart_kernel<kSeav, 2, kSpec>;
-    default: return (void*)scan_bpart_kernel<kSeav, 3, kSpec>;
+    case 0: return (void*)scan_bpart_kernel<kSeav, 0, kCons>;
+    case 1: return (void*)scan_bpart_kernel<kSeav, 1, kCons>;
+    case 2: return (void*)scan_bpart_kernel<kSeav, 2, kCons>;
+    default: return (void*)scan_bpart_kernel<kSeav, 3, kCons>;
   }
+}
+
+template <bool kSeav>
+static void* kernel_for(int hb, int cons) {
+  return cons == kWarpTma ? kernel_hb<kSeav, kWarpTma>(hb)
+                          : (cons == kWarpLdg ? kernel_hb<kSeav, kWarpLdg>(hb) : kernel_hb<kSeav, kInline>(hb));
 }
 
 static void device_limits(int& dev, int& sms, int& max_smem) {
@@ -477,8 +604,8 @@ uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk) {
   bpart::Plan P;
   uint64_t smem = 0, need = 0;
   int hb = 0;
-  bool spec = false;
-  if (!bpart::plan(p, 1, chunk, sms, max_smem, P, smem, need, hb, spec)) return 0;
+  int cons = 0;
+  if (!bpart::plan(p, 1, chunk, sms, max_smem, P, smem, need, hb, cons)) return 0;
   return need;
 }
 
@@ -492,8 +619,8 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   bpart::Plan P;
   uint64_t smem = 0, need = 0;
   int hb = 0;
-  bool spec = false;
-  if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb, spec)) return SSPD_ERR_CONFIG;
+  int cons = 0;
+  if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb, cons)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
@@ -501,8 +628,7 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
               (P.chunk & 3u) == 0)
                  ? 1u
                  : 0u;
-  void* kern = seav ? (spec ? bpart::kernel_for<true, true>(hb) : bpart::kernel_for<true, false>(hb))
-                     : (spec ? bpart::kernel_for<false, true>(hb) : bpart::kernel_for<false, false>(hb));
+  void* kern = seav ? bpart::kernel_for<true>(hb, cons) : bpart::kernel_for<false>(hb, cons);
   // attribute/occupancy answers only change with (kernel, smem, device)
   static void* c_kern = nullptr;
   static uint64_t c_smem = 0;

@@ -1,4 +1,5 @@
-OUT=gpurun_out/p3; mkdir -p $OUT
-S="SSPD_BPART_SPEC=1"
-python tools/sweep_k1p.py --reps 5 "" "$S,SSPD_BPART_CONS_WARPS=8,SSPD_PART_WEIGHT=64" "$S,SSPD_BPART_CONS_WARPS=8,SSPD_PART_WEIGHT=68" "$S,SSPD_BPART_CONS_WARPS=8,SSPD_PART_WEIGHT=78" "$S,SSPD_BPART_CONS_WARPS=6,SSPD_PART_WEIGHT=70" "$S,SSPD_BPART_CONS_WARPS=10,SSPD_PART_WEIGHT=73" "$S,SSPD_BPART_CONS_WARPS=8,SSPD_BPART_TILES=24" "$S,SSPD_BPART_CONS_WARPS=8,SSPD_BPART_TILES=32" > $OUT/sweep3.jsonl 2> $OUT/sweep3.err
-cat $OUT/sweep3.jsonl; tail -3 $OUT/sweep3.err
+OUT=gpurun_out/p5; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "partitioned" > $OUT/pt.log 2>&1; echo pt=$?; tail -2 $OUT/pt.log
+SSPD_BPART_CONS=2 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "partitioned" > $OUT/pt2.log 2>&1; echo pt2=$?; tail -2 $OUT/pt2.log
+timeout 900 python tools/sweep_k1p.py --reps 5 "" "SSPD_BPART_CONS=0" "SSPD_BPART_CONS=2" "SSPD_BPART_CONS=1,SSPD_BPART_TILES=32" > $OUT/sweep.jsonl 2> $OUT/sweep.err
+cat $OUT/sweep.jsonl; tail -3 $OUT/sweep.err
