@@ -44,6 +44,10 @@ def main():
         "dram_write_bytes_per_packet": m.get("dram__bytes_write.sum", 0) / packets,
         "warp_inst_per_packet": m.get("smsp__inst_executed.sum", 0) / packets,
         "l2_red_requests_per_packet": m.get("lts__t_requests_srcunit_tex_op_red.sum", 0) / packets,
+        "issue_active_pct": m.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "shared_atom_bank_conflict_frac": (m["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum"] /
+                                           m["l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"])
+        if m.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum") else None,
         "source": f"ncu --metrics (profiles/{Path(path).name}), config-2 stream",
     }
     OUT.write_text(json.dumps(summary, indent=1))
