@@ -73,6 +73,7 @@ struct Plan {
   uint32_t gshift;       // log2 of the flush group (threads per destination)
   uint32_t tau_mask;
   uint32_t cons_warps;   // kWarpLdg / kWarpTma: consumer warps of an owner CTA
+  uint32_t tma_flush;    // 1: staging runs leave shared memory as TMA bulk stores
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
 };
 
@@ -158,6 +159,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(b))
       : "memory");
 }
+
+// shared -> global bulk copy (TMA store) in this thread's bulk group
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Weighted producer slice of CTA s in [c0, c1): pure producers (s >= nparts)
 // take w_other/w_owner as much as owners; boundaries are 4-aligned.  Full
@@ -430,7 +441,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         // flush: the G = 2^gshift threads of group fq copy destination fq's
         // run of 16-B entries into this CTA's own region of that bucket (no
         // global atomics); `pos` lives in registers, identical in the group
-        if (flusher) {
+        if (P.tma_flush) {
+          // one TMA bulk store per destination run (its lane group's lane 0);
+          // the run must have been read out of shared memory before the next
+          // tile's staging writes: wait_group.read ahead of the barrier
+          if (flusher && gl == 0) {
+            const uint32_t m = min(cnt[fq], P.stage_slots);
+            const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
+            if (fit) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging writes -> TMA reads
+              bulk_s2g(dstq + pos, srcq, fit * 16u);
+              bulk_commit();
+            }
+            for (uint32_t s2 = fit; s2 < m; ++s2) direct_entry<HB>(P, fq, srcq[s2], ldca);  // region full (exact)
+            pos += fit;
+            cnt[fq] = 0;
+            bulk_wait_read();
+          }
+          if (flusher) pos = __shfl_sync(__activemask(), pos, 0, G);  // keep the group's copies equal
+        } else if (flusher) {
           const uint32_t m = min(cnt[fq], P.stage_slots);
           const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
           uint4* dst = dstq + pos;
@@ -453,7 +482,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
       }
       // publish this CTA's run lengths for chunk t
-      if (flusher && gl == 0) __stcg(P.counts + ((size_t)bb * np + fq) * ns + self, pos);
+      if (flusher && gl == 0) {
+        if (P.tma_flush) {  // the bulk stores must be complete and visible before the grid barrier
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __stcg(P.counts + ((size_t)bb * np + fq) * ns + self, pos);
+      }
     }
     grid.sync();  // chunk t produced everywhere; chunk t-1 consumed everywhere
   }
@@ -522,6 +557,11 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   if (cons == kWarpTma) smem += ring_bytes;
   if ((int64_t)smem > max_smem) return false;
   const bool spec = cons != kInline;
+  // staging runs leave shared memory as TMA bulk stores (default; 4.36 vs
+  // 4.65 ms per config-2 window: no per-entry LDS/STG, no short-scoreboard
+  // stalls in the flush) or as 16-B stores by 2^gshift threads each
+  P.tma_flush = 1;
+  if (const char* e = getenv("SSPD_BPART_FLUSH_TMA")) P.tma_flush = atoi(e) != 0;
   // producer slice weights: pure producers hash with all 32 warps; owners
   // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;

@@ -226,6 +226,8 @@ PART_CASES = {
     # K1b consumer modes other than the default warp-specialised global-load drain
     "cons_inline": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
     "cons_tma_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    # K1b flush by threads (16-B stores) instead of TMA bulk stores
+    "flush_threads_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
 }
 
 
@@ -245,6 +247,8 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
         monkeypatch.setenv("SSPD_PART_LEGACY", "1")
     if case.startswith("cons_"):
         monkeypatch.setenv("SSPD_BPART_CONS", "0" if case == "cons_inline" else "2")
+    if case.startswith("flush_threads"):
+        monkeypatch.setenv("SSPD_BPART_FLUSH_TMA", "0")
     dp = DetectorParams(design_n=1e6, **geom)
     _, _, p = params_block(dp)
     rng = np.random.default_rng(77)
@@ -254,7 +258,7 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     if case in ("skewed", "legacy_skewed"):
         hips[: n // 2] = 0xC0A80001  # one host: its 8 cells take half of all updates
         hips[n // 2: n // 2 + 100_000] = 0x0A000001
-    if case in ("skewed_oip", "cons_tma_skewed_oip"):
+    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip"):
         oips[: n // 2] = 0x08080808  # one opposite IP: one b, so one K1b partition
         oips[n // 2: n // 2 + 100_000] = 0x01010101
         perm = rng.permutation(n)
