@@ -565,7 +565,10 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   // producer slice weights: pure producers hash with all 32 warps; owners
   // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;
-  P.w_other = spec ? 76 : 80;
+  // measured with the TMA flush, 16-tile chunks: 64-70 -> 4.27 ms, 72-73 ->
+  // 4.18, 74-76 -> 4.30-4.35, 82 -> 4.58 (slices are whole tiles, so the
+  // optimum is a step, not a slope)
+  P.w_other = spec ? 72 : 80;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
   // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
   // outweigh the part of the bucket exchange that then spills from L2)
