@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <pthread.h>
 #include <thread>
 #include <vector>
 #include "sspd_common.cuh"
@@ -50,11 +51,29 @@ struct Job {
   uint64_t n;
 };
 
+class CopyPool;
+static std::atomic<CopyPool*> g_pool{nullptr};
+static std::mutex g_pool_mu;
+
+// A forked child inherits the pool object but none of its threads: forget
+// it there, so the child builds its own pool on first use instead of
+// waiting forever for workers that do not exist.
+static void forget_pool_in_child() { g_pool.store(nullptr, std::memory_order_relaxed); }
+
 class CopyPool {
  public:
   static CopyPool& get() {
-    static CopyPool* pool = new CopyPool();  // leaked on purpose: detached workers outlive static destructors
-    return *pool;
+    CopyPool* p = g_pool.load(std::memory_order_acquire);
+    if (p) return *p;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    p = g_pool.load(std::memory_order_relaxed);
+    if (!p) {
+      static bool atfork = (pthread_atfork(nullptr, nullptr, forget_pool_in_child), true);
+      (void)atfork;
+      p = new CopyPool();  // leaked on purpose: detached workers outlive static destructors
+      g_pool.store(p, std::memory_order_release);
+    }
+    return *p;
   }
 
   int workers() const { return (int)nworkers_; }
