@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libsspd_b200.so"
-SOURCES = ["scan.cu", "scan_smem.cu", "scan_bpart.cu", "estimate.cu", "sliding.cu", "merge.cu", "ingest.cu", "exact.cu", "abi.cu", "host_stage.cu"]
+SOURCES = ["scan.cu", "scan_smem.cu", "scan_bpart.cu", "estimate.cu", "sliding.cu", "merge.cu", "ingest.cu", "exact.cu", "abi.cu", "host_stage.cu", "radix.cu"]
 HEADERS = ["sspd_common.cuh", "launch.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

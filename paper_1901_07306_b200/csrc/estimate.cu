@@ -31,7 +31,6 @@
 #include <algorithm>
 #include <cstring>
 #include <cuda_runtime.h>
-#include <cub/device/device_radix_sort.cuh>
 #include "sspd_common.cuh"
 #include "launch.cuh"
 
@@ -1044,33 +1043,25 @@ static int restore_launch(const uint8_t* seav, const sspd_params* p, uint32_t rp
   return check_launch();
 }
 
+// csrc/radix.cu: library-free stable LSD radix sort of u32 keys (+ values)
+namespace sspd {
+size_t radix_sort_scratch(uint64_t n, bool with_vals);
+int radix_sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, void* scratch, size_t scratch_bytes,
+                   cudaStream_t st);
+}  // namespace sspd
+
 extern "C" int sspd_sort_candidates(uint32_t* ip, uint32_t* aux, uint64_t n, void* scratch, size_t* scratch_bytes,
                                     void* stream) {
   if (!scratch_bytes) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t alt = ((n * sizeof(uint32_t) + 255) / 256) * 256;
-  size_t temp = 0;
-  cub::DoubleBuffer<uint32_t> keys(ip, ip), vals(aux, aux);
-  if (cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, vals, (int)(n ? n : 1), 0, 32, st) != cudaSuccess)
-    return SSPD_ERR_CUDA;
-  const size_t need = 2 * alt + temp + 256;
+  const size_t need = radix_sort_scratch(n ? n : 1, true);
   if (!scratch) {
     *scratch_bytes = need;
     return SSPD_OK;
   }
   if (*scratch_bytes < need) return SSPD_ERR_CAPACITY;
   if (n <= 1) return SSPD_OK;
-  uint8_t* s = static_cast<uint8_t*>(scratch);
-  uint32_t* ip_alt = reinterpret_cast<uint32_t*>(s);
-  uint32_t* aux_alt = reinterpret_cast<uint32_t*>(s + alt);
-  void* tmp = s + 2 * alt;
-  cub::DoubleBuffer<uint32_t> k2(ip, ip_alt), v2(aux, aux_alt);
-  if (cub::DeviceRadixSort::SortPairs(tmp, temp, k2, v2, (int)n, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
-  if (k2.Current() != ip) {
-    cudaMemcpyAsync(ip, k2.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(aux, v2.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
-  }
-  return check_launch();
+  return radix_sort_u32(ip, aux, n, scratch, *scratch_bytes, st);
 }
 
 extern "C" int sspd_filter(const uint8_t* ldca, const sspd_params* p, const uint32_t* ips, uint64_t n,
@@ -1175,12 +1166,7 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   const uint32_t hshift = 32 - (31 - __builtin_clz(nb));
   // the filter and the report list need the candidate IPs only: sort keys
   // (restore's AND-weights are not part of a report)
-  size_t sort_tmp = 0;
-  {
-    cub::DoubleBuffer<uint32_t> k0(nullptr, nullptr);
-    if (cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, k0, (int)C, 0, 32, st) != cudaSuccess)
-      return SSPD_ERR_CUDA;
-  }
+  const size_t sort_tmp = radix_sort_scratch(C, false);
   const size_t segs = (C + kSeg - 1) / kSeg;
   // [ip | aux | ip_alt | aux_alt | z0 | keep | sort temp | compaction segs | hist, cursor | starts]
   const size_t o_aux = vec, o_ipa = 2 * vec, o_z0 = 4 * vec, o_keep = 5 * vec;  // [3 vec, 4 vec): spare
@@ -1223,10 +1209,9 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
     if (cudaMemsetAsync(ip, 0xFF, C * 4, st) != cudaSuccess) return SSPD_ERR_CUDA;
     rc = restore_launch(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, nullptr, 0, stream);
     if (rc) return rc;
-    size_t tb = sort_tmp;
-    cub::DoubleBuffer<uint32_t> kb(ip, ipa);
-    if (cub::DeviceRadixSort::SortKeys(s8 + o_tmp, tb, kb, (int)C, 0, 32, st) != cudaSuccess) return SSPD_ERR_CUDA;
-    sorted = kb.Current();
+    rc = radix_sort_u32(ip, nullptr, C, s8 + o_tmp, sort_tmp, st);
+    if (rc) return rc;
+    sorted = ip;
   }
   const int grid = grid_for(filter_kernel, 256, C * 32);
   filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);

@@ -460,3 +460,30 @@ def test_finalize_bucket_sort_vs_oracle(cuda, oracle, skewed):
     assert got == want
     assert st.seav._radix_sort == skewed
     assert len(set(heavy.tolist()) & set(got)) > nheavy // 2
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 1023, 4097, 100_003, 1_048_579])
+def test_candidate_radix_sort_stable(cuda, n):
+    """sspd_sort_candidates (csrc/radix.cu, no CUB): keys ascending, values
+    carried along, equal keys in their input order (stable), clustered and
+    duplicated keys included."""
+    import ctypes
+
+    import torch
+
+    from paper_1901_07306_b200._device import call, stream_ptr
+
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    keys[: n // 3] = (keys[: n // 3] & 0xFF) | 0xC0A80000  # one /16: deep equal prefixes
+    keys[n // 2: n // 2 + n // 5] = keys[n // 2]           # runs of duplicates
+    vals = np.arange(n, dtype=np.uint32)
+    k = torch.from_numpy(keys.view(np.int32)).cuda()
+    v = torch.from_numpy(vals.view(np.int32)).cuda()
+    need = ctypes.c_size_t(0)
+    call("sspd_sort_candidates", k.data_ptr(), v.data_ptr(), n, None, ctypes.byref(need), stream_ptr())
+    scratch = torch.empty(need.value, dtype=torch.uint8, device="cuda")
+    call("sspd_sort_candidates", k.data_ptr(), v.data_ptr(), n, scratch.data_ptr(), ctypes.byref(need), stream_ptr())
+    order = np.argsort(keys, kind="stable")
+    assert (k.cpu().numpy().view(np.uint32) == keys[order]).all()
+    assert (v.cpu().numpy().view(np.uint32) == vals[order]).all()
