@@ -199,6 +199,9 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 // measured slower on B200: 6.3-6.9 ms -- the 16 KB ring the shared-memory
 // budget leaves keeps too few bytes in flight).
 enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2 };
+#ifndef SSPD_BPART_DRAIN_LOADS
+#define SSPD_BPART_DRAIN_LOADS 4
+#endif
 constexpr uint32_t kConsWarpsLdg = 8;  // measured: 4 -> 5.48 ms, 6 -> 4.70, 8 -> 4.60, 10 -> 4.75
 constexpr uint32_t kConsWarpsTma = 6;
 
@@ -329,13 +332,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t src = src0, j = 0; src < ns && j < 32u; src += ncw, ++j) {
         const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
         const uint4* reg = regions + (size_t)src * P.region_cap;  // 128-B aligned
-        for (uint32_t j0 = lane; j0 < m; j0 += 128) {  // 4 independent 16-B loads in flight per lane
-          uint4 u[4];
+        // kInFlight independent 16-B loads in flight per lane (8 measured
+        // 5.4 vs 4.2 ms: the kernel's 64-register budget is shared with the
+        // producers, which then spill)
+        constexpr int kInFlight = kSpec ? SSPD_BPART_DRAIN_LOADS : 4;
+        for (uint32_t j0 = lane; j0 < m; j0 += 32 * kInFlight) {
+          uint4 u[kInFlight];
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
+          for (int g = 0; g < kInFlight; ++g)
             if (j0 + 32 * g < m) u[g] = __ldcg(reg + j0 + 32 * g);
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
+          for (int g = 0; g < kInFlight; ++g) {
             if (j0 + 32 * g < m) {
               const uint4 e = u[g];
               const uint32_t bit = 1u << ((e.x >> bss) & 31u);

@@ -1,3 +1,3 @@
-OUT=gpurun_out/p9; mkdir -p $OUT
-timeout 1200 python tools/sweep_k1p.py --reps 6 "SSPD_PART_WEIGHT=72" "SSPD_PART_WEIGHT=73" "SSPD_PART_WEIGHT=74" "SSPD_PART_WEIGHT=75" "SSPD_PART_WEIGHT=73,SSPD_BPART_TILES=20" "SSPD_PART_WEIGHT=73,SSPD_BPART_TILES=24" "SSPD_PART_WEIGHT=73,SSPD_BPART_TILES=32" "SSPD_PART_WEIGHT=73,SSPD_BPART_TILES=10" > $OUT/sweep.jsonl 2> $OUT/sweep.err
+OUT=gpurun_out/p10; mkdir -p $OUT
+timeout 1200 python tools/sweep_k1p.py --reps 6 "" "SSPD_BPART_CONS_WARPS=4" "SSPD_BPART_CONS_WARPS=6" "SSPD_BPART_CONS_WARPS=4,SSPD_PART_WEIGHT=68" "SSPD_BPART_CONS_WARPS=6,SSPD_PART_WEIGHT=70" > $OUT/sweep.jsonl 2> $OUT/sweep.err
 cat $OUT/sweep.jsonl; tail -3 $OUT/sweep.err
