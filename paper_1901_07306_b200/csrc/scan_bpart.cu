@@ -555,7 +555,17 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 16ull * kSeavQueue;
   // consumer mode (SSPD_BPART_CONS = 0 in line / 1 warp-specialised, global
   // loads (default) / 2 warp-specialised, TMA ring)
+  // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
+  // outweigh the part of the bucket exchange that then spills from L2)
+  uint32_t tiles = 16;
+  if (const char* e = getenv("SSPD_BPART_TILES")) tiles = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 16;
+  P.chunk = chunk ? ((chunk + 3) & ~3ull) : (uint64_t)P.nsrc * kTile * tiles;
+  if (P.chunk >= (1ull << 32)) return false;  // slice offsets are 32-bit
   cons = kWarpLdg;
+  // a single-chunk launch (a sliding slice, a small batch) has no chunk to
+  // drain while the next is produced: every warp produces, then drains
+  // (config-4 slice: 66 vs 73 us)
+  if (n <= P.chunk) cons = kInline;
   if (const char* e = getenv("SSPD_BPART_CONS")) cons = std::min(2, std::max(0, atoi(e)));
   P.cons_warps = cons == kWarpTma ? kConsWarpsTma : kConsWarpsLdg;
   if (const char* e = getenv("SSPD_BPART_CONS_WARPS")) P.cons_warps = (uint32_t)std::min(16, std::max(2, atoi(e)));
@@ -577,12 +587,6 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   // optimum is a step, not a slope)
   P.w_other = spec ? 72 : 80;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
-  // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
-  // outweigh the part of the bucket exchange that then spills from L2)
-  uint32_t tiles = 16;
-  if (const char* e = getenv("SSPD_BPART_TILES")) tiles = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 16;
-  P.chunk = chunk ? ((chunk + 3) & ~3ull) : (uint64_t)P.nsrc * kTile * tiles;
-  if (P.chunk >= (1ull << 32)) return false;  // slice offsets are 32-bit
   const double share =
       (double)std::max(P.w_owner, P.w_other) / ((double)np * P.w_owner + (double)(P.nsrc - np) * P.w_other);
   const double rmean = (double)P.chunk * share / np;  // largest producer -> one destination
