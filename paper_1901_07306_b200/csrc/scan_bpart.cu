@@ -74,6 +74,8 @@ struct Plan {
   uint32_t tau_mask;
   uint32_t cons_warps;   // kWarpLdg / kWarpTma: consumer warps of an owner CTA
   uint32_t tma_flush;    // 1: staging runs leave shared memory as TMA bulk stores
+  uint32_t* ready;       // kWarpFlag: [dst][src] = chunks of src published to dst (zeroed per launch)
+  uint32_t* drained;     // kWarpFlag: [dst] = chunks dst has drained
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
 };
 
@@ -160,6 +162,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // shared -> global bulk copy (TMA store) in this thread's bulk group
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
@@ -197,8 +208,13 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 // window); kWarpTma = the same split, fed by TMA bulk copies into a
 // shared-memory ring (1 issuing lane + draining warps; bit-exact but
 // measured slower on B200: 6.3-6.9 ms -- the 16 KB ring the shared-memory
-// budget leaves keeps too few bytes in flight).
-enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2 };
+// budget leaves keeps too few bytes in flight); kWarpFlag = kWarpLdg with
+// the per-chunk grid barrier replaced by point-to-point release/acquire
+// flags (ready[dst][src] per published chunk, drained[dst] per drained
+// chunk; producers wait only before reusing a bucket buffer) -- bit-exact,
+// 4.23 vs 4.19 ms: the barrier share of the stall samples is the drain's
+// pace, not the barrier itself.
+enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2, kWarpFlag = 3 };
 #ifndef SSPD_BPART_DRAIN_LOADS
 #define SSPD_BPART_DRAIN_LOADS 4
 #endif
@@ -328,6 +344,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // source w+W*j, fetched at once so no region waits on its count
       for (uint32_t src0 = cw; src0 < ns; src0 += 32u * ncw) {
       const uint32_t my_src = src0 + ncw * lane;
+      if (kCons == kWarpFlag && my_src < ns) {  // chunk t-1 of this source published to us?
+        const uint32_t* f = P.ready + (size_t)self * ns + my_src;
+        while (ld_acquire(f) < (uint32_t)t) __nanosleep(64);
+      }
       const uint32_t my_cnt = my_src < ns ? min(__ldcg(cnts + my_src), P.region_cap) : 0u;
       for (uint32_t src = src0, j = 0; src < ns && j < 32u; src += ncw, ++j) {
         const uint32_t m = __shfl_sync(0xffffffffu, my_cnt, j);
@@ -365,9 +385,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
     }
+    if (kCons == kWarpFlag && t >= 1 && owner && !producer) {
+      // every draining warp is done reading chunk t-1's buckets: tell the
+      // producers that buffer (t-1)&1 may be overwritten
+      asm volatile("bar.sync 2, %0;" ::"r"(kThreads - nprod) : "memory");
+      if (tid == nprod) st_release(P.drained + self, (uint32_t)t);
+    }
     // ---------------- produce chunk t ------------------------------------
     if (t < nchunks && producer) {
       const uint32_t bb = (uint32_t)(t & 1);
+      if (kCons == kWarpFlag && t >= 2) {
+        // buffer bb last held chunk t-2: every destination must have drained it
+        if (warp == 0) {
+          for (uint32_t q0 = 0; q0 < np; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            if (q < np)
+              while (ld_acquire(P.drained + q) < (uint32_t)(t - 1)) __nanosleep(64);
+          }
+          __syncwarp();
+        }
+        pbar();
+      }
       const uint64_t c0 = t * P.chunk;
       const uint64_t c1 = min(P.n, c0 + P.chunk);
       const uint64_t lo = slice_start(P, c0, c1, self);
@@ -495,9 +533,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         __stcg(P.counts + ((size_t)bb * np + fq) * ns + self, pos);
+        if (kCons == kWarpFlag) st_release(P.ready + (size_t)fq * ns + self, (uint32_t)(t + 1));
       }
     }
-    grid.sync();  // chunk t produced everywhere; chunk t-1 consumed everywhere
+    // chunk t produced everywhere; chunk t-1 consumed everywhere -- or, with
+    // point-to-point flags, only before the fold
+    if (kCons != kWarpFlag || t == nchunks) grid.sync();
   }
   // fold the partition into the global LDCA: word (row, cell, j) of
   // partition q is global word (row*lc + cell)*k/32 + q*2^HB + j.  After the
@@ -566,7 +607,7 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   // drain while the next is produced: every warp produces, then drains
   // (config-4 slice: 66 vs 73 us)
   if (n <= P.chunk) cons = kInline;
-  if (const char* e = getenv("SSPD_BPART_CONS")) cons = std::min(2, std::max(0, atoi(e)));
+  if (const char* e = getenv("SSPD_BPART_CONS")) cons = std::min(3, std::max(0, atoi(e)));
   P.cons_warps = cons == kWarpTma ? kConsWarpsTma : kConsWarpsLdg;
   if (const char* e = getenv("SSPD_BPART_CONS_WARPS")) P.cons_warps = (uint32_t)std::min(16, std::max(2, atoi(e)));
   const uint64_t ring_bytes = 16ull * kRing * kSlot + 16ull * kRing;  // TMA ring + full/empty mbarriers
@@ -579,6 +620,7 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   // stalls in the flush) or as 16-B stores by 2^gshift threads each
   P.tma_flush = 1;
   if (const char* e = getenv("SSPD_BPART_FLUSH_TMA")) P.tma_flush = atoi(e) != 0;
+  if (cons == kWarpFlag && !P.tma_flush) cons = kWarpLdg;  // flags are released by the one flushing lane
   // producer slice weights: pure producers hash with all 32 warps; owners
   // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;
@@ -604,7 +646,8 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
     }
   }
   P.n = n;
-  scratch = 16ull * 2 * np * P.qstride + 4ull * 2 * np * P.nsrc;
+  // [buckets | counts | ready flags [np][ns] | drained flags [np]]
+  scratch = 16ull * 2 * np * P.qstride + 4ull * 2 * np * P.nsrc + 4ull * np * P.nsrc + 4ull * np;
   P.k_mask = p->k - 1;
   P.lc_mask = p->lc - 1;
   P.log2k = ilog2_exact(p->k);
@@ -632,8 +675,12 @@ static void* kernel_hb(int hb) {
 
 template <bool kSeav>
 static void* kernel_for(int hb, int cons) {
-  return cons == kWarpTma ? kernel_hb<kSeav, kWarpTma>(hb)
-                          : (cons == kWarpLdg ? kernel_hb<kSeav, kWarpLdg>(hb) : kernel_hb<kSeav, kInline>(hb));
+  switch (cons) {
+    case kWarpTma: return kernel_hb<kSeav, kWarpTma>(hb);
+    case kWarpLdg: return kernel_hb<kSeav, kWarpLdg>(hb);
+    case kWarpFlag: return kernel_hb<kSeav, kWarpFlag>(hb);
+    default: return kernel_hb<kSeav, kInline>(hb);
+  }
 }
 
 static void device_limits(int& dev, int& sms, int& max_smem) {
@@ -678,6 +725,11 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
+  P.ready = P.counts + 2ull * P.nparts * P.nsrc;
+  P.drained = P.ready + (uint64_t)P.nparts * P.nsrc;
+  if (cons == bpart::kWarpFlag &&
+      cudaMemsetAsync(P.ready, 0, 4ull * P.nparts * (P.nsrc + 1), static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return SSPD_ERR_CUDA;
   P.vec_ok = (((reinterpret_cast<uintptr_t>(hips) | reinterpret_cast<uintptr_t>(oips)) & 15u) == 0 &&
               (P.chunk & 3u) == 0)
                  ? 1u

@@ -226,6 +226,7 @@ PART_CASES = {
     # K1b consumer modes other than the default warp-specialised global-load drain
     "cons_inline": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
     "cons_tma_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    "cons_flags_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
     # K1b flush by threads (16-B stores) instead of TMA bulk stores
     "flush_threads_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
 }
@@ -246,7 +247,7 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     if case.startswith("legacy"):
         monkeypatch.setenv("SSPD_PART_LEGACY", "1")
     if case.startswith("cons_"):
-        monkeypatch.setenv("SSPD_BPART_CONS", "0" if case == "cons_inline" else "2")
+        monkeypatch.setenv("SSPD_BPART_CONS", {"cons_inline": "0", "cons_flags_skewed_oip": "3"}.get(case, "2"))
     if case.startswith("flush_threads"):
         monkeypatch.setenv("SSPD_BPART_FLUSH_TMA", "0")
     dp = DetectorParams(design_n=1e6, **geom)
@@ -258,7 +259,7 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     if case in ("skewed", "legacy_skewed"):
         hips[: n // 2] = 0xC0A80001  # one host: its 8 cells take half of all updates
         hips[n // 2: n // 2 + 100_000] = 0x0A000001
-    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip"):
+    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "cons_flags_skewed_oip"):
         oips[: n // 2] = 0x08080808  # one opposite IP: one b, so one K1b partition
         oips[n // 2: n // 2 + 100_000] = 0x01010101
         perm = rng.permutation(n)
@@ -269,7 +270,8 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     assert lib().sspd_scan_partitioned_variant(st.seav._params, 0) == variant
     if case == "tiny_chunks":
         st.partitioned_chunk = 1 << 14
-    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "k16384_hb2"):
+    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "cons_flags_skewed_oip",
+                "k16384_hb2"):
         st.partitioned_chunk = 1 << 20  # several chunks: the warp-specialised drain overlaps production
     st.process_batch(hips[: n // 3], oips[: n // 3])
     st.process_batch(hips[n // 3:], oips[n // 3:])
