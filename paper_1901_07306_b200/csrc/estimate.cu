@@ -559,7 +559,24 @@ __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__
     const uint64_t off_b =
         lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, seed_b, p.div_lc)) * cell_bytes : 0;
     uint32_t pop = 0;
-    if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
+    if (p.lr == 8 && cell_bytes == 1024 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
+      // the BASELINE geometry (LR = 8, k = 8192): all 8 cell offsets first,
+      // then the 8 rows' 16-byte loads of each half in flight at once (the
+      // generic loop below issues one row's loads per shuffle round trip)
+      uint64_t off[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) off[i] = __shfl_sync(0xFFFFFFFFu, off_a, i);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // two halves of the 1 KB cells, 8 loads in flight each
+        uint4 w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = __ldg(reinterpret_cast<const uint4*>(ldca + off[i]) + 32 * h + lane);
+        uint4 a = w[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) a.x &= w[i].x, a.y &= w[i].y, a.z &= w[i].z, a.w &= w[i].w;
+        pop += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+      }
+    } else if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
       // 16-byte loads: lane l ANDs words 4l..4l+3 of each 128-word stripe
       const uint32_t vecs = (uint32_t)(cell_bytes >> 4);
       for (uint32_t base = 0; base < vecs; base += 32) {
