@@ -361,14 +361,57 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
         const uint64_t full = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
         const uint64_t hot0 = misc->rmask[0];
         const uint32_t h0 = (uint32_t)__popcll(hot0);
+        const uint32_t lane = G.tid;
+        // the walk is spread over consistent (row-0, row-1) PAIRS, not row-0
+        // columns: a SEA with few hot row-0 columns but many pairs (a busy
+        // late-trace SEA) keeps all 32 lanes walking.  Row-0 hot column j
+        // (j = lane, lane + 32) and the size of its consistent row-1 set:
+        auto row1_of = [&](uint32_t c0) {
+          return misc->rmask[1] & col_match(T->keymask[1],
+                                            index_of(scatter_col(c0, T->isb[0], T->ibn[0], P.w), T->isb[1],
+                                                     T->ibn[1], P.w),
+                                            T->sc[1]);
+        };
+        const uint32_t cnt_a = lane < h0 ? (uint32_t)__popcll(row1_of(nth_bit64(hot0, lane))) : 0u;
+        const uint32_t cnt_b = lane + 32 < h0 ? (uint32_t)__popcll(row1_of(nth_bit64(hot0, lane + 32))) : 0u;
+        uint32_t inc_a = cnt_a, inc_b = cnt_b;  // inclusive prefixes over j = 0..63
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t ya = __shfl_up_sync(0xFFFFFFFFu, inc_a, o), yb = __shfl_up_sync(0xFFFFFFFFu, inc_b, o);
+          if (lane >= (uint32_t)o) inc_a += ya, inc_b += yb;
+        }
+        inc_b += __shfl_sync(0xFFFFFFFFu, inc_a, 31);
+        const uint32_t npairs = __shfl_sync(0xFFFFFFFFu, inc_b, 31);
+        auto incl_at = [&](uint32_t j) {  // every lane takes part (per-lane source j)
+          const uint32_t a = __shfl_sync(0xFFFFFFFFu, inc_a, j & 31), b = __shfl_sync(0xFFFFFFFFu, inc_b, j & 31);
+          return j < 32 ? a : b;
+        };
         uint64_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR], rem_st[SSPD_MAX_SR];
-        for (uint32_t t = G.tid; t < h0; t += 32) {
-          const uint32_t c0 = nth_bit64(hot0, t);
-          lp_st[0] = scatter_col(c0, T->isb[0], T->ibn[0], P.w);
-          and_st[0] = full & sm[T->off_regs[0] + c0];
-          uint32_t lvl = 1;
-          rem_st[1] = misc->rmask[1] & col_match(T->keymask[1], index_of(lp_st[0], T->isb[1], T->ibn[1], P.w), T->sc[1]);
-          while (lvl >= 1) {
+        for (uint32_t base = 0; base < npairs; base += 32) {
+          const uint32_t t = base + lane;
+          // row-0 entry of pair t: the first j with incl(j) > t
+          uint32_t lo = 0, hi = 63;
+#pragma unroll
+          for (int it = 0; it < 6; ++it) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (incl_at(mid) > t) hi = mid; else lo = mid + 1;
+          }
+          const uint32_t j = lo;
+          const uint32_t excl = incl_at(j == 0 ? 0 : j - 1);
+          if (t >= npairs) continue;
+          const uint32_t c0 = nth_bit64(hot0, j);
+          const uint64_t r1 = row1_of(c0);
+          const uint32_t c1 = nth_bit64(r1, t - (j == 0 ? 0u : excl));
+          lp_st[1] = scatter_col(c0, T->isb[0], T->ibn[0], P.w) | scatter_col(c1, T->isb[1], T->ibn[1], P.w);
+          and_st[1] = full & sm[T->off_regs[0] + c0] & sm[T->off_regs[1] + c1];
+          if (sr == 2) {
+            const uint32_t wgt = (uint32_t)__popcll(and_st[1]);
+            if (wgt >= 3) emit_candidate(P, lp_st[1], rp, wgt, out_ip, out_aux, out_capacity, out_count);
+            continue;
+          }
+          uint32_t lvl = 2;
+          rem_st[2] = misc->rmask[2] & col_match(T->keymask[2], index_of(lp_st[1], T->isb[2], T->ibn[2], P.w), T->sc[2]);
+          while (lvl >= 2) {
             const uint64_t rem = rem_st[lvl];
             if (rem == 0) {
               --lvl;
