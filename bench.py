@@ -11,20 +11,27 @@ geometric(0.3) duplicates -- seeded synthetic data generated on the GPU
 k=8192); SEAV r=12 (2 MiB) because the reference default r=4 overflows
 every register array at this scale.
 
-One step = K1 scan of the whole window + finalize (K5 restore, sort, K6
-filter, compaction, report D2H) + reset.  `value` is timed with the inputs
-resident in HBM; `e2e` is the same step through the public API from pinned
-HOST buffers (DetectorState.process_host_stream: H2D inside the timed
-region, double-buffered) with the report list read back.
+One step = the scan of the whole window (K1b: the LDCA in shared memory,
+cut along its b axis) + finalize (K5 restore, sort, K6 filter, compaction,
+report D2H) + reset.  `value` is timed with the inputs resident in HBM;
+`e2e` is the same step through the public API from pinned HOST buffers
+(DetectorState.process_host_stream: H2D inside the timed region,
+double-buffered) with the report list read back; `e2e.dropin` is the
+reference's own call pattern (65,536-pair numpy process_batch calls).
 
-N > 1 (torchrun, one process per GPU): weak scaling -- every rank is one
-border router scanning its own config-2-sized window (seed 2 + rank); the
-per-rank sketches are OR-merged on rank 0 (multigpu.py: CUDA-IPC peer
-reads over NVLink, NCCL gather as fallback) and rank 0 detects once.
+--gpus N > 1: the N ranks are launched by this script (torch.distributed.run
+on 127.0.0.1) unless it already runs under torchrun.  Config 2 = weak
+scaling: every rank is one border router scanning its own config-2-sized
+window (seed 2 + rank); the per-rank sketches are OR-merged on rank 0
+(multigpu.py: CUDA-IPC peer reads over NVLink, NCCL gather as fallback)
+and rank 0 detects once.  --config 3 / 4 / 5 have multi-rank modes too
+(DESIGN.md §6).  --same-device puts every rank on GPU 0 (gloo; a protocol
+check).
 
 --impl reference: the reference path on the host CPU (the oracle port,
-oracle/sspd_oracle.c, all host threads) on a bounded sample of the same
-workload, printed on the same metric.
+oracle/sspd_oracle.c, on all host threads) over the full config-2 window,
+plus the reference package itself on a bounded sample (reference_python),
+printed on the same metric.
 """
 
 from __future__ import annotations
@@ -614,7 +621,7 @@ def run_gpu(args) -> dict | None:
                    "l2": "inputs (2 GiB/window) exceed the 126 MB L2; no flush needed",
                    "seav_r": dp.r, "ldca": "LR=8 LC=1024 k=8192 (8 MiB)"},
         "e2e": e2e,
-        # per step: K1p scan, K5 restore, bucket sort (scatter + per-bucket
+        # per step: the scan, K5 restore, bucket sort (scatter + per-bucket
         # rank), K6 filter, compaction (count + scatter) = 7 launches of
         # libsspd_b200.so (+ the merge kernels at N > 1)
         "gpu_launches": args.steps * (7 + (2 if merger else 0)),
@@ -938,7 +945,7 @@ def run_sharded(args) -> dict | None:
     into ONE local sketch: OR idempotence), the per-rank sketches are
     OR-merged onto rank 0 (multigpu.OrMerger: CUDA-IPC peer reads), and
     rank 0 detects once.  Strong scaling: the 2^30 packets are fixed.
-    A step = every local shard's K1 scan + merge + finalize + reset."""
+    A step = every local shard's scan (K1b) + merge + finalize + reset."""
     import torch
 
     from paper_1901_07306_b200 import DetectorParams, DetectorState
