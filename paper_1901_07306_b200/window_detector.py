@@ -518,8 +518,9 @@ class DetectorState:
 
         hs = getattr(self, "_hstage", None)
         if hs is None or hs["cap"] != self.host_stage_pairs:
-            if hs is not None:
+            if hs is not None:  # resized: scan what is staged, let the old buffers' copies/scans finish
                 self._flush_host()
+                torch.cuda.synchronize()
             cap, dev = int(self.host_stage_pairs), device()
             pin = lambda: torch.empty(cap, dtype=torch.int32, pin_memory=True)  # noqa: E731
             dbuf = lambda: torch.empty(cap, dtype=torch.int32, device=dev)  # noqa: E731
