@@ -242,6 +242,16 @@ SSPD_API int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes,
                uint64_t now_wrapped, uint64_t window_slices,
                uint64_t clamp_value, void* stream);
 
+/* TimestampPool.touch_batch (sliding.py:77-79): pool[slot_indexes[j]] =
+ * now_wrapped for j < n (int64 device indexes; negative ones count from
+ * the end, as numpy's).  An index outside [-n_slots, n_slots) is skipped
+ * and ORs 1 into *bad_flag (device u32, may be NULL).  The Python host
+ * checks the bounds first and raises IndexError before any store, as the
+ * reference's numpy fancy-index store does. */
+SSPD_API int sspd_touch_slots(void* pool, uint64_t n_slots, uint32_t ts_bytes,
+               const int64_t* slot_indexes, uint64_t n, uint64_t now_wrapped,
+               uint32_t* bad_flag, void* stream);
+
 /* ---- K4 materialize ----------------------------------------------------
  * materialize_seav (sliding.py:191-203): active slots -> SEAV payload.
  * materialize_ldca (sliding.py:215-220): active slots -> packed LDCA bytes.

@@ -113,6 +113,7 @@ _SIGS = {
     "sspd_seav_advance": (C.c_int, [_VP, _U32, _PP, _VP, _VP, _U64, _VP, _U32, _U64, _U64, _VP]),
     "sspd_materialize_seav_if": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP, _VP]),
     "sspd_sweep": (C.c_int, [_VP, _U64, _U32, _U64, _U64, _U64, _VP]),
+    "sspd_touch_slots": (C.c_int, [_VP, _U64, _U32, _VP, _U64, _U64, _VP, _VP]),
     "sspd_materialize_seav": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP]),
     "sspd_materialize_ldca": (C.c_int, [_VP, _U32, _PP, _U64, _U64, _VP, _VP]),
     "sspd_scan_sliding_deferred": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP, _VP, _U64, _VP, _VP,

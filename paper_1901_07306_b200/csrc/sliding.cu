@@ -201,6 +201,23 @@ __global__ void __launch_bounds__(256) ages_kernel(const T* __restrict__ pool, u
     out[j] = (uint64_t)(T)(now - pool[j]);
 }
 
+// TimestampPool.touch_batch (sliding.py:77-79): ts[slot_indexes] = now.
+// Duplicates all store the same value, so the scatter needs no ordering.
+template <typename T>
+__global__ void touch_slots_kernel(T* __restrict__ pool, uint64_t n_slots, const int64_t* __restrict__ idx,
+                                   uint64_t n, T now, uint32_t* __restrict__ bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    int64_t s = idx[j];
+    if (s < 0) s += (int64_t)n_slots;  // numpy's negative indexes
+    if (s < 0 || (uint64_t)s >= n_slots) {
+      if (bad) atomicOr(bad, 1u);
+    } else {
+      pool[s] = now;
+    }
+  }
+}
+
 }  // namespace sspd
 
 using namespace sspd;
@@ -222,6 +239,19 @@ extern "C" int sspd_sweep(void* pool, uint64_t n_slots, uint32_t ts_bytes, uint6
   SSPD_TS_DISPATCH(ts_bytes, {
     const int grid = grid_for(sweep_kernel<T>, 256, n_slots);
     sweep_kernel<T><<<grid, 256, 0, st>>>((T*)pool, n_slots, (T)now_wrapped, window_slices, (T)clamp_value);
+  })
+  return check_launch();
+}
+
+extern "C" int sspd_touch_slots(void* pool, uint64_t n_slots, uint32_t ts_bytes, const int64_t* slot_indexes,
+                                uint64_t n, uint64_t now_wrapped, uint32_t* bad_flag, void* stream) {
+  if (n == 0) return SSPD_OK;
+  if (!pool || !slot_indexes) return SSPD_ERR_DATA;
+  if (n_slots > (uint64_t)INT64_MAX) return SSPD_ERR_CONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SSPD_TS_DISPATCH(ts_bytes, {
+    const int grid = grid_for(touch_slots_kernel<T>, 256, n);
+    touch_slots_kernel<T><<<grid, 256, 0, st>>>((T*)pool, n_slots, slot_indexes, n, (T)now_wrapped, bad_flag);
   })
   return check_launch();
 }

@@ -181,8 +181,17 @@ class SeavConfig:
         return rotated & ((1 << self.ibn[row]) - 1)
 
     def index_of_array(self, row: int, lp: np.ndarray) -> np.ndarray:
-        return np.array([self.index_of(row, int(x)) for x in np.asarray(lp).reshape(-1)],
-                        dtype=np.uint64).reshape(np.shape(lp))
+        """index_of over an array (short_sketch.py:196-205), vectorised: the
+        same rotate-right of the w-bit LP (w <= 32, so uint64 holds it)."""
+        if not 0 <= row < self.sr:
+            raise ConfigError(f"row {row} out of range [0, {self.sr})")
+        w = self.lp_bits
+        wmask = np.uint64((1 << w) - 1)
+        x = np.asarray(lp).astype(np.uint64) & wmask
+        s = self.isb[row] % w
+        if s:
+            x = ((x >> np.uint64(s)) | (x << np.uint64(w - s))) & wmask
+        return x & np.uint64((1 << self.ibn[row]) - 1)
 
     def lp_from_indexes(self, indexes) -> int:
         """Inverse of index_of over all rows (short_sketch.py:196-205)."""
@@ -223,6 +232,23 @@ class CandidateHost:
 
 
 # ------------------------------------------------------------------ sketch
+class _RowList(list):
+    """`SeavSketch.rows`: a list of host row snapshots whose item assignment
+    writes through to the device."""
+
+    def __init__(self, sketch):
+        super().__init__()
+        self._sketch = sketch
+
+    def __setitem__(self, i, regs):
+        if isinstance(i, slice):
+            raise TypeError("assign SeavSketch rows one at a time, or the whole list")
+        super().__setitem__(i, self._sketch._store_row(i, regs))
+
+    def __reduce__(self):  # copies and pickles are plain lists of the arrays
+        return (list, (list(self),))
+
+
 class SeavSketch(PreReadHook):
     """Device-resident SEAV with the reference's API (short_sketch.py:259-408).
 
@@ -277,15 +303,44 @@ class SeavSketch(PreReadHook):
 
     @property
     def rows(self) -> list[np.ndarray]:
-        """Host snapshot of the registers, one (2^r, SC_i) array per row."""
+        """Host snapshot of the registers, one (2^r, SC_i) array per row.
+
+        The arrays are read-only (an in-place write would not reach the
+        device, so it fails loudly); assigning a row through the list
+        (`sk.rows[i] = regs`, as the reference's sliding.py:202 does) or the
+        whole list (`sk.rows = [...]`) uploads it."""
         flat = self._buf[: self.nbytes].cpu().numpy()
         dt = register_dtype(self.config.g)
-        out, off = [], 0
+        out, off = _RowList(self), 0
         for sc in self.config.sc:
             nb = (1 << self.config.r) * sc * self.config.register_bytes
-            out.append(flat[off:off + nb].view(dt).reshape(1 << self.config.r, sc).copy())
+            row = flat[off:off + nb].view(dt).reshape(1 << self.config.r, sc).copy()
+            row.setflags(write=False)
+            out.append(row)
             off += nb
         return out
+
+    @rows.setter
+    def rows(self, rows) -> None:
+        self.load_rows(rows)
+
+    def _store_row(self, i: int, regs) -> np.ndarray:
+        """Upload one row's (2^r, SC_i) registers; returns the read-only copy."""
+        import torch
+
+        c = self.config
+        if not -c.sr <= i < c.sr:
+            raise IndexError(f"row {i} out of range")
+        i %= c.sr
+        a = np.ascontiguousarray(regs, dtype=register_dtype(c.g))
+        if a.shape != (1 << c.r, c.sc[i]):
+            raise ConfigError(f"row {i} shape {a.shape} != {(1 << c.r, c.sc[i])}")
+        off = sum((1 << c.r) * sc for sc in c.sc[:i]) * c.register_bytes
+        host = torch.from_numpy(a.view(np.uint8).reshape(-1).copy())
+        self._buf[off:off + host.numel()].copy_(host)
+        a = a.copy()
+        a.setflags(write=False)
+        return a
 
     def load_rows(self, rows) -> None:
         """Upload host register arrays (inverse of `.rows`)."""

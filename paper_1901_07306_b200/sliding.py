@@ -115,7 +115,11 @@ class TimestampPool:
 
     @property
     def ts(self) -> np.ndarray:
-        return self.device_buffer().cpu().numpy().view(self.dtype)
+        """Host snapshot of the stamps (read-only: assign `pool.ts = arr`
+        or use touch / touch_batch to write)."""
+        out = self.device_buffer().cpu().numpy().view(self.dtype)
+        out.setflags(write=False)
+        return out
 
     @ts.setter
     def ts(self, values: np.ndarray):
@@ -153,13 +157,34 @@ class TimestampPool:
             self._buf[slot_index] = _as_signed(now & self._mask, self.ts_bytes)
 
     def touch_batch(self, slot_indexes):
+        """ts[slot_indexes] = now (sliding.py:77-79) by `sspd_touch_slots`.
+        numpy indexing semantics: a boolean mask selects, negative indexes
+        count from the end, any index out of range raises IndexError before
+        a slot is stamped."""
         import torch
 
-        idx = torch.as_tensor(np.asarray(slot_indexes, dtype=np.int64)).to(self._buf.device)
+        from ._device import call, stream_ptr
+
+        a = np.asarray(slot_indexes)
+        if a.dtype == np.bool_:
+            if a.shape != (self.n_slots,):
+                raise IndexError(f"boolean index of shape {a.shape} does not match {self.n_slots} slots")
+            a = np.flatnonzero(a)
+        elif a.dtype.kind not in "iu":
+            raise IndexError("slot indexes must be integers or a boolean mask")
+        a = a.reshape(-1)
+        if a.size == 0:
+            return
+        lo, hi = int(a.min()), int(a.max())
+        if lo < -self.n_slots or hi >= self.n_slots:
+            bad = hi if hi >= self.n_slots else lo
+            raise IndexError(f"index {bad} is out of bounds for axis 0 with size {self.n_slots}")
+        idx = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).to(self._buf.device, non_blocking=False)
         self.flush()
         self._version += 1
         self._pristine = False
-        self._buf.index_fill_(0, idx, _as_signed(self._wrapped_now(), self.ts_bytes))
+        call("sspd_touch_slots", self._buf.data_ptr(), self.n_slots, self.ts_bytes, idx.data_ptr(), idx.numel(),
+             self._wrapped_now(), None, stream_ptr())
 
     def advance_slice(self):
         self.flush()  # deferred stamps belong to the slice that ends here

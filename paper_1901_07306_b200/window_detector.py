@@ -134,6 +134,10 @@ class ReportList(Sequence):
         eq = self.__eq__(other)
         return eq if eq is NotImplemented else not eq
 
+    def copy(self) -> list:
+        """A plain list[DetectionReport] (for callers that mutate it)."""
+        return list(self)
+
     def __add__(self, other):
         return list(self) + list(other)
 

@@ -114,6 +114,23 @@ def test_index_round_trip():
                 assert idx[i] == ref
 
 
+def test_index_of_array_vectorised_matches_scalar():
+    """index_of_array (short_sketch.py:196-205) is the scalar map over an
+    array, any integer dtype and shape; out-of-range LP bits are masked."""
+    from paper_1901_07306_b200 import make_config
+
+    for cfg in (make_config(), make_config(r=2, sr=5, a=1), make_config(r=12), make_config(r=16)):
+        rng = np.random.default_rng(7)
+        lp = rng.integers(0, 1 << 40, size=(40, 25), dtype=np.uint64)
+        for i in range(cfg.sr):
+            got = cfg.index_of_array(i, lp)
+            assert got.shape == lp.shape and got.dtype == np.uint64
+            assert got.reshape(-1).tolist() == [cfg.index_of(i, int(x)) for x in lp.reshape(-1).tolist()]
+            assert cfg.index_of_array(i, lp.astype(np.int64)).tolist() == got.tolist()
+        with pytest.raises(Exception):
+            cfg.index_of_array(cfg.sr, lp)
+
+
 def test_ldc_estimate_and_keep_table():
     import math
 

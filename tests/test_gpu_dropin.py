@@ -53,6 +53,39 @@ def test_scalar_update_matches_batch_and_is_idempotent(cuda):  # :249-291
         a.rows[0][int(hips[0]) & 15, cfg.index_of(0, int(hips[0]) >> 4)])
 
 
+def test_host_snapshots_read_only_and_row_assignment_uploads(cuda):
+    """`.rows` / `.data` are host snapshots: in-place writes fail loudly;
+    `sk.rows[i] = regs` (the reference's sliding.py:202 idiom) and
+    `ldca.data = arr` upload."""
+    from paper_1901_07306_b200 import LdcaConfig, LdcaSketch, SeavSketch, SeedFamily, make_config
+
+    cfg = make_config(theta=64)
+    rng = np.random.default_rng(5)
+    hips = rng.integers(0, 2**32, size=2000, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=2000, dtype=np.uint64)
+    a, b = SeavSketch(cfg, SeedFamily()), SeavSketch(cfg, SeedFamily())
+    a.update_batch(hips, oips)
+    with pytest.raises(ValueError):
+        a.rows[0][0, 0] = 1
+    rows_b = b.rows
+    for i, r in enumerate(a.rows):
+        rows_b[i] = r
+    assert b.payload_bytes() == a.payload_bytes()
+    assert (rows_b[1] == a.rows[1]).all()
+    b.clear()
+    b.rows = a.rows
+    assert b.payload_bytes() == a.payload_bytes()
+    with pytest.raises(Exception):
+        rows_b[0] = np.zeros((3, 3))
+
+    la, lb = LdcaSketch(LdcaConfig(), SeedFamily()), LdcaSketch(LdcaConfig(), SeedFamily())
+    la.update_batch(hips, oips)
+    with pytest.raises(ValueError):
+        la.data[0, 0, 0] = 1
+    lb.data = la.data
+    assert lb.payload_bytes() == la.payload_bytes()
+
+
 def test_restore_single_heavy_host_and_sorted_unique(cuda):  # :342-352, :418-426
     from paper_1901_07306_b200 import SeavSketch, SeedFamily, make_config
 
@@ -296,6 +329,33 @@ def test_expiry_boundary_and_all_expire(cuda):  # :27-69
     for _ in range(3):
         pool.advance_slice()
     assert not pool.active().any()
+
+
+def test_touch_batch_numpy_index_semantics(cuda):  # sliding.py:77-79 is `ts[slot_indexes] = now`
+    from paper_1901_07306_b200 import TimestampPool
+
+    rng = np.random.default_rng(3)
+    for ts_window in (3, 300, 40000):  # u8 / u16 / u32 stamps
+        pool = TimestampPool(1000, window_slices=ts_window)
+        ref = pool.ts.copy()
+        for step in range(4):
+            idx = rng.integers(-1000, 1000, size=300)
+            pool.touch_batch(idx)
+            ref[idx] = pool._wrapped_now()
+            mask = rng.random(1000) < 0.1
+            pool.touch_batch(mask)
+            ref[mask] = pool._wrapped_now()
+            pool.touch_batch(np.array([], dtype=np.int64))
+            assert (pool.ts == ref).all(), (ts_window, step)
+            pool.advance_slice()
+            ref = pool.ts.copy()
+        before = pool.ts.copy()
+        for bad in (np.array([5, 1000]), np.array([-1001, 3]), np.array([2**63], dtype=np.uint64)):
+            with pytest.raises(IndexError):
+                pool.touch_batch(bad)
+        with pytest.raises(IndexError):
+            pool.touch_batch(np.ones(7, dtype=bool))
+        assert (pool.ts == before).all()
 
 
 def test_boundary_straddler_found_only_by_sliding(cuda):  # :165-196, acceptance criterion 7
