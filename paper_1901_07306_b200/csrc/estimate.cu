@@ -574,94 +574,186 @@ __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict_
                            out_count, overflow, G, &tab);
 }
 
+// ---------------------------------------------------------- cell summary
+// zeros[c] = k - popcount(cell c) for every LDCA cell (LR x LC of them), one
+// warp per cell.  The filter's z0 is the zero count of the AND of a
+// candidate's LR cells; a full cell (zeros = 0) is the AND identity, so the
+// filter reads only the non-full cells, and none at all when every cell is
+// full (a saturated LDCA: z0 = 0) or only one is not (z0 = its zeros).
+__global__ void __launch_bounds__(256) cell_zeros_kernel(const uint8_t* __restrict__ ldca,
+                                                         const __grid_constant__ sspd_params p,
+                                                         uint32_t* __restrict__ zeros) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t cells = (uint64_t)p.lr * p.lc, cell_bytes = p.k >> 3;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0;
+  for (uint64_t c = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < cells; c += nwarps) {
+    const uint8_t* cell = ldca + c * cell_bytes;
+    uint32_t pop = 0;
+    if (vec) {
+      for (uint64_t v = lane; v < (cell_bytes >> 4); v += 32) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(cell) + v);
+        pop += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+      }
+    } else {
+      for (uint64_t b = lane; b < cell_bytes; b += 32) pop += __popc((uint32_t)cell[b]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
+    if (lane == 0) zeros[c] = p.k - pop;
+  }
+}
+
 // ------------------------------------------------------------------ filter
-// One warp per candidate: AND of the LR row cells, popcount, z0 = k - pop.
-// n_dev (optional): the live count lives in device memory (<= n); entries
-// at or beyond it get keep = 0 so a fixed-capacity compaction skips them.
+// popcount of the AND of candidate ip's LR row cells, by the whole warp
+// (every lane calls it with the same ip; the result is warp-uniform).
+// rows: the rows to AND (bit i = row i; rows >= 32 always taken) -- the
+// others are full cells, the AND identity.  lane i (and i+32) hashes row i
+// once; the cell offsets are broadcast by shuffle.
+__device__ __forceinline__ uint32_t and_popcount(const uint8_t* __restrict__ ldca, const sspd_params& p,
+                                                 uint32_t ip, uint32_t rows, uint32_t lane, uint64_t seed_a,
+                                                 uint64_t seed_b) {
+  const uint64_t cell_bytes = p.k >> 3;
+  const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, seed_a, p.div_lc)) * cell_bytes : 0;
+  const uint64_t off_b =
+      lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, seed_b, p.div_lc)) * cell_bytes : 0;
+  uint32_t pop = 0;
+  if (p.lr == 8 && cell_bytes == 1024 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
+    // the BASELINE geometry (LR = 8, k = 8192): all 8 cell offsets first,
+    // then the 8 rows' 16-byte loads of each half in flight at once (the
+    // generic loop below issues one row's loads per shuffle round trip).
+    // A full row's loads are redirected to the first taken row's cell (AND
+    // is idempotent; the repeat hits L1, not L2).
+    const uint32_t first = __ffs(rows) - 1;
+    uint64_t off[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) off[i] = __shfl_sync(0xFFFFFFFFu, off_a, ((rows >> i) & 1u) ? i : first);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two halves of the 1 KB cells, 8 loads in flight each
+      uint4 w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = __ldg(reinterpret_cast<const uint4*>(ldca + off[i]) + 32 * h + lane);
+      uint4 a = w[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) a.x &= w[i].x, a.y &= w[i].y, a.z &= w[i].z, a.w &= w[i].w;
+      pop += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+    }
+  } else if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
+    // 16-byte loads: lane l ANDs words 4l..4l+3 of each 128-word stripe
+    const uint32_t vecs = (uint32_t)(cell_bytes >> 4);
+    for (uint32_t base = 0; base < vecs; base += 32) {
+      const uint32_t v = base + lane;
+      uint4 acc = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      for (uint32_t i = 0; i < p.lr; ++i) {
+        if (i < 32 && !((rows >> i) & 1u)) continue;  // a full cell (warp-uniform)
+        const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+        if (v < vecs) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(ldca + off) + v);
+          acc.x &= w.x, acc.y &= w.y, acc.z &= w.z, acc.w &= w.w;
+        }
+      }
+      if (v < vecs) pop += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+    }
+  } else if ((p.k & 31u) == 0) {
+    const uint32_t words = p.k >> 5;
+    for (uint32_t base = 0; base < words; base += 32) {
+      const uint32_t wd = base + lane;
+      uint32_t acc = 0xFFFFFFFFu;
+      for (uint32_t i = 0; i < p.lr; ++i) {
+        if (i < 32 && !((rows >> i) & 1u)) continue;
+        const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+        if (wd < words) acc &= __ldg(reinterpret_cast<const uint32_t*>(ldca + off) + wd);
+      }
+      if (wd < words) pop += __popc(acc);
+    }
+  } else {
+    for (uint32_t base = 0; base < cell_bytes; base += 32) {
+      const uint32_t by = base + lane;
+      uint32_t acc = 0xFFu;
+      for (uint32_t i = 0; i < p.lr; ++i) {
+        if (i < 32 && !((rows >> i) & 1u)) continue;
+        const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
+        if (by < cell_bytes) acc &= ldca[off + by];
+      }
+      if (by < cell_bytes) pop += __popc(acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
+  return pop;
+}
+
+// K6: z0 = k - popcount(AND of the LR row cells) per candidate, keep =
+// keep_table[z0]; one warp per candidate.  n_dev (optional): the live count
+// lives in device memory (<= n); entries at or beyond it get keep = 0 so a
+// fixed-capacity compaction skips them.  work / work_rows / work_n
+// (optional, from filter_summary_kernel): the candidates left to AND are
+// work[0 .. *work_n), each over its non-full rows work_rows[t] only.
 __global__ void __launch_bounds__(256) filter_kernel(const uint8_t* __restrict__ ldca,
                                                      const __grid_constant__ sspd_params p,
                                                      const uint32_t* __restrict__ ips, uint64_t n,
                                                      const uint8_t* __restrict__ keep_table, uint32_t* z0_out,
-                                                     uint8_t* keep_out, const unsigned long long* n_dev) {
+                                                     uint8_t* keep_out, const unsigned long long* n_dev,
+                                                     const uint32_t* __restrict__ work,
+                                                     const uint32_t* __restrict__ work_rows,
+                                                     const unsigned long long* work_n) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t cell_bytes = p.k >> 3;
   const uint64_t live = n_dev ? min(n, (uint64_t)*n_dev) : n;
+  const uint64_t items = work ? min(n, (uint64_t)*work_n) : n;
+  const uint32_t all_rows = p.lr >= 32 ? 0xFFFFFFFFu : ((1u << p.lr) - 1u);
   // lane i (and i+32) owns row i: its seed is loaded once (a lane-indexed
   // constant load is serialised across the warp's distinct addresses)
   const uint64_t seed_a = lane < p.lr ? p.seed_lh[lane] : 0, seed_b = lane + 32 < p.lr ? p.seed_lh[lane + 32] : 0;
-  for (uint64_t j = warp; j < n; j += nwarps) {
+  for (uint64_t t = warp; t < items; t += nwarps) {
+    const uint64_t j = work ? work[t] : t;
     if (j >= live) {
       if (lane == 0 && keep_out) keep_out[j] = 0;
       continue;
     }
-    const uint32_t ip = ips[j];
-    // lane i (and i+32) hashes row i once; cells are broadcast by shuffle
-    const uint64_t off_a = lane < p.lr ? ((uint64_t)lane * p.lc + hash_range(ip, seed_a, p.div_lc)) * cell_bytes : 0;
-    const uint64_t off_b =
-        lane + 32 < p.lr ? ((uint64_t)(lane + 32) * p.lc + hash_range(ip, seed_b, p.div_lc)) * cell_bytes : 0;
-    uint32_t pop = 0;
-    if (p.lr == 8 && cell_bytes == 1024 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
-      // the BASELINE geometry (LR = 8, k = 8192): all 8 cell offsets first,
-      // then the 8 rows' 16-byte loads of each half in flight at once (the
-      // generic loop below issues one row's loads per shuffle round trip)
-      uint64_t off[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) off[i] = __shfl_sync(0xFFFFFFFFu, off_a, i);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // two halves of the 1 KB cells, 8 loads in flight each
-        uint4 w[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = __ldg(reinterpret_cast<const uint4*>(ldca + off[i]) + 32 * h + lane);
-        uint4 a = w[0];
-#pragma unroll
-        for (int i = 1; i < 8; ++i) a.x &= w[i].x, a.y &= w[i].y, a.z &= w[i].z, a.w &= w[i].w;
-        pop += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
-      }
-    } else if ((cell_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(ldca) & 15u) == 0) {
-      // 16-byte loads: lane l ANDs words 4l..4l+3 of each 128-word stripe
-      const uint32_t vecs = (uint32_t)(cell_bytes >> 4);
-      for (uint32_t base = 0; base < vecs; base += 32) {
-        const uint32_t v = base + lane;
-        uint4 acc = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        for (uint32_t i = 0; i < p.lr; ++i) {
-          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
-          if (v < vecs) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(ldca + off) + v);
-            acc.x &= w.x, acc.y &= w.y, acc.z &= w.z, acc.w &= w.w;
-          }
-        }
-        if (v < vecs) pop += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
-      }
-    } else if ((p.k & 31u) == 0) {
-      const uint32_t words = p.k >> 5;
-      for (uint32_t base = 0; base < words; base += 32) {
-        const uint32_t wd = base + lane;
-        uint32_t acc = 0xFFFFFFFFu;
-        for (uint32_t i = 0; i < p.lr; ++i) {
-          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
-          if (wd < words) acc &= __ldg(reinterpret_cast<const uint32_t*>(ldca + off) + wd);
-        }
-        if (wd < words) pop += __popc(acc);
-      }
-    } else {
-      for (uint32_t base = 0; base < cell_bytes; base += 32) {
-        const uint32_t by = base + lane;
-        uint32_t acc = 0xFFu;
-        for (uint32_t i = 0; i < p.lr; ++i) {
-          const uint64_t off = __shfl_sync(0xFFFFFFFFu, i < 32 ? off_a : off_b, i & 31);
-          if (by < cell_bytes) acc &= ldca[off + by];
-        }
-        if (by < cell_bytes) pop += __popc(acc);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) pop += __shfl_xor_sync(0xFFFFFFFFu, pop, o);
+    const uint32_t pop = and_popcount(ldca, p, ips[j], work ? work_rows[t] : all_rows, lane, seed_a, seed_b);
     if (lane == 0) {
       const uint32_t z0 = p.k - pop;
       z0_out[j] = z0;
       if (keep_out) keep_out[j] = keep_table ? keep_table[z0] : 1;
+    }
+  }
+}
+
+// K6 first pass over the cell summary (LR <= 32), one thread per candidate:
+// hash the LR cells, read their zero counts; with at most one non-full cell
+// z0 is known without touching the LDCA (every candidate of a saturated
+// LDCA), otherwise the candidate and its non-full rows go to the work list
+// that filter_kernel ANDs (full cells are the AND identity: exact).
+// Candidates past the live count get keep = 0.
+__global__ void __launch_bounds__(256) filter_summary_kernel(const __grid_constant__ sspd_params p,
+                                                             const uint32_t* __restrict__ ips, uint64_t n,
+                                                             const unsigned long long* n_dev,
+                                                             const uint32_t* __restrict__ cell_zeros,
+                                                             const uint8_t* __restrict__ keep_table,
+                                                             uint32_t* z0_out, uint8_t* keep_out, uint32_t* work,
+                                                             uint32_t* work_rows, unsigned long long* work_n) {
+  const uint64_t live = n_dev ? min(n, (uint64_t)*n_dev) : n;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    if (j >= live) {
+      if (keep_out) keep_out[j] = 0;
+      continue;
+    }
+    const uint32_t ip = ips[j];
+    uint32_t rows = 0, zlast = 0;
+    for (uint32_t i = 0; i < p.lr; ++i) {  // row index uniform across the warp: broadcast constant loads
+      const uint32_t z = __ldg(cell_zeros + (uint64_t)i * p.lc + hash_range(ip, p.seed_lh[i], p.div_lc));
+      if (z) rows |= 1u << i, zlast = z;
+    }
+    if (__popc(rows) <= 1) {
+      z0_out[j] = zlast;
+      if (keep_out) keep_out[j] = keep_table ? keep_table[zlast] : 1;
+    } else {
+      const uint32_t t = (uint32_t)atomicAdd(work_n, 1ull);
+      work[t] = (uint32_t)j;
+      work_rows[t] = rows;
     }
   }
 }
@@ -1132,7 +1224,8 @@ extern "C" int sspd_filter(const uint8_t* ldca, const sspd_params* p, const uint
   if (!ldca || !ips || !z0_out) return SSPD_ERR_DATA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = grid_for(filter_kernel, 256, n * 32);
-  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, ips, n, keep_table, z0_out, keep_out, nullptr);
+  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, ips, n, keep_table, z0_out, keep_out, nullptr, nullptr, nullptr,
+                                      nullptr);
   return check_launch();
 }
 
@@ -1235,7 +1328,10 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   const size_t seg_bytes = 4 * segs * (segs > kSegDirect ? 2 : 1);  // sspd_compact_reports scratch
   const size_t o_hist = o_seg + ((seg_bytes + 255) / 256) * 256;
   const size_t o_start = o_hist + 8ull * 16384;
-  const size_t need = o_start + 4ull * (16384 + 1) + 256;
+  const size_t o_cz = o_start + ((4ull * (16384 + 1) + 255) / 256) * 256;  // cell summary (LR <= 32)
+  const uint64_t cells = p->lr <= 32 ? (uint64_t)p->lr * p->lc : 0;
+  const size_t o_wn = o_cz + ((4 * cells + 255) / 256) * 256;  // work-list count (u64)
+  const size_t need = o_wn + 256;
   if (!scratch) {
     *scratch_bytes = need;
     return SSPD_OK;
@@ -1274,7 +1370,23 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
     sorted = ip;
   }
   const int grid = grid_for(filter_kernel, 256, C * 32);
-  filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts);
+  if (cells) {
+    // the cell summary, then the thread-per-candidate pass; the warps AND
+    // only the candidates it could not settle (work list in the free
+    // [2 vec, 4 vec) of the scratch: ip_alt and the spare vector)
+    uint32_t* cz = reinterpret_cast<uint32_t*>(s8 + o_cz);
+    uint32_t* work_rows = reinterpret_cast<uint32_t*>(s8 + o_ipa);
+    uint32_t* work = reinterpret_cast<uint32_t*>(s8 + 3 * vec);
+    unsigned long long* work_n = reinterpret_cast<unsigned long long*>(s8 + o_wn);
+    if (cudaMemsetAsync(work_n, 0, sizeof(unsigned long long), st) != cudaSuccess) return SSPD_ERR_CUDA;
+    cell_zeros_kernel<<<grid_for(cell_zeros_kernel, 256, cells * 32), 256, 0, st>>>(ldca, *p, cz);
+    filter_summary_kernel<<<grid_for(filter_summary_kernel, 256, C), 256, 0, st>>>(
+        *p, sorted, C, counts, cz, keep_table, z0, keep, work, work_rows, work_n);
+    filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts, work, work_rows, work_n);
+  } else {
+    filter_kernel<<<grid, 256, 0, st>>>(ldca, *p, sorted, C, keep_table, z0, keep, counts, nullptr, nullptr,
+                                        nullptr);
+  }
   size_t cb = seg_bytes;
   rc = sspd_compact_reports(sorted, z0, keep, C, out_ip, out_z0, counts + 1, s8 + o_seg, &cb, stream);
   if (rc) return rc;

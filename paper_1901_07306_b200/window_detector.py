@@ -196,7 +196,7 @@ def device_keep_table(k: int, cutoff: float):
     return t
 
 
-_FINALIZE_SCRATCH: dict = {}  # capacity -> sspd_finalize work-space bytes
+_FINALIZE_SCRATCH: dict = {}  # (capacity, LR, LC) -> sspd_finalize work-space bytes
 _SM_COUNT: dict = {}  # device -> SMs
 
 
@@ -235,7 +235,7 @@ class DeviceFinalize:
         if table is None:
             table = device_keep_table(self.k, self.cutoff)
         base = out.data_ptr()
-        need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
+        need = _FINALIZE_SCRATCH.get(self._scratch_key(cap)) or self._scratch_query(cap)
         scratch = seav._scratch(need)
         call("sspd_finalize", seav._buf.data_ptr(), self.ldca.data_ptr(), self.p, seav.restore_cap,
              table.data_ptr(), cap, base, base + 4 * cap, base + 8 * cap, base + 8 * cap + 16,
@@ -261,7 +261,7 @@ class DeviceFinalize:
             # pointers).  The keep table is a device INPUT of the graph: the
             # view set owns one (k+1)-byte buffer, refreshed on the stream
             # when beta*theta changes, so the cutoff is not part of the key.
-            need = _FINALIZE_SCRATCH.get(cap) or self._scratch_query(cap)
+            need = _FINALIZE_SCRATCH.get(self._scratch_key(cap)) or self._scratch_query(cap)
             scratch = seav._scratch(need)  # allocated outside the capture
             key = (cap, seav._radix_sort, self.ldca.data_ptr(), seav.restore_cap, scratch.data_ptr(), self.k)
             keep = self.graphs.get("keep")
@@ -293,12 +293,16 @@ class DeviceFinalize:
             self.event = torch.cuda.Event()
             self.event.record(self.stream)
 
+    def _scratch_key(self, cap: int):
+        p = self.p.contents if hasattr(self.p, "contents") else self.p
+        return (cap, int(p.lr), int(p.lc))
+
     def _scratch_query(self, cap: int):
         from ._device import call
 
         nb = ctypes.c_size_t(0)
         call("sspd_finalize", None, None, self.p, 0, None, cap, None, None, None, None, None, ctypes.byref(nb), 0, 0)
-        _FINALIZE_SCRATCH[cap] = nb.value
+        _FINALIZE_SCRATCH[self._scratch_key(cap)] = nb.value
         return nb.value
 
     def detach(self):

@@ -466,6 +466,53 @@ def test_finalize_bucket_sort_vs_oracle(cuda, oracle, skewed):
     assert len(set(heavy.tolist()) & set(got)) > nheavy // 2
 
 
+@pytest.mark.parametrize("lr,lc,k", [(8, 1024, 8192), (4, 256, 4096), (5, 64, 4128), (3, 128, 8200)])
+def test_finalize_partly_saturated_ldca_vs_oracle(cuda, oracle, lr, lc, k):
+    """The filter's cell summary (cell_zeros_kernel) skips full LDCA cells:
+    an LDCA whose cells are a mix of full, nearly full and half-set ones
+    drives every branch -- all cells full (z0 = 0 without a read), one cell
+    not full (z0 from the summary), several (AND over the non-full cells
+    only) -- across the LR = 8 / 16-byte / word / byte filter paths.  The
+    report list equals the oracle's on the same bytes."""
+    import math
+
+    from paper_1901_07306_b200 import DetectorParams
+
+    dp = DetectorParams(theta=256, r=8, k=k, lr=lr, lc=lc, design_n=4e5)
+    _, _, p = params_block(dp)
+    rng = np.random.default_rng(lr * 7 + k)
+    n = 400_000
+    hips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    oips = rng.integers(0, 2**32, size=n, dtype=np.uint64)
+    heavy = rng.integers(0, 2**32, size=300, dtype=np.uint64)
+    hips[: 300 * 600] = np.repeat(heavy, 600)
+    st = make_state(dp)
+    st.process_batch(hips, oips)
+    cb = k // 8
+    cells = lr * lc
+    kind = rng.choice(3, size=cells, p=[0.75, 0.15, 0.10])
+    ldca = np.empty((cells, cb), dtype=np.uint8)
+    ldca[kind == 0] = 0xFF
+    dense = np.packbits(rng.random(((kind == 1).sum(), cb * 8)) < 0.995, axis=1)
+    ldca[kind == 1] = dense
+    ldca[kind == 2] = rng.integers(0, 256, size=((kind == 2).sum(), cb), dtype=np.uint8)
+    st.ldca.load_payload(ldca.tobytes())
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        reports = st.finalize_window()
+    seav = np.frombuffer(st.seav.payload_bytes(), dtype=np.uint8)
+    ips, _, _, _ = oracle.restore(p, seav, dp.restore_cap)
+    z0 = oracle.filter_z0(p, ldca.reshape(-1), ips)
+    want = [(int(ip), int(z)) for ip, z in zip(ips.tolist(), z0.tolist())
+            if z == 0 or -k * math.log(z / k) >= dp.beta * dp.theta]
+    got = [(r.ip, r.estimated_cardinality) for r in reports]
+    est = {z: (k * math.log(k) if z == 0 else -k * math.log(z / k)) for _, z in want}
+    assert [ip for ip, _ in got] == [ip for ip, _ in want]
+    assert [e for _, e in got] == [est[z] for _, z in want]
+    zs = [z for _, z in want]
+    assert zs.count(0) > 10 and sum(1 for z in zs if z) > 10  # both the shortcut and the read paths ran
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 1023, 4097, 100_003, 1_048_579])
 def test_candidate_radix_sort_stable(cuda, n):
     """sspd_sort_candidates (csrc/radix.cu, no CUB): keys ascending, values
