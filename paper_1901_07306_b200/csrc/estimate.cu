@@ -93,6 +93,21 @@ struct WarpTab {
   uint32_t off_bstart[SSPD_MAX_SR], off_cols[SSPD_MAX_SR], row_lane0[SSPD_MAX_SR];
 };
 
+// Enumeration path (warp kernel only): ctab[i][x] = the columns of row i
+// (<= 64) whose bits on keymask[i] equal x's (x = the walk's LP bits at row
+// i, masked to keymask[i] < 64) -- col_match() as one shared-memory load.
+struct EnumTab {
+  uint64_t ctab[SSPD_MAX_SR][64];
+};
+
+__device__ __forceinline__ uint64_t col_match(uint32_t km, uint32_t v, uint32_t sc);
+
+__device__ void fill_enum_tab(const RestorePlan& P, EnumTab* E) {
+  if (P.lane_enum)
+    for (uint32_t x = threadIdx.x; x < P.sr * 64u; x += blockDim.x)
+      E->ctab[x >> 6][x & 63] = col_match(P.keymask[x >> 6], x & 63, P.sc[x >> 6]);
+}
+
 __device__ void fill_warp_tab(const RestorePlan& P, WarpTab* T) {
   const uint32_t t = threadIdx.x;
   if (t < 32) {
@@ -172,10 +187,80 @@ __device__ __forceinline__ uint64_t col_match(uint32_t km, uint32_t v, uint32_t 
   return m;
 }
 
-// k-th (0-based) set bit of a 64-bit mask
+// k-th (0-based) set bit of a 64-bit mask (k < popcount(m))
 __device__ __forceinline__ uint32_t nth_bit64(uint64_t m, uint32_t k) {
   const uint32_t lo = (uint32_t)m, nlo = __popc(lo);
   return k < nlo ? __fns(lo, 0, (int)k + 1) : 32u + __fns((uint32_t)(m >> 32), 0, (int)(k - nlo) + 1);
+}
+
+// the same by popcount halving: ~20 ALU ops, where __fns is a loop
+__device__ __forceinline__ uint32_t select64(uint64_t m, uint32_t k) {
+  uint32_t pos = 0, c = __popc((uint32_t)m);
+  if (k >= c) k -= c, m >>= 32, pos = 32;
+  uint32_t x = (uint32_t)m;
+  c = __popc(x & 0xFFFFu);
+  if (k >= c) k -= c, x >>= 16, pos += 16;
+  c = __popc(x & 0xFFu);
+  if (k >= c) k -= c, x >>= 8, pos += 8;
+  c = __popc(x & 0xFu);
+  if (k >= c) k -= c, x >>= 4, pos += 4;
+  c = __popc(x & 0x3u);
+  if (k >= c) k -= c, x >>= 2, pos += 2;
+  return pos + (k >= (x & 1u) ? 1u : 0u);
+}
+
+// Candidates of the enumeration path are staged per warp in shared memory
+// and leave with ONE global counter atomic per flush (a warp restores many
+// SEAs): per-candidate-group atomics on the single shared counter were
+// round trips to one L2 slice that every emitting lane waited on.
+constexpr uint32_t kEmitBuf = 128;
+struct EmitBuf {
+  uint32_t n;
+  uint32_t ip[kEmitBuf], aux[kEmitBuf];
+};
+
+__device__ __forceinline__ void emit_buffered(const RestorePlan& P, EmitBuf* eb, uint64_t lp, uint32_t rp,
+                                              uint32_t wgt, uint32_t* out_ip, uint32_t* out_aux,
+                                              uint64_t out_capacity, unsigned long long* out_count) {
+  const uint32_t ip = (uint32_t)((lp << P.r) | rp), aux = (rp << 8) | wgt;
+  const uint32_t pos = atomicAdd(&eb->n, 1u);
+  if (pos < kEmitBuf) {
+    eb->ip[pos] = ip;
+    eb->aux[pos] = aux;
+    return;
+  }
+  const unsigned long long slot = atomicAdd(out_count, 1ull);  // buffer full (rare): straight out
+  if (slot < out_capacity) {
+    out_ip[slot] = ip;
+    out_aux[slot] = aux;
+    if (P.hist) atomicAdd(P.hist + (ip >> P.hshift), 1u);
+  }
+}
+
+// whole warp, converged: write the staged candidates out once there are at
+// least `thresh` of them
+__device__ __forceinline__ void flush_emit(const RestorePlan& P, EmitBuf* eb, uint32_t thresh, uint32_t* out_ip,
+                                           uint32_t* out_aux, uint64_t out_capacity,
+                                           unsigned long long* out_count) {
+  __syncwarp();
+  const uint32_t n = eb->n;
+  if (n < thresh || n == 0) return;
+  const uint32_t lane = threadIdx.x & 31, m = min(n, kEmitBuf);
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(out_count, (unsigned long long)m);
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  for (uint32_t i = lane; i < m; i += 32) {
+    const unsigned long long slot = base + i;
+    if (slot < out_capacity) {
+      const uint32_t ip = eb->ip[i];
+      out_ip[slot] = ip;
+      out_aux[slot] = eb->aux[i];
+      if (P.hist) atomicAdd(P.hist + (ip >> P.hshift), 1u);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) eb->n = 0;
+  __syncwarp();
 }
 
 template <bool kEmit>
@@ -310,7 +395,8 @@ template <bool kWarp>
 __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const RestorePlan& P, uint8_t* sm, uint32_t rp,
                                   uint32_t slot, uint64_t cap, uint32_t* out_ip, uint32_t* out_aux,
                                   uint64_t out_capacity, unsigned long long* out_count, uint8_t* overflow,
-                                  const Group<kWarp> G, const WarpTab* T) {
+                                  const Group<kWarp> G, const WarpTab* T, uint64_t pre = 0,
+                                  EmitBuf* eb = nullptr, const EnumTab* E = nullptr) {
   Misc* misc = reinterpret_cast<Misc*>(sm + P.off_misc);
   const uint32_t sr = P.sr;
 
@@ -323,10 +409,9 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
     // the whole SEA in ONE independent 8-byte load per lane (instead of a
     // dependent round trip per row, which is what a restore co-running with
     // the L2-atomic-bound sliding scan waits on); hot = a byte of weight >= 3
-    const uint32_t lsc = T->lane_sc[G.tid];
-    const bool act = lsc != 0;
-    uint64_t v = 0;
-    if (act) v = __ldg(reinterpret_cast<const uint64_t*>(seav + T->lane_src[G.tid] + (uint64_t)rp * lsc));
+    // (loaded by the caller one SEA ahead: `pre`)
+    const bool act = T->lane_sc[G.tid] != 0;
+    const uint64_t v = pre;
     uint64_t c = v - ((v >> 1) & 0x5555555555555555ull);
     c = (c & 0x3333333333333333ull) + ((c >> 2) & 0x3333333333333333ull);
     c = (c + (c >> 4)) & 0x0F0F0F0F0F0F0F0Full;                      // per-byte popcounts (<= 8)
@@ -366,15 +451,16 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
         // columns: a SEA with few hot row-0 columns but many pairs (a busy
         // late-trace SEA) keeps all 32 lanes walking.  Row-0 hot column j
         // (j = lane, lane + 32) and the size of its consistent row-1 set:
+        (void)h0;
         auto row1_of = [&](uint32_t c0) {
-          return misc->rmask[1] & col_match(T->keymask[1],
-                                            index_of(scatter_col(c0, T->isb[0], T->ibn[0], P.w), T->isb[1],
-                                                     T->ibn[1], P.w),
-                                            T->sc[1]);
+          return misc->rmask[1] &
+                 E->ctab[1][index_of(scatter_col(c0, T->isb[0], T->ibn[0], P.w), T->isb[1], T->ibn[1], P.w) &
+                            T->keymask[1]];
         };
-        const uint32_t cnt_a = lane < h0 ? (uint32_t)__popcll(row1_of(nth_bit64(hot0, lane))) : 0u;
-        const uint32_t cnt_b = lane + 32 < h0 ? (uint32_t)__popcll(row1_of(nth_bit64(hot0, lane + 32))) : 0u;
-        uint32_t inc_a = cnt_a, inc_b = cnt_b;  // inclusive prefixes over j = 0..63
+        // indexed by row-0 COLUMN (lane, lane + 32), a cold column counting 0
+        const uint32_t cnt_a = (hot0 >> lane) & 1u ? (uint32_t)__popcll(row1_of(lane)) : 0u;
+        const uint32_t cnt_b = (hot0 >> (lane + 32)) & 1u ? (uint32_t)__popcll(row1_of(lane + 32)) : 0u;
+        uint32_t inc_a = cnt_a, inc_b = cnt_b;  // inclusive prefixes over columns 0..63
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t ya = __shfl_up_sync(0xFFFFFFFFu, inc_a, o), yb = __shfl_up_sync(0xFFFFFFFFu, inc_b, o);
@@ -389,7 +475,7 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
         uint64_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR], rem_st[SSPD_MAX_SR];
         for (uint32_t base = 0; base < npairs; base += 32) {
           const uint32_t t = base + lane;
-          // row-0 entry of pair t: the first j with incl(j) > t
+          // row-0 column of pair t: the first j with incl(j) > t
           uint32_t lo = 0, hi = 63;
 #pragma unroll
           for (int it = 0; it < 6; ++it) {
@@ -399,18 +485,18 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
           const uint32_t j = lo;
           const uint32_t excl = incl_at(j == 0 ? 0 : j - 1);
           if (t >= npairs) continue;
-          const uint32_t c0 = nth_bit64(hot0, j);
+          const uint32_t c0 = j;
           const uint64_t r1 = row1_of(c0);
-          const uint32_t c1 = nth_bit64(r1, t - (j == 0 ? 0u : excl));
+          const uint32_t c1 = select64(r1, t - (j == 0 ? 0u : excl));
           lp_st[1] = scatter_col(c0, T->isb[0], T->ibn[0], P.w) | scatter_col(c1, T->isb[1], T->ibn[1], P.w);
           and_st[1] = full & sm[T->off_regs[0] + c0] & sm[T->off_regs[1] + c1];
           if (sr == 2) {
             const uint32_t wgt = (uint32_t)__popcll(and_st[1]);
-            if (wgt >= 3) emit_candidate(P, lp_st[1], rp, wgt, out_ip, out_aux, out_capacity, out_count);
+            if (wgt >= 3) emit_buffered(P, eb, lp_st[1], rp, wgt, out_ip, out_aux, out_capacity, out_count);
             continue;
           }
           uint32_t lvl = 2;
-          rem_st[2] = misc->rmask[2] & col_match(T->keymask[2], index_of(lp_st[1], T->isb[2], T->ibn[2], P.w), T->sc[2]);
+          rem_st[2] = misc->rmask[2] & E->ctab[2][index_of(lp_st[1], T->isb[2], T->ibn[2], P.w) & T->keymask[2]];
           while (lvl >= 2) {
             const uint64_t rem = rem_st[lvl];
             if (rem == 0) {
@@ -423,14 +509,13 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
             const uint64_t nand = and_st[lvl - 1] & sm[T->off_regs[lvl] + c];
             if (lvl + 1 == sr) {
               const uint32_t wgt = (uint32_t)__popcll(nand);
-              if (wgt >= 3) emit_candidate(P, nlp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
+              if (wgt >= 3) emit_buffered(P, eb, nlp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
               continue;
             }
             lp_st[lvl] = nlp;
             and_st[lvl] = nand;
             ++lvl;
-            rem_st[lvl] = misc->rmask[lvl] &
-                          col_match(T->keymask[lvl], index_of(nlp, T->isb[lvl], T->ibn[lvl], P.w), T->sc[lvl]);
+            rem_st[lvl] = misc->rmask[lvl] & E->ctab[lvl][index_of(nlp, T->isb[lvl], T->ibn[lvl], P.w) & T->keymask[lvl]];
           }
         }
         return;
@@ -542,7 +627,9 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
   restore_walk<true>(P, sm, rp, cap, out_ip, out_aux, out_capacity, out_count, G.tid, G.size, T);
 }
 
-// one SEA per warp, 4 warps per CTA, each warp with its own smem slice
+// one SEA at a time per warp, 4 warps per CTA, each warp with its own smem
+// slice; persistent (the grid is what fits on the GPU at once, each warp
+// strides over the SEAs), the next SEA's registers loaded one SEA ahead
 __global__ void __launch_bounds__(128) restore_warp_kernel(const uint8_t* __restrict__ seav,
                                                            const __grid_constant__ RestorePlan P, uint32_t rp_begin,
                                                            uint32_t rp_count, uint64_t cap, uint32_t* out_ip,
@@ -550,14 +637,32 @@ __global__ void __launch_bounds__(128) restore_warp_kernel(const uint8_t* __rest
                                                            unsigned long long* out_count, uint8_t* overflow) {
   extern __shared__ __align__(16) uint8_t smw[];
   __shared__ WarpTab tab;
+  __shared__ EmitBuf ebuf[4];
+  __shared__ EnumTab etab;
   fill_warp_tab(P, &tab);
+  fill_enum_tab(P, &etab);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  if (lane == 0) ebuf[warp].n = 0;
   __syncthreads();
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (slot >= rp_count) return;
-  const Group<true> G{threadIdx.x & 31u, 32u, 0u, 1u};
-  restore_sea_group<true>(seav, P, smw + (size_t)warp * P.smem_bytes, rp_begin + slot, slot, cap, out_ip, out_aux,
-                          out_capacity, out_count, overflow, G, &tab);
+  const Group<true> G{lane, 32u, 0u, 1u};
+  const uint32_t stride = gridDim.x * (blockDim.x >> 5);
+  const uint32_t lsc = tab.lane_sc[lane];
+  const uint64_t lsrc = tab.lane_src[lane];
+  auto load = [&](uint32_t slot) -> uint64_t {
+    return (P.lane_fast && lsc && slot < rp_count)
+               ? __ldg(reinterpret_cast<const uint64_t*>(seav + lsrc + (uint64_t)(rp_begin + slot) * lsc))
+               : 0ull;
+  };
+  uint32_t slot = blockIdx.x * (blockDim.x >> 5) + warp;
+  uint64_t next = load(slot);
+  for (; slot < rp_count; slot += stride) {
+    const uint64_t v = next;
+    next = load(slot + stride);
+    restore_sea_group<true>(seav, P, smw + (size_t)warp * P.smem_bytes, rp_begin + slot, slot, cap, out_ip, out_aux,
+                            out_capacity, out_count, overflow, G, &tab, v, &ebuf[warp], &etab);
+    flush_emit(P, &ebuf[warp], kEmitBuf / 2, out_ip, out_aux, out_capacity, out_count);
+  }
+  flush_emit(P, &ebuf[warp], 1, out_ip, out_aux, out_capacity, out_count);
 }
 
 __global__ void __launch_bounds__(128) restore_kernel(const uint8_t* __restrict__ seav,
@@ -1183,7 +1288,17 @@ static int restore_launch(const uint8_t* seav, const sspd_params* p, uint32_t rp
   uint32_t warp_regs = 256;
   if (const char* e = getenv("SSPD_RESTORE_WARP_REGS")) warp_regs = (uint32_t)atoi(e);
   if (regs <= warp_regs && 4 * P.smem_bytes <= 48 * 1024) {  // small arrays: one warp per SEA
-    const uint32_t blocks = (rp_count + 3) / 4;
+    static int per_sm = 0, sms = 0;
+    static uint32_t per_sm_smem = 0;
+    if (per_sm == 0 || per_sm_smem != P.smem_bytes) {
+      // dynamic + the static tables (WarpTab, EmitBuf) may pass the 48 KB default
+      cudaFuncSetAttribute(restore_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * P.smem_bytes));
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, restore_warp_kernel, 128, 4 * P.smem_bytes);
+      if (per_sm < 1) per_sm = 1;
+      per_sm_smem = P.smem_bytes;
+    }
+    const uint32_t blocks = std::min<uint32_t>((rp_count + 3) / 4, (uint32_t)(sms * per_sm));
     restore_warp_kernel<<<blocks, 128, 4 * P.smem_bytes, st>>>(seav, P, rp_begin, rp_count, cap, out_ip, out_aux,
                                                                out_capacity, out_count, overflow);
     return check_launch();
