@@ -60,6 +60,7 @@ struct RestorePlan {
   uint32_t lane_enum, enum_max;
   uint32_t row_lane0[SSPD_MAX_SR];  // first lane of row i
   uint32_t row_bits[SSPD_MAX_SR];   // LP positions row i fixes (row_mask), w <= 32
+  uint32_t rows8;  // enumeration with every row 64 registers = 8 aligned lanes (SR <= 4)
 };
 
 __device__ __forceinline__ uint32_t pext32(uint32_t x, uint32_t m) {
@@ -98,14 +99,30 @@ struct WarpTab {
 // i, masked to keymask[i] < 64) -- col_match() as one shared-memory load.
 struct EnumTab {
   uint64_t ctab[SSPD_MAX_SR][64];
+  uint32_t scol[SSPD_MAX_SR][64];  // scatter_col(c, row i): column c's LP bits (w <= 32)
+  uint32_t rd[SSPD_MAX_SR];        // row descriptor: isb | ibn << 8 | keymask << 16
+  uint32_t wmask;                  // (1 << w) - 1
 };
 
 __device__ __forceinline__ uint64_t col_match(uint32_t km, uint32_t v, uint32_t sc);
 
 __device__ void fill_enum_tab(const RestorePlan& P, EnumTab* E) {
-  if (P.lane_enum)
-    for (uint32_t x = threadIdx.x; x < P.sr * 64u; x += blockDim.x)
-      E->ctab[x >> 6][x & 63] = col_match(P.keymask[x >> 6], x & 63, P.sc[x >> 6]);
+  if (!P.lane_enum) return;
+  for (uint32_t x = threadIdx.x; x < P.sr * 64u; x += blockDim.x) {
+    const uint32_t i = x >> 6, c = x & 63;
+    E->ctab[i][c] = col_match(P.keymask[i], c, P.sc[i]);
+    E->scol[i][c] = c < P.sc[i] ? (uint32_t)scatter_col(c, P.isb[i], P.ibn[i], P.w) : 0u;
+  }
+  if (threadIdx.x < P.sr) E->rd[threadIdx.x] = P.isb[threadIdx.x] | P.ibn[threadIdx.x] << 8 | P.keymask[threadIdx.x] << 16;
+  if (threadIdx.x == 0) E->wmask = P.w >= 32 ? 0xFFFFFFFFu : ((1u << P.w) - 1u);
+}
+
+// index_of on a w <= 32 bit LP, masked to the row's key bits: the ctab row
+// index of the columns consistent with lp at row `rd`
+__device__ __forceinline__ uint32_t key32(uint32_t lp, uint32_t rd, uint32_t w, uint32_t wmask) {
+  const uint32_t isb = rd & 255u;
+  const uint32_t rot = isb == 0 ? lp : (((lp >> isb) | (lp << (w - isb))) & wmask);
+  return rot & (rd >> 16);  // keymask bits lie inside the column's ibn bits
 }
 
 __device__ void fill_warp_tab(const RestorePlan& P, WarpTab* T) {
@@ -425,17 +442,32 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
       // per-row hot-column masks: lane l's 8 hot bits are bits lane_off..+7
       // of its row's mask (bytes in lane order = little-endian mask bytes)
       const uint64_t hb8 = ((c + 0x7D7D7D7D7D7D7D7Dull) >> 7) & 0x0101010101010101ull;
-      misc->hmask[G.tid] = act ? (uint8_t)((hb8 * 0x0102040810204080ull) >> 56) : (uint8_t)0;
-      __syncwarp();
-      if (G.tid < sr) {
-        uint64_t m = 0;
-        for (uint32_t j = 0; j < (T->sc[G.tid] >> 3); ++j)
-          m |= (uint64_t)misc->hmask[T->row_lane0[G.tid] + j] << (8 * j);
-        misc->rmask[G.tid] = m;
-      }
-      __syncwarp();
+      const uint32_t hbyte = act ? (uint32_t)((hb8 * 0x0102040810204080ull) >> 56) : 0u;
       uint64_t tuples = 1;
-      for (uint32_t i = 0; i < sr && tuples <= cap; ++i) tuples *= (uint64_t)__popcll(misc->rmask[i]);
+      if (P.rows8) {
+        // row i = lanes 8i .. 8i+7: OR the bytes within each 8-lane group
+        uint64_t x = (uint64_t)hbyte << (8 * (G.tid & 7));
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 1);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+        x |= __shfl_xor_sync(0xFFFFFFFFu, x, 4);
+        if ((G.tid & 7) == 0 && (G.tid >> 3) < sr) misc->rmask[G.tid >> 3] = x;
+        const uint32_t pc = (uint32_t)__popcll(x);
+        uint32_t t32 = 1;  // <= 64^4
+        for (uint32_t i = 0; i < sr; ++i) t32 *= __shfl_sync(0xFFFFFFFFu, pc, 8 * i);
+        tuples = t32;
+        __syncwarp();
+      } else {
+        misc->hmask[G.tid] = (uint8_t)hbyte;
+        __syncwarp();
+        if (G.tid < sr) {
+          uint64_t m = 0;
+          for (uint32_t j = 0; j < (T->sc[G.tid] >> 3); ++j)
+            m |= (uint64_t)misc->hmask[T->row_lane0[G.tid] + j] << (8 * j);
+          misc->rmask[G.tid] = m;
+        }
+        __syncwarp();
+        for (uint32_t i = 0; i < sr && tuples <= cap; ++i) tuples *= (uint64_t)__popcll(misc->rmask[i]);
+      }
       if (tuples <= cap && tuples <= P.enum_max) {
         // every complete tuple is one LP, so the survivors (<= tuples) cannot
         // exceed the cap: no counting pass.  Depth-first walk straight from
@@ -443,23 +475,20 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
         // the consistent hot columns are hot_i & (columns whose bits on the
         // already-fixed LP positions equal the walk's) -- the prune of
         // short_sketch.py:379-388 as one 64-bit mask, no bucket tables
-        const uint64_t full = ((uint64_t)P.full_bits_hi << 32) | P.full_bits_lo;
-        const uint64_t hot0 = misc->rmask[0];
-        const uint32_t h0 = (uint32_t)__popcll(hot0);
-        const uint32_t lane = G.tid;
+        const uint32_t hot0_lo = (uint32_t)misc->rmask[0], hot0_hi = (uint32_t)(misc->rmask[0] >> 32);
+        const uint32_t lane = G.tid, w = P.w, wmask = E->wmask;
+        const uint8_t* reg0 = sm + T->off_regs[0];
+        const uint8_t* reg1 = sm + T->off_regs[1];
+        const uint32_t rd1 = E->rd[1];
+        const uint64_t hot1 = misc->rmask[1];
         // the walk is spread over consistent (row-0, row-1) PAIRS, not row-0
         // columns: a SEA with few hot row-0 columns but many pairs (a busy
-        // late-trace SEA) keeps all 32 lanes walking.  Row-0 hot column j
-        // (j = lane, lane + 32) and the size of its consistent row-1 set:
-        (void)h0;
-        auto row1_of = [&](uint32_t c0) {
-          return misc->rmask[1] &
-                 E->ctab[1][index_of(scatter_col(c0, T->isb[0], T->ibn[0], P.w), T->isb[1], T->ibn[1], P.w) &
-                            T->keymask[1]];
-        };
-        // indexed by row-0 COLUMN (lane, lane + 32), a cold column counting 0
-        const uint32_t cnt_a = (hot0 >> lane) & 1u ? (uint32_t)__popcll(row1_of(lane)) : 0u;
-        const uint32_t cnt_b = (hot0 >> (lane + 32)) & 1u ? (uint32_t)__popcll(row1_of(lane + 32)) : 0u;
+        // late-trace SEA) keeps all 32 lanes walking.  Row-0 columns lane and
+        // lane + 32 and the sizes of their consistent hot row-1 sets (a cold
+        // column counts 0):
+        auto row1_of = [&](uint32_t c0) { return hot1 & E->ctab[1][key32(E->scol[0][c0], rd1, w, wmask)]; };
+        const uint32_t cnt_a = (hot0_lo >> lane) & 1u ? (uint32_t)__popcll(row1_of(lane)) : 0u;
+        const uint32_t cnt_b = (hot0_hi >> lane) & 1u ? (uint32_t)__popcll(row1_of(lane + 32)) : 0u;
         uint32_t inc_a = cnt_a, inc_b = cnt_b;  // inclusive prefixes over columns 0..63
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -472,7 +501,13 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
           const uint32_t a = __shfl_sync(0xFFFFFFFFu, inc_a, j & 31), b = __shfl_sync(0xFFFFFFFFu, inc_b, j & 31);
           return j < 32 ? a : b;
         };
-        uint64_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR], rem_st[SSPD_MAX_SR];
+        auto emit = [&](uint32_t lp, uint32_t a) {
+          const uint32_t wgt = (uint32_t)__popc(a);
+          if (wgt >= 3) emit_buffered(P, eb, lp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
+        };
+        // rows 2 and 3 (the reference default SR = 4) walked in registers
+        const uint64_t hot2 = sr > 2 ? misc->rmask[2] : 0ull, hot3 = sr > 3 ? misc->rmask[3] : 0ull;
+        const uint32_t rd2 = sr > 2 ? E->rd[2] : 0u, rd3 = sr > 3 ? E->rd[3] : 0u;
         for (uint32_t base = 0; base < npairs; base += 32) {
           const uint32_t t = base + lane;
           // row-0 column of pair t: the first j with incl(j) > t
@@ -482,21 +517,37 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
             const uint32_t mid = (lo + hi) >> 1;
             if (incl_at(mid) > t) hi = mid; else lo = mid + 1;
           }
-          const uint32_t j = lo;
-          const uint32_t excl = incl_at(j == 0 ? 0 : j - 1);
+          const uint32_t c0 = lo;
+          const uint32_t excl = incl_at(c0 == 0 ? 0 : c0 - 1);
           if (t >= npairs) continue;
-          const uint32_t c0 = j;
-          const uint64_t r1 = row1_of(c0);
-          const uint32_t c1 = select64(r1, t - (j == 0 ? 0u : excl));
-          lp_st[1] = scatter_col(c0, T->isb[0], T->ibn[0], P.w) | scatter_col(c1, T->isb[1], T->ibn[1], P.w);
-          and_st[1] = full & sm[T->off_regs[0] + c0] & sm[T->off_regs[1] + c1];
+          const uint32_t c1 = select64(row1_of(c0), t - (c0 == 0 ? 0u : excl));
+          const uint32_t lp1 = E->scol[0][c0] | E->scol[1][c1];
+          const uint32_t and1 = (uint32_t)reg0[c0] & reg1[c1];
           if (sr == 2) {
-            const uint32_t wgt = (uint32_t)__popcll(and_st[1]);
-            if (wgt >= 3) emit_buffered(P, eb, lp_st[1], rp, wgt, out_ip, out_aux, out_capacity, out_count);
+            emit(lp1, and1);
             continue;
           }
+          if (sr == 4) {
+            const uint8_t* reg2 = sm + T->off_regs[2];
+            const uint8_t* reg3 = sm + T->off_regs[3];
+            for (uint64_t rem2 = hot2 & E->ctab[2][key32(lp1, rd2, w, wmask)]; rem2; rem2 &= rem2 - 1) {
+              const uint32_t c2 = (uint32_t)__ffsll((long long)rem2) - 1;
+              const uint32_t lp2 = lp1 | E->scol[2][c2];
+              const uint32_t and2 = and1 & reg2[c2];
+              for (uint64_t rem3 = hot3 & E->ctab[3][key32(lp2, rd3, w, wmask)]; rem3; rem3 &= rem3 - 1) {
+                const uint32_t c3 = (uint32_t)__ffsll((long long)rem3) - 1;
+                emit(lp2 | E->scol[3][c3], and2 & reg3[c3]);
+              }
+            }
+            continue;
+          }
+          // any other SR: explicit-stack walk over rows 2 .. sr-1
+          uint32_t lp_st[SSPD_MAX_SR], and_st[SSPD_MAX_SR];
+          uint64_t rem_st[SSPD_MAX_SR];
+          lp_st[1] = lp1;
+          and_st[1] = and1;
           uint32_t lvl = 2;
-          rem_st[2] = misc->rmask[2] & E->ctab[2][index_of(lp_st[1], T->isb[2], T->ibn[2], P.w) & T->keymask[2]];
+          rem_st[2] = hot2 & E->ctab[2][key32(lp1, rd2, w, wmask)];
           while (lvl >= 2) {
             const uint64_t rem = rem_st[lvl];
             if (rem == 0) {
@@ -505,17 +556,16 @@ __device__ void restore_sea_group(const uint8_t* __restrict__ seav, const Restor
             }
             const uint32_t c = (uint32_t)__ffsll((long long)rem) - 1;
             rem_st[lvl] = rem & (rem - 1);
-            const uint64_t nlp = lp_st[lvl - 1] | scatter_col(c, T->isb[lvl], T->ibn[lvl], P.w);
-            const uint64_t nand = and_st[lvl - 1] & sm[T->off_regs[lvl] + c];
+            const uint32_t nlp = lp_st[lvl - 1] | E->scol[lvl][c];
+            const uint32_t nand = and_st[lvl - 1] & sm[T->off_regs[lvl] + c];
             if (lvl + 1 == sr) {
-              const uint32_t wgt = (uint32_t)__popcll(nand);
-              if (wgt >= 3) emit_buffered(P, eb, nlp, rp, wgt, out_ip, out_aux, out_capacity, out_count);
+              emit(nlp, nand);
               continue;
             }
             lp_st[lvl] = nlp;
             and_st[lvl] = nand;
             ++lvl;
-            rem_st[lvl] = misc->rmask[lvl] & E->ctab[lvl][index_of(nlp, T->isb[lvl], T->ibn[lvl], P.w) & T->keymask[lvl]];
+            rem_st[lvl] = misc->rmask[lvl] & E->ctab[lvl][key32(nlp, E->rd[lvl], w, wmask)];
           }
         }
         return;
@@ -1149,6 +1199,8 @@ static int build_plan(const sspd_params& p, RestorePlan& P) {
       P.row_bits[i] = (uint32_t)row_mask(p.isb[i], p.ibn[i], p.lp_bits);
     }
     P.lane_enum = en ? 1u : 0u;
+    P.rows8 = en && p.sr <= 4 ? 1u : 0u;
+    for (uint32_t i = 0; i < p.sr && P.rows8; ++i) P.rows8 = p.sc[i] == 64 ? 1u : 0u;
     // mask walk whenever the tuple bound allows it (<= cap); the knob caps
     // it further for A/B against the bucket tables
     P.enum_max = 0xFFFFFFFFu;

@@ -120,6 +120,13 @@ def test_overflow_semantics(cuda, golden, garr):
     dict(theta=256, r=16, k=4096, lr=2, lc=4096),
     dict(theta=8, r=4, addr_bits=16, k=256, lr=2, lc=16),
     dict(theta=1024, r=16, k=8192, lr=8, lc=8192),  # config 5: 64 MiB LDCA
+    # the warp restore's hot-mask enumeration beyond SR = 4 / 64-column rows:
+    dict(theta=256, r=16, sr=4, a=1, k=4096, lr=4, lc=512),   # SR = 4, 32-column rows
+    dict(theta=256, r=12, sr=4, a=1, k=4096, lr=4, lc=512),   # SR = 4, 64-column rows
+    dict(theta=256, r=12, sr=5, a=1, k=4096, lr=4, lc=512),   # stack walk, SR = 5
+    dict(theta=256, r=8, sr=6, a=1, k=4096, lr=4, lc=512),    # SR = 6
+    dict(theta=256, r=11, sr=7, a=2, k=4096, lr=4, lc=512),   # SR = 7
+    dict(theta=256, r=16, sr=8, a=1, k=4096, lr=4, lc=512),   # SR = 8, 8-column rows
 ])
 def test_random_streams_vs_oracle(cuda, oracle, geom):
     """Geometries beyond the golden set, checked against the pinned oracle."""
