@@ -137,6 +137,14 @@ SSPD_API int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips, u
                                    const sspd_params* p, uint8_t* seav, uint8_t* ldca,
                                    void* scratch, uint64_t scratch_bytes, uint64_t chunk,
                                    void* stream);
+/* The same into an LDCA buffer that holds only zeros on entry (a fresh
+ * sliding dirty-bitmap slot, see sspd_scan_sliding_seav): K1b's final fold
+ * then stores its words instead of read-modify-writing them.  Same result
+ * as sspd_scan_partitioned on a zeroed buffer. */
+SSPD_API int sspd_scan_partitioned_fresh(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                   const sspd_params* p, uint8_t* seav, uint8_t* ldca,
+                                   void* scratch, uint64_t scratch_bytes, uint64_t chunk,
+                                   void* stream);
 SSPD_API uint64_t sspd_scan_partitioned_scratch(const sspd_params* p, uint64_t chunk);
 SSPD_API int sspd_scan_partitioned_variant(const sspd_params* p, uint64_t chunk);
 

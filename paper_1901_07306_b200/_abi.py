@@ -101,6 +101,7 @@ _SIGS = {
     "sspd_mix64_host": (_U64, [_U64]),
     "sspd_scan_discrete": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP]),
     "sspd_scan_partitioned": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "sspd_scan_partitioned_fresh": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "sspd_scan_partitioned_scratch": (_U64, [_PP, _U64]),
     "sspd_scan_partitioned_variant": (C.c_int, [_PP, _U64]),
     "sspd_host_check_u32": (C.c_int, [_VP, _U64, _U32, C.c_int]),

@@ -74,6 +74,7 @@ struct Plan {
   uint32_t tau_mask;
   uint32_t cons_warps;   // kWarpLdg / kWarpTma: consumer warps of an owner CTA
   uint32_t tma_flush;    // 1: staging runs leave shared memory as TMA bulk stores
+  uint32_t dst_zero;     // 1: the LDCA holds only zeros on entry: the fold stores, no read-modify-write
   uint32_t* ready;       // kWarpFlag: [dst][src] = chunks of src published to dst (zeroed per launch)
   uint32_t* drained;     // kWarpFlag: [dst] = chunks dst has drained
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
@@ -543,7 +544,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // fold the partition into the global LDCA: word (row, cell, j) of
   // partition q is global word (row*lc + cell)*k/32 + q*2^HB + j.  After the
   // last barrier no direct reds are in flight and the partitions are
-  // disjoint, so a plain read-modify-write is exact.
+  // disjoint, so a plain read-modify-write is exact -- and into an all-zero
+  // destination (a fresh sliding dirty bitmap) a plain store.
   if (!owner) return;
   __syncthreads();
   const uint32_t rshift = 31 - __clz(P.row_words);  // row_words is a power of two
@@ -552,7 +554,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (v) {
       const uint32_t row = i >> rshift, within = i & (P.row_words - 1u);
       const uint64_t cell = (uint64_t)row * P.lc + (within >> HB);
-      ldca[cell * P.kw + ((uint64_t)self << HB) + (within & kHMask)] |= v;
+      uint32_t* dst = ldca + cell * P.kw + ((uint64_t)self << HB) + (within & kHMask);
+      if (P.dst_zero)
+        *dst = v;
+      else
+        *dst |= v;
     }
   }
 }
@@ -712,7 +718,8 @@ uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk) {
 
 // Launch; SSPD_ERR_CONFIG when not applicable (the caller tries K1p).
 int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
-                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream) {
+                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream,
+                      bool dst_zero) {
   int dev, sms, max_smem, coop = 0;
   bpart::device_limits(dev, sms, max_smem);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -723,6 +730,7 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   int cons = 0;
   if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb, cons)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  P.dst_zero = dst_zero ? 1u : 0u;
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
   P.ready = P.counts + 2ull * P.nparts * P.nsrc;

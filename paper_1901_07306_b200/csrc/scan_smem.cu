@@ -508,7 +508,8 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
 // packet; preferred whenever its plan applies.
 uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk);
 int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
-                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream);
+                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream,
+                      bool dst_zero = false);
 
 }  // namespace sspd
 
@@ -579,6 +580,21 @@ extern "C" int sspd_scan_partitioned(const uint32_t* hips, const uint32_t* oips,
 
 // Scratch bytes the partitioned scan needs for a given chunk size (0 when
 // the LDCA cannot be partitioned into shared memory on this device).
+// sspd_scan_partitioned into an LDCA buffer that holds only zeros (a fresh
+// sliding dirty-bitmap slot): K1b's fold then stores instead of
+// read-modify-writing.  The result is the same as sspd_scan_partitioned's.
+extern "C" int sspd_scan_partitioned_fresh(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                           const sspd_params* p, uint8_t* seav, uint8_t* ldca, void* scratch,
+                                           uint64_t scratch_bytes, uint64_t chunk, void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n == 0) return SSPD_OK;
+  if (!hips || !oips || !ldca) return SSPD_ERR_DATA;
+  if (scan_bpart_scratch(p, chunk) != 0)
+    return scan_bpart_launch(hips, oips, n, p, seav, ldca, scratch, scratch_bytes, chunk, stream, true);
+  return sspd_scan_partitioned(hips, oips, n, p, seav, ldca, scratch, scratch_bytes, chunk, stream);
+}
+
 // Which partitioned scan sspd_scan_partitioned runs for this geometry:
 // 2 = K1b (b-axis partitions), 1 = K1p (word-range partitions), 0 = none
 // (the LDCA does not fit the SMs' shared memory: SSPD_ERR_CONFIG).

@@ -273,6 +273,7 @@ class _DeferredLdca:
         self.w = window_slices
         self.ring = None
         self.pending = False  # scanned since the last fold
+        self.fresh = True  # the current slice's bitmap is all zeros (nothing scanned into it yet)
         if ring:
             import torch
 
@@ -297,6 +298,7 @@ class _DeferredLdca:
 
     def mark_scanned(self):
         self.pending = True
+        self.fresh = False
         if self.ring is not None:
             self.cur_merged = False
 
@@ -315,6 +317,7 @@ class _DeferredLdca:
              pool._wrapped_now(), pool.window_slices, None if ldca_view is None else ldca_view.data_ptr(),
              stream_ptr())
         self.pending = False
+        self.fresh = True  # the fold clears the bitmap
         return ldca_view is not None
 
     def drop(self):
@@ -325,6 +328,7 @@ class _DeferredLdca:
         elif self.pending:
             self.dirty.zero_()
         self.pending = False
+        self.fresh = True
 
     # -- ring mode ------------------------------------------------------------
     @property
@@ -357,6 +361,7 @@ class _DeferredLdca:
         self.prev_ok = False
         self.pristine = pristine
         self.pending = False
+        self.fresh = True
         self.version = pool._version
 
     def sync(self, pool):
@@ -404,6 +409,7 @@ class _DeferredLdca:
             self.fold_lo = self.cur + 1
         self.cur += 1
         self.cur_merged = True
+        self.fresh = True  # slot cur + 1 was cleared above (or by view_into)
 
 
 @dataclass(frozen=True)
@@ -606,7 +612,7 @@ class SlidingDetector:
             # + tracking) with K2 restricted to the sampled packets
             if iv is not None:
                 self._iv_check(iv)
-            self._scan_dirty_partitioned(h, o, dfr.dirty_ptr())
+            self._scan_dirty_partitioned(h, o, dfr.dirty_ptr(), fresh=dfr.fresh)
             call("sspd_scan_sliding_seav", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
                  pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
                  None if iv is None else iv["view"].device_buffer().data_ptr(),
@@ -648,7 +654,7 @@ class SlidingDetector:
             ok = self._k1b_ok = int(lib().sspd_scan_partitioned_variant(self._params, 0)) > 0
         return ok
 
-    def _scan_dirty_partitioned(self, h, o, dirty_ptr: int):
+    def _scan_dirty_partitioned(self, h, o, dirty_ptr: int, fresh: bool = False):
         import torch
 
         from ._abi import check, lib
@@ -660,9 +666,9 @@ class SlidingDetector:
         buf = getattr(self, "_part_scratch", None)
         if buf is None or buf.numel() < need:
             buf = self._part_scratch = torch.empty(need, dtype=torch.uint8, device=h.device)
-        check(lib().sspd_scan_partitioned(h.data_ptr(), o.data_ptr(), n, self._params, None, dirty_ptr,
-                                          buf.data_ptr(), buf.numel(), chunk, stream_ptr()),
-              "sspd_scan_partitioned")
+        fn = lib().sspd_scan_partitioned_fresh if fresh else lib().sspd_scan_partitioned
+        check(fn(h.data_ptr(), o.data_ptr(), n, self._params, None, dirty_ptr, buf.data_ptr(), buf.numel(), chunk,
+                 stream_ptr()), "sspd_scan_partitioned")
 
     def observe(self, hip: int, oip: int):
         self.observe_batch(np.array([hip], dtype=np.uint64), np.array([oip], dtype=np.uint64))

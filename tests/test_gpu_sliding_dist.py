@@ -513,6 +513,9 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom, monk
             od = torch.zeros(n + 1, dtype=torch.int32, device="cuda")
             od[1:] = torch.from_numpy(oips.astype(np.uint32).view(np.int32)).cuda()
             a.observe_batch(hd, od[1:])
+        elif s % 4 == 1 and n > 1:  # two batches in one slice: the second ORs into a used bitmap
+            a.observe_batch(hips[: n // 3], oips[: n // 3])
+            a.observe_batch(hips[n // 3:], oips[n // 3:])
         else:
             a.observe_batch(hips, oips)
         b.observe_batch(hips, oips)
