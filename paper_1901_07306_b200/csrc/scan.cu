@@ -189,6 +189,55 @@ struct SeavTracker {
   uint32_t log_mask;             // ring size - 1
 };
 
+// The log positions are reserved per BLOCK: a sampled packet takes a slot of
+// a shared-memory staging area (shared atomic), and the block writes its
+// staged entries out with ONE atomic on the global log head when half full
+// and at its end.  (Reserving per warp from the single global counter
+// serialised every sampled packet at one L2 slice: ~14 k dependent atomics
+// per config-4 slice, 80 % of K2's stall samples.)  The ring's order within
+// a slice is irrelevant to sspd_seav_advance; only the head per slice is.
+constexpr uint32_t kLogPk = 256;  // packets staged per block (x SR entries of dynamic smem)
+struct LogStage {
+  uint32_t np;
+  unsigned long long base;
+};
+
+// one sampled packet: where its SR log entries go (staged or, when the
+// staging area is full, straight to the ring)
+struct LogDst {
+  uint32_t* ent;               // staged entries, or nullptr
+  unsigned long long base;     // ring position otherwise
+};
+
+__device__ __forceinline__ LogDst log_reserve(LogStage* ls, uint32_t* lbuf, const SeavTracker& tr, uint32_t sr) {
+  const uint32_t pk = atomicAdd(&ls->np, 1u);
+  if (pk < kLogPk) return {lbuf + pk * sr, 0ull};
+  return {nullptr, atomicAdd(tr.log_head, (unsigned long long)sr)};
+}
+
+__device__ __forceinline__ void log_put(const LogDst& d, const SeavTracker& tr, uint32_t i, uint32_t slot) {
+  if (d.ent)
+    d.ent[i] = slot;
+  else
+    tr.log[(d.base + i) & tr.log_mask] = slot;
+}
+
+// whole block (uniform call): write the staged entries out once at least
+// `thresh` packets are staged
+__device__ __forceinline__ void log_flush(LogStage* ls, const uint32_t* lbuf, const SeavTracker& tr, uint32_t sr,
+                                          uint32_t thresh) {
+  __syncthreads();
+  const uint32_t np = min(ls->np, kLogPk);
+  __syncthreads();
+  if (np == 0 || np < thresh) return;
+  if (threadIdx.x == 0) ls->base = atomicAdd(tr.log_head, (unsigned long long)np * sr);
+  __syncthreads();
+  const unsigned long long base = ls->base;
+  for (uint32_t i = threadIdx.x; i < np * sr; i += blockDim.x) tr.log[(base + i) & tr.log_mask] = lbuf[i];
+  __syncthreads();
+  if (threadIdx.x == 0) ls->np = 0;
+}
+
 // Deferred LDCA stamps (optional, `dirty != nullptr`): instead of storing
 // `now` into the 134 MB LDCA stamp region (8 random 2-byte stores per
 // packet, most of them DRAM read-modify-writes), the scan sets the slot's
@@ -216,18 +265,19 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
   const uint64_t nq = (n - head) >> 2;
   const uint4* hq = reinterpret_cast<const uint4*>(hips + head);
   const uint4* oq = reinterpret_cast<const uint4*>(oips + head);
+  extern __shared__ uint32_t lbuf[];  // kTrack: kLogPk * SR staged log entries
+  __shared__ LogStage ls;
+  if (kTrack) {
+    if (threadIdx.x == 0) ls.np = 0;
+    __syncthreads();
+  }
   auto one = [&](uint32_t hip, uint32_t oip) {
     if (sampled(oip, p.seed_h1, tmask)) {
       const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
       const uint64_t rp = hip & ((1u << p.r) - 1u);
       const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
-      unsigned long long pos = 0;
-      if (kTrack) {  // one log reservation per group of lanes sampling together (one shared counter)
-        cg::coalesced_group g = cg::coalesced_threads();
-        unsigned long long base = 0;
-        if (g.thread_rank() == 0) base = atomicAdd(tr.log_head, (unsigned long long)g.size() * p.sr);
-        pos = g.shfl(base, 0) + (unsigned long long)g.thread_rank() * p.sr;
-      }
+      LogDst d{nullptr, 0ull};
+      if (kTrack) d = log_reserve(&ls, lbuf, tr, p.sr);
       for (uint32_t i = 0; i < p.sr; ++i) {
         const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
         const uint64_t reg = rp * p.sc[i] + col;
@@ -236,7 +286,7 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
         if (kTrack) {
           const uint64_t vbit = (p.seav_row_off[i] + reg * p.reg_bytes) * 8 + bit;
           atomicOr(tr.view + (vbit >> 5), 1u << (vbit & 31));
-          tr.log[(pos + i) & tr.log_mask] = (uint32_t)slot;
+          log_put(d, tr, i, (uint32_t)slot);
         }
       }
     }
@@ -253,16 +303,22 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_fast_kernel(const uint32
       cell += p.lc;
     }
   };
-  for (uint64_t q = tid; q < nq; q += stride) {
-    const uint4 h = ld_stream(hq + q);
-    const uint4 o = ld_stream(oq + q);
-    one(h.x, o.x);
-    one(h.y, o.y);
-    one(h.z, o.z);
-    one(h.w, o.w);
+  // block-uniform trip count (the log flush is a block barrier)
+  for (uint64_t qb = tid - threadIdx.x; qb < nq; qb += stride) {
+    const uint64_t q = qb + threadIdx.x;
+    if (q < nq) {
+      const uint4 h = ld_stream(hq + q);
+      const uint4 o = ld_stream(oq + q);
+      one(h.x, o.x);
+      one(h.y, o.y);
+      one(h.z, o.z);
+      one(h.w, o.w);
+    }
+    if (kTrack) log_flush(&ls, lbuf, tr, p.sr, kLogPk / 2);
   }
   if (tid < head) one(hips[tid], oips[tid]);
   for (uint64_t j = head + (nq << 2) + tid; j < n; j += stride) one(hips[j], oips[j]);
+  if (kTrack) log_flush(&ls, lbuf, tr, p.sr, 1);
 }
 
 // K2 for u16 stamps when the fast path does not apply (k or lc not a power
@@ -279,19 +335,24 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_generic_kernel(const uin
   const uint32_t tmask = tau_mask(p.tau);
   uint16_t* const lpool = pool + p.slot_ldca_base;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+  extern __shared__ uint32_t lbuf[];  // kTrack: kLogPk * SR staged log entries
+  __shared__ LogStage ls;
+  if (kTrack) {
+    if (threadIdx.x == 0) ls.np = 0;
+    __syncthreads();
+  }
+  // block-uniform trip count (the log flush is a block barrier)
+  for (uint64_t jb = (uint64_t)blockIdx.x * blockDim.x; jb < n; jb += stride) {
+    const uint64_t j = jb + threadIdx.x;
+    if (kTrack) log_flush(&ls, lbuf, tr, p.sr, kLogPk / 2);
+    if (j >= n) continue;
     const uint32_t hip = hips[j], oip = oips[j];
     if (sampled(oip, p.seed_h1, tmask)) {
       const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
       const uint64_t rp = hip & ((1u << p.r) - 1u);
       const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
-      unsigned long long pos = 0;
-      if (kTrack) {
-        cg::coalesced_group g = cg::coalesced_threads();
-        unsigned long long base = 0;
-        if (g.thread_rank() == 0) base = atomicAdd(tr.log_head, (unsigned long long)g.size() * p.sr);
-        pos = g.shfl(base, 0) + (unsigned long long)g.thread_rank() * p.sr;
-      }
+      LogDst d{nullptr, 0ull};
+      if (kTrack) d = log_reserve(&ls, lbuf, tr, p.sr);
       for (uint32_t i = 0; i < p.sr; ++i) {
         const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
         const uint64_t reg = rp * p.sc[i] + col;
@@ -300,7 +361,7 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_generic_kernel(const uin
         if (kTrack) {
           const uint64_t vbit = (p.seav_row_off[i] + reg * p.reg_bytes) * 8 + bit;
           atomicOr(tr.view + (vbit >> 5), 1u << (vbit & 31));
-          tr.log[(pos + i) & tr.log_mask] = (uint32_t)slot;
+          log_put(d, tr, i, (uint32_t)slot);
         }
       }
     }
@@ -317,6 +378,7 @@ __global__ void __launch_bounds__(256) scan_sliding_u16_generic_kernel(const uin
       cell += p.lc;
     }
   }
+  if (kTrack) log_flush(&ls, lbuf, tr, p.sr, 1);
 }
 
 template <bool S, bool L>
@@ -467,7 +529,8 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
           const int cap = (int)cap_bps * sms;
           if (grid > cap) grid = cap;
         }
-        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker, dirty);
+        const size_t lsm = tracker.view ? (size_t)kLogPk * p->sr * 4 : 0;
+        kern<<<grid, 256, lsm, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, frac, tracker, dirty);
         break;
       }
       if (tracker.view || dirty) {  // the caller's tracked / deferred state must be honoured
@@ -476,7 +539,8 @@ static int scan_sliding_impl(const uint32_t* hips, const uint32_t* oips, uint64_
                         ? (dirty ? scan_sliding_u16_generic_kernel<true, true> : scan_sliding_u16_generic_kernel<true, false>)
                         : scan_sliding_u16_generic_kernel<false, true>;
         const int grid = grid_for(kern, 256, n);
-        kern<<<grid, 256, 0, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, tracker, dirty);
+        const size_t lsm = tracker.view ? (size_t)kLogPk * p->sr * 4 : 0;
+        kern<<<grid, 256, lsm, st>>>(hips, oips, n, *p, (uint16_t*)pool, (uint16_t)now_wrapped, tracker, dirty);
         break;
       }
       const int grid = grid_for(scan_sliding_kernel<uint16_t>, 256, n);
