@@ -385,6 +385,12 @@ SSPD_API int sspd_microbench_red(void* buf, uint64_t bytes, int blocks_per_sm,
 SSPD_API int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                   const sspd_params* p, int blocks_per_sm, uint32_t* sink,
                                   double* pkts_per_s, void* stream);
+/* Self-check of the scans' 32-bit-key hash (mix64_lo_fast: low word of
+ * SplitMix64, hashing.py:48-53, evaluated in 32-bit halves) against the
+ * 64-bit definition for every key in [key0, key0 + nkeys) (<= 2^32):
+ * *mismatches = count, *first_bad = smallest mismatching key (~0 if none). */
+SSPD_API int sspd_check_hash32(uint64_t seed, uint64_t key0, uint64_t nkeys, uint64_t* mismatches,
+                               uint64_t* first_bad, void* stream);
 /* Random st.global.u16 rate over a `bytes` (power of two) footprint -- the
  * measured roofline term of the sliding scan K2. */
 SSPD_API int sspd_microbench_store16(void* buf, uint64_t bytes, int blocks_per_sm,

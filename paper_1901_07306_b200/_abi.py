@@ -135,6 +135,7 @@ _SIGS = {
     "sspd_route_pairs": (C.c_int, [_VP, _VP, _U64, _PP, C.POINTER(Divisor_t), C.c_int, _U64, _VP, _VP]),
     "sspd_microbench_red": (C.c_int, [_VP, _U64, C.c_int, C.c_int, C.POINTER(C.c_double), _VP]),
     "sspd_microbench_hash": (C.c_int, [_VP, _VP, _U64, _PP, C.c_int, _VP, C.POINTER(C.c_double), _VP]),
+    "sspd_check_hash32": (C.c_int, [_U64, _U64, _U64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _VP]),
     "sspd_microbench_store16": (C.c_int, [_VP, _U64, C.c_int, C.c_int, C.POINTER(C.c_double), _VP]),
     "sspd_ipc_alloc": (C.c_int, [_U64, C.POINTER(_VP)]),
     "sspd_ipc_free": (C.c_int, [_VP]),

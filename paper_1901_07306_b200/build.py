@@ -31,16 +31,19 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > built for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source into one shared library (idempotent)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None) -> Path:
+    """Compile every CUDA source into one shared library (idempotent).  `out`
+    (tuning A/B builds only) writes the library elsewhere."""
+    if out is None and not force and not _stale():
         return LIB_PATH
+    lib_path = Path(out) if out is not None else LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                     "-I", str(ROOT / "include"), "-Xptxas", "-v" if verbose else "-O3"]
+    flags += os.environ.get("SSPD_NVCC_FLAGS", "").split()  # A/B builds of compile-time knobs
     for src in SOURCES:
-        obj = LIB_DIR / (Path(src).stem + ".o")
+        obj = LIB_DIR / (Path(src).stem + f".{os.getpid()}.o")
         cmd = [NVCC, "-c", str(CSRC / src), "-o", str(obj)] + flags
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -48,16 +51,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose and res.stderr:
             print(res.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    tmp = lib_path.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-o", str(tmp)] + ARCH + [*objs, "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, lib_path)
     for o in objs:
         os.unlink(o)
-    return LIB_PATH
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    outs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=Path(outs[0]) if outs else None))

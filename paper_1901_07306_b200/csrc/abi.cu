@@ -43,11 +43,11 @@ __global__ void __launch_bounds__(256) microbench_store16_kernel(uint16_t* buf, 
 // it reaches bound any scan that must compute these indexes (SURVEY.md
 // §8(a) a1-a2): K1b is issue-bound on exactly this work.
 struct HashSeeds {
-  uint32_t s_lo[2 + SSPD_MAX_LR], s_hg[2 + SSPD_MAX_LR];
+  SplitSeed ss[2 + SSPD_MAX_LR];
   uint32_t lr, k_mask, lc_mask, tmask;
 };
 
-template <int kMinBlocks>
+template <int kMinBlocks, int kLRc>
 __global__ void __launch_bounds__(1024, kMinBlocks)
     microbench_hash_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips, uint64_t nq,
                            const __grid_constant__ HashSeeds S, uint32_t* sink) {
@@ -59,10 +59,11 @@ __global__ void __launch_bounds__(1024, kMinBlocks)
     const uint32_t h[4] = {hv.x, hv.y, hv.z, hv.w}, o[4] = {ov.x, ov.y, ov.z, ov.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      uint32_t v = mix64_lo_split(o[e], S.s_lo[0], S.s_hg[0]) & S.k_mask;
-      v ^= (mix64_lo_split(o[e], S.s_lo[1], S.s_hg[1]) & S.tmask) == 0u ? 0x80000000u : 0u;
+      uint32_t v = mix64_lo_fast(o[e], S.ss[0]) & S.k_mask;
+      v ^= (mix64_lo_fast(o[e], S.ss[1]) & S.tmask) == 0u ? 0x80000000u : 0u;
+      const uint32_t lr = kLRc ? kLRc : S.lr;  // LR = 8 (the scans' compile-time rows): seeds as constant operands
 #pragma unroll 8
-      for (uint32_t i = 0; i < S.lr; ++i) v += (mix64_lo_split(h[e], S.s_lo[2 + i], S.s_hg[2 + i]) & S.lc_mask) << i;
+      for (uint32_t i = 0; i < lr; ++i) v += (mix64_lo_fast(h[e], S.ss[2 + i]) & S.lc_mask) << i;
       acc ^= v;
     }
   }
@@ -90,8 +91,7 @@ extern "C" int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, 
   const uint64_t seeds[2] = {p->seed_h3, p->seed_h1};
   for (int i = 0; i < 2 + (int)p->lr; ++i) {
     const uint64_t sd = i < 2 ? seeds[i] : p->seed_lh[i - 2];
-    S.s_lo[i] = (uint32_t)sd;
-    S.s_hg[i] = (uint32_t)(sd >> 32) + (uint32_t)(kGolden >> 32);
+    S.ss[i] = split_seed(sd);
   }
   S.lr = p->lr;
   S.k_mask = p->k - 1;
@@ -104,10 +104,15 @@ extern "C" int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, 
   const uint64_t nq = n / 4;
   const int threads = 1024, grid = sms * blocks_per_sm;
   auto launch = [&]() {
-    if (blocks_per_sm == 1)
-      microbench_hash_kernel<1><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+    const bool lr8 = S.lr == 8;
+    if (blocks_per_sm == 1 && lr8)
+      microbench_hash_kernel<1, 8><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+    else if (blocks_per_sm == 1)
+      microbench_hash_kernel<1, 0><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+    else if (lr8)
+      microbench_hash_kernel<2, 8><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
     else
-      microbench_hash_kernel<2><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
+      microbench_hash_kernel<2, 0><<<grid, threads, 0, st>>>(hips, oips, nq, S, sink);
   };
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -126,6 +131,50 @@ extern "C" int sspd_microbench_hash(const uint32_t* hips, const uint32_t* oips, 
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   *pkts_per_s = (double)(nq * 4) / (best * 1e-3);
+  return check_launch();
+}
+
+// ---- the scans' 32-bit hash against the 64-bit definition --------------
+// Every 32-bit key k in [key0, key0 + nkeys): mix64_lo_fast(k, split_seed(seed))
+// == (uint32_t)mix64(k ^ seed) (hashing.py:48-53).  Mismatches are counted
+// and the smallest mismatching key is kept (0xFFFFFFFFFFFFFFFF when none).
+__global__ void check_mix_kernel(uint64_t seed, SplitSeed ss, uint64_t key0, uint64_t nkeys,
+                                 unsigned long long* out) {
+  uint32_t bad = 0;
+  unsigned long long first = ~0ull;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nkeys; i += stride) {
+    const uint32_t k = (uint32_t)(key0 + i);
+    if (mix64_lo_fast(k, ss) != (uint32_t)mix64((uint64_t)k ^ seed)) {
+      ++bad;
+      first = min(first, (unsigned long long)k);
+    }
+  }
+  if (bad) {
+    atomicAdd(out, (unsigned long long)bad);
+    atomicMin(out + 1, first);
+  }
+}
+
+extern "C" int sspd_check_hash32(uint64_t seed, uint64_t key0, uint64_t nkeys, uint64_t* mismatches,
+                                 uint64_t* first_bad, void* stream) {
+  if (!mismatches || !first_bad || key0 + nkeys > (1ull << 32) || nkeys == 0) return SSPD_ERR_DATA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 16) != cudaSuccess) return SSPD_ERR_CUDA;
+  const unsigned long long init[2] = {0ull, ~0ull};
+  cudaMemcpyAsync(d, init, 16, cudaMemcpyHostToDevice, st);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  check_mix_kernel<<<sms * 8, 256, 0, st>>>(seed, split_seed(seed), key0, nkeys, d);
+  unsigned long long h[2];
+  cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) return SSPD_ERR_CUDA;
+  *mismatches = h[0];
+  *first_bad = h[1];
   return check_launch();
 }
 

@@ -67,7 +67,7 @@ struct Plan {
   uint32_t* counts;      // [2][dst][src]
   uint32_t k_mask, lc_mask, log2k, lc;
   uint32_t kw;           // k / 32: words per cell in the global LDCA
-  uint32_t s_lo[10], s_hg[10];  // split seeds (mix64_lo_split): H3, H1, LH0..7
+  SplitSeed ss[10];     // split seeds (mix64_lo_fast): H3, H1, LH0..7
   uint32_t vec_ok;       // hips/oips 16-byte aligned and chunk % 4 == 0
   uint32_t qstride;      // nsrc * region_cap: bucket entries per destination
   uint32_t gshift;       // log2 of the flush group (threads per destination)
@@ -102,7 +102,7 @@ __device__ __noinline__ void seav_update_ool(const sspd_params& p, uint32_t hip,
 // Staging row full (rare): the packet's LR bits as direct L2 reds (exact).
 __device__ __noinline__ void direct_packet(const Plan& P, uint32_t hip, uint32_t b, uint32_t* ldca) {
   for (uint32_t i = 0; i < kLR; ++i) {
-    const uint32_t c = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
+    const uint32_t c = mix64_lo_fast(hip, P.ss[2 + i]) & P.lc_mask;
     const uint32_t bit = ((i * P.lc + c) << P.log2k) | b;
     red_or_g(ldca + (bit >> 5), 1u << (bit & 31u));
   }
@@ -448,14 +448,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t j = base + (uint64_t)tid * kPkt + e;
           const uint32_t hip = ch[e], oip = co[e];
           if (j < hi) {
-            const uint32_t b = mix64_lo_split(oip, P.s_lo[0], P.s_hg[0]) & P.k_mask;
+            const uint32_t b = mix64_lo_fast(oip, P.ss[0]) & P.k_mask;
             const uint32_t q = b >> P.bshift;
             const uint32_t bhi = (b >> 5) & kHMask;
             // the word bits shared by all halves (half 0: word index, 1..7: byte offsets)
             const uint32_t both = (bhi << 2) * 0x10001u;
             uint32_t c[kLR];
 #pragma unroll
-            for (uint32_t i = 0; i < kLR; ++i) c[i] = mix64_lo_split(hip, P.s_lo[2 + i], P.s_hg[2 + i]) & P.lc_mask;
+            for (uint32_t i = 0; i < kLR; ++i) c[i] = mix64_lo_fast(hip, P.ss[2 + i]) & P.lc_mask;
             uint4 ent;
             ent.x = (c[0] << HB) + bhi + ((b & 31u) << P.bsh_shift) + c[1] * (1u << (18 + HB)) + (both & 0xFFFF0000u) +
                     P.rowc[0];
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               stage[q * P.stage_slots + slot] = ent;
             else
               direct_packet(P, hip, b, ldca);  // staging row full: direct (exact)
-            if (kSeav && (mix64_lo_split(oip, P.s_lo[1], P.s_hg[1]) & P.tau_mask) == 0u) {
+            if (kSeav && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
               const uint32_t qs = atomicAdd(sq_cnt + par, 1u);
               if (qs < kSeavQueue)
                 sq_base[par * kSeavQueue + qs] = make_uint2(hip, oip);
@@ -662,10 +662,7 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   P.tau_mask = tau_mask(p->tau);
   const uint64_t seeds[10] = {p->seed_h3,    p->seed_h1,    p->seed_lh[0], p->seed_lh[1], p->seed_lh[2],
                               p->seed_lh[3], p->seed_lh[4], p->seed_lh[5], p->seed_lh[6], p->seed_lh[7]};
-  for (int i = 0; i < 10; ++i) {
-    P.s_lo[i] = (uint32_t)seeds[i];
-    P.s_hg[i] = (uint32_t)(seeds[i] >> 32) + (uint32_t)(kGolden >> 32);
-  }
+  for (int i = 0; i < 10; ++i) P.ss[i] = split_seed(seeds[i]);
   return true;
 }
 

@@ -44,6 +44,61 @@ __device__ __forceinline__ uint32_t mix64_lo_split(uint32_t key, uint32_t s_lo, 
 }
 #endif
 
+// Per-seed constants of mix64_lo_fast (host-computed once per launch).
+struct SplitSeed {
+  uint32_t lo;  // low word of the seed
+  uint32_t hg;  // high word of the seed + high word of the golden gamma
+  uint32_t d;   // T(hg+1) - T(hg), T(h) = (h ^ (h >> 30)) * lo32(kMixA)
+  uint32_t e;   // T(hg) - hg * d
+};
+
+SSPD_HD SplitSeed split_seed(uint64_t seed) {
+  SplitSeed s;
+  s.lo = (uint32_t)seed;
+  s.hg = (uint32_t)(seed >> 32) + (uint32_t)(kGolden >> 32);
+  const uint32_t h1 = s.hg + 1u;
+  const uint32_t t0 = (s.hg ^ (s.hg >> 30)) * (uint32_t)kMixA, t1 = (h1 ^ (h1 >> 30)) * (uint32_t)kMixA;
+  s.d = t1 - t0;
+  s.e = t0 - s.hg * s.d;
+  return s;
+}
+
+#if defined(__CUDACC__)
+// Low 32 bits of mix64(key ^ seed) for a 32-bit key, in 32-bit halves with
+// the high-word chain of the first round folded away: after the gamma add
+// the high word H0 is hg or hg + 1 (the carry of the low add), so its
+// contribution to the first product, (H0 ^ (H0 >> 30)) * lo32(kMixA), is the
+// affine H0 * d + e.  18 instructions per hash instead of 21.  Measured B200
+// pipe costs (tools/pipe_probe.cu): LOP3/SHF/IADD3 and IMAD take 2 cycles of
+// their pipe (alu / fma), IMAD.WIDE and IMAD.HI take 4; this form is 10 alu +
+// 8 fma instructions (2 of them WIDE) = 20 + 20 pipe cycles per warp, against
+// 24 alu-pipe cycles for the 64-bit form (tools/hash_variants.cu: 129 vs
+// 115 Gpps for the scans' ten hashes per packet).  Bit-identical to
+// (uint32_t)mix64(key ^ seed) for every key and seed (checked exhaustively
+// over the 2^32 keys in tests/test_gpu_hash.py).
+__device__ __forceinline__ uint32_t mix64_lo_fast(uint32_t key, uint32_t s_lo, uint32_t hg, uint32_t d, uint32_t e) {
+  uint32_t l0, h0;
+  asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;"
+      : "=r"(l0), "=r"(h0)
+      : "r"(key ^ s_lo), "n"((uint32_t)(kGolden & 0xFFFFFFFFull)), "r"(hg));
+  const uint32_t yl = l0 ^ __funnelshift_r(l0, h0, 30);
+  const uint32_t p = yl * (uint32_t)(kMixA >> 32) + (h0 * d + e);
+  const uint64_t w = (uint64_t)yl * (uint32_t)kMixA;
+  const uint32_t z1l = (uint32_t)w, z1h = (uint32_t)(w >> 32) + p;
+  const uint32_t y2l = z1l ^ __funnelshift_r(z1l, z1h, 27);
+  const uint32_t y2h = z1h ^ (z1h >> 27);
+  const uint64_t w2 = (uint64_t)y2l * (uint32_t)kMixB;
+  uint32_t z2h;  // hi(y2l * lo(B)) + y2l * hi(B) + y2h * lo(B) as one dependent chain (2 IMAD after the wide one)
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(z2h) : "r"(y2l), "n"((uint32_t)(kMixB >> 32)), "r"((uint32_t)(w2 >> 32)));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(z2h) : "r"(y2h), "n"((uint32_t)kMixB));
+  const uint32_t z2l = (uint32_t)w2;
+  return z2l ^ __funnelshift_r(z2l, z2h, 31);
+}
+__device__ __forceinline__ uint32_t mix64_lo_fast(uint32_t key, const SplitSeed& s) {
+  return mix64_lo_fast(key, s.lo, s.hg, s.d, s.e);
+}
+#endif
+
 SSPD_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #if defined(__CUDA_ARCH__)
   return __umul64hi(a, b);
