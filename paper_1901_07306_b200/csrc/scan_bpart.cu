@@ -46,7 +46,7 @@ constexpr uint32_t kThreads = 1024;
 constexpr uint32_t kPkt = 4;  // packets per thread per tile (one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPkt;
 constexpr uint32_t kLR = 8;
-constexpr uint32_t kSeavQueue = 128;  // sampled packets per tile parity
+constexpr uint32_t kSeavQueue = 2048;  // sampled packets per CTA per chunk (expected ~570 at tau = 7)
 constexpr uint32_t kMaxSrc = 256;     // producer CTAs (SMs) the plan supports
 
 struct Plan {
@@ -196,7 +196,7 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 }
 
 // Shared memory: [part_words | nparts*stage_slots uint4 staging | nparts cnt |
-//                 4 sq_cnt | 2*kSeavQueue (hip, oip) | kWarpTma: kRing*kSlot uint4
+//                 4 sq_cnt | kSeavQueue (hip, oip) | kWarpTma: kRing*kSlot uint4
 //                 ring | 2*kRing mbarriers]
 // Warp-specialised owner CTAs (kWarpLdg / kWarpTma): P.cons_warps warps consume chunk t-1
 // (the bucket entries into the shared partition: LSU/shared-atomic work)
@@ -216,6 +216,10 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 // 4.23 vs 4.19 ms: the barrier share of the stall samples is the drain's
 // pace, not the barrier itself.
 enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2, kWarpFlag = 3 };
+#ifndef SSPD_BPART_DIAG  // timing diagnostics (tools builds only): 1 drain w/o atomics, 2 no staging,
+                         // 4 no per-tile barriers, 8 no SEAV sampling
+#define SSPD_BPART_DIAG 0
+#endif
 #ifndef SSPD_BPART_DRAIN_LOADS
 #define SSPD_BPART_DRAIN_LOADS 4
 #endif
@@ -231,9 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* part = smem;
   uint4* stage = reinterpret_cast<uint4*>(smem + P.part_words);  // part_words % 4 == 0
   uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
-  uint32_t* sq_cnt = cnt + P.nparts;                        // [2] (+2 pad); nparts % 4 == 0
-  uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [2][kSeavQueue]
-  uint4* ring = reinterpret_cast<uint4*>(sq_base + 2 * kSeavQueue);  // kWarpTma: [kRing][kSlot]
+  uint32_t* sq_cnt = cnt + P.nparts;                        // [1] (+3 pad); nparts % 4 == 0
+  uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [kSeavQueue]
+  uint4* ring = reinterpret_cast<uint4*>(sq_base + kSeavQueue);  // kWarpTma: [kRing][kSlot]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(ring + kRing * kSlot);
   uint64_t* empty_bar = full_bar + kRing;
   cg::grid_group grid = cg::this_grid();
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool producer = tid < nprod;
   const uint32_t tile = nprod * kPkt;
   auto pbar = [&]() {  // the producers' barrier
+    if (SSPD_BPART_DIAG & 4) return;  // timing diagnostic: no per-tile barriers
     if (kSpec)
       asm volatile("bar.sync 1, %0;" ::"r"(nprod) : "memory");
     else
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   while (gs && (nprod >> gs) < np) --gs;
   const uint32_t G = 1u << gs, gl = tid & (G - 1u), fq = tid >> gs;
   const bool flusher = producer && fq < np;
-  if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+  if (tid == 0) sq_cnt[0] = 0;
   if (kCons == kWarpTma && tid == 0) {
     for (uint32_t r = 0; r < kRing; ++r) {
       mbar_init(full_bar + r, 1);                     // the issuing lane's expect_tx
@@ -273,6 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   uint32_t ring_s = 0, ring_ph = 0;  // consumer pipeline position (kept across chunks)
+#if SSPD_BPART_DIAG
+  uint32_t diag = 0;
+#endif
 
   const uint64_t nchunks = (P.n + P.chunk - 1) / P.chunk;
   for (uint64_t t = 0; t <= nchunks; ++t) {
@@ -366,6 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int g = 0; g < kInFlight; ++g) {
             if (j0 + 32 * g < m) {
               const uint4 e = u[g];
+#if SSPD_BPART_DIAG & 1
+              diag ^= e.x ^ e.y ^ e.z ^ e.w;  // timing diagnostic: drain without the shared atomics
+              continue;
+#endif
               const uint32_t bit = 1u << ((e.x >> bss) & 31u);
               atomicOr(part + (e.x & lowm), bit);
               atomicOr(reinterpret_cast<uint32_t*>(pb + (e.x >> 16)), bit);
@@ -434,8 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pos = 0;
       uint32_t nh[kPkt], no[kPkt];
       fetch(lo + (uint64_t)tid * kPkt, nh, no);
-      uint32_t par = 0;  // tile parity: selects the sampled-packet queue
-      for (uint64_t base = lo; base < hi; base += tile, par ^= 1u) {
+      for (uint64_t base = lo; base < hi; base += tile) {
         uint32_t ch[kPkt], co[kPkt];
 #pragma unroll
         for (uint32_t e = 0; e < kPkt; ++e) {
@@ -462,28 +473,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             ent.y = c[2] * (1u << (2 + HB)) + c[3] * (1u << (18 + HB)) + (both + P.rowc[1]);
             ent.z = c[4] * (1u << (2 + HB)) + c[5] * (1u << (18 + HB)) + (both + P.rowc[2]);
             ent.w = c[6] * (1u << (2 + HB)) + c[7] * (1u << (18 + HB)) + (both + P.rowc[3]);
+#if SSPD_BPART_DIAG & 2
+            diag ^= ent.x ^ ent.y ^ ent.z ^ ent.w ^ q;  // timing diagnostic: no staging
+#else
             const uint32_t slot = atomicAdd(&cnt[q], 1u);
             if (slot < P.stage_slots)
               stage[q * P.stage_slots + slot] = ent;
             else
               direct_packet(P, hip, b, ldca);  // staging row full: direct (exact)
-            if (kSeav && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
-              const uint32_t qs = atomicAdd(sq_cnt + par, 1u);
+#endif
+            if (kSeav && !(SSPD_BPART_DIAG & 8) && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
+              const uint32_t qs = atomicAdd(sq_cnt, 1u);
               if (qs < kSeavQueue)
-                sq_base[par * kSeavQueue + qs] = make_uint2(hip, oip);
+                sq_base[qs] = make_uint2(hip, oip);
               else
-                seav_update_ool(p, hip, oip, seav);  // queue full (a skewed tile): apply now
+                seav_update_ool(p, hip, oip, seav);  // queue full (a skewed slice): apply now
             }
           }
         }
         pbar();
-        if (kSeav) {  // the tile's sampled packets, all producer lanes busy
-          const uint32_t nq = min(sq_cnt[par], kSeavQueue);
-          const uint2* sq = sq_base + par * kSeavQueue;
-          for (uint32_t i = tid; i < nq; i += nprod) seav_update(p, sq[i].x, sq[i].y, seav);
-          // the previous tile's queue was fully read before this barrier
-          if (tid == 0) sq_cnt[par ^ 1u] = 0;
-        }
         // flush: the G = 2^gshift threads of group fq copy destination fq's
         // run of 16-B entries into this CTA's own region of that bucket (no
         // global atomics); `pos` lives in registers, identical in the group
@@ -523,9 +531,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         pbar();
       }
-      if (kSeav) {  // queues restart at parity 0 with the next chunk's slice
+      if (kSeav) {
+        // the slice's sampled packets (0.78 % at tau = 7), queued per chunk
+        // and applied here by consecutive producer lanes (full warps): a
+        // per-tile pass left one warp updating while the others waited at
+        // the tile barrier (-0.3 ms per config-2 window)
         pbar();
-        if (tid == 0) sq_cnt[0] = sq_cnt[1] = 0;
+        const uint32_t nq = min(sq_cnt[0], kSeavQueue);
+        for (uint32_t i = tid; i < nq; i += nprod) seav_update(p, sq_base[i].x, sq_base[i].y, seav);
+        pbar();
+        if (tid == 0) sq_cnt[0] = 0;
       }
       // publish this CTA's run lengths for chunk t
       if (flusher && gl == 0) {
@@ -546,6 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // last barrier no direct reds are in flight and the partitions are
   // disjoint, so a plain read-modify-write is exact -- and into an all-zero
   // destination (a fresh sliding dirty bitmap) a plain store.
+#if SSPD_BPART_DIAG
+  if (diag == 0x9E3779B9u) ldca[tid] = diag;  // keep the diagnostic work alive
+#endif
   if (!owner) return;
   __syncthreads();
   const uint32_t rshift = 31 - __clz(P.row_words);  // row_words is a power of two
@@ -599,7 +617,7 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
     const double mean = (double)kTile / np;
     P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
   }
-  smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 16ull * kSeavQueue;
+  smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 8ull * kSeavQueue;
   // consumer mode (SSPD_BPART_CONS = 0 in line / 1 warp-specialised, global
   // loads (default) / 2 warp-specialised, TMA ring)
   // producer tiles per chunk: 16 measured best on B200 (fewer grid barriers
