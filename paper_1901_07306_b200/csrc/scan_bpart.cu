@@ -217,7 +217,7 @@ __device__ __forceinline__ uint64_t slice_start(const Plan& P, uint64_t c0, uint
 // pace, not the barrier itself.
 enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2, kWarpFlag = 3 };
 #ifndef SSPD_BPART_DIAG  // timing diagnostics (tools builds only): 1 drain w/o atomics, 2 no staging,
-                         // 4 no per-tile barriers, 8 no SEAV sampling
+                         // 4 no per-tile barriers, 8 no SEAV sampling, 16 no drain
 #define SSPD_BPART_DIAG 0
 #endif
 #ifndef SSPD_BPART_DRAIN_LOADS
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       char* const pb = reinterpret_cast<char*>(part);
       // warp w drains sources w, w+W, ...: lane j holds the run length of
       // source w+W*j, fetched at once so no region waits on its count
-      for (uint32_t src0 = cw; src0 < ns; src0 += 32u * ncw) {
+      for (uint32_t src0 = cw; src0 < ((SSPD_BPART_DIAG & 16) ? 0u : ns); src0 += 32u * ncw) {
       const uint32_t my_src = src0 + ncw * lane;
       if (kCons == kWarpFlag && my_src < ns) {  // chunk t-1 of this source published to us?
         const uint32_t* f = P.ready + (size_t)self * ns + my_src;

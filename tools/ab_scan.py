@@ -36,14 +36,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--tag", default=os.environ.get("SSPD_B200_LIB", "default"))
+    ap.add_argument("--packets", type=int, default=0, help="scan only the first N pairs (e.g. a config-4 slice)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     hips, oips, _ = generate(CONFIG2, "torch", dev)
+    if args.packets:
+        hips, oips = hips[:args.packets].contiguous(), oips[:args.packets].contiguous()
     n = int(hips.numel())
     dp = DetectorParams(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=80.5e6)
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         st = DetectorState.create(dp)
+    st.partitioned_min_packets = 1  # the partitioned scan at any size
     sink = torch.empty(4096 * 148, dtype=torch.int32, device=dev)
     floor = {}
     for bps in (1, 2):
