@@ -216,6 +216,19 @@ SSPD_API int sspd_scan_sliding_seav(const uint32_t* hips, const uint32_t* oips, 
                                     const sspd_params* p, void* pool, uint32_t ts_bytes, uint64_t now_wrapped,
                                     uint32_t max_blocks_per_sm, uint8_t* seav_view, uint32_t* log,
                                     uint64_t log_entries, unsigned long long* log_head, void* stream);
+/* sspd_scan_sliding_partitioned = both halves of one sliding slice in ONE
+ *       launch of the partitioned scan K1b: the LDCA half into the slice's
+ *       dirty bitmap `dirty` (dirty_fresh: it holds only zeros), the SEAV
+ *       stamps (+ optional view and slot log) from K1b's sampled-packet
+ *       queue.  Same state as sspd_scan_partitioned(seav = NULL, ldca =
+ *       dirty) + sspd_scan_sliding_seav (observe_batch, sliding.py:156-185);
+ *       u16 stamps only; SSPD_ERR_CONFIG when K1b does not apply. */
+SSPD_API int sspd_scan_sliding_partitioned(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                           const sspd_params* p, void* pool, uint32_t ts_bytes,
+                                           uint64_t now_wrapped, uint8_t* seav_view, uint32_t* log,
+                                           uint64_t log_entries, unsigned long long* log_head, uint8_t* dirty,
+                                           int dirty_fresh, void* scratch, uint64_t scratch_bytes,
+                                           uint64_t chunk, void* stream);
 SSPD_API int sspd_scan_sliding_deferred(const uint32_t* hips, const uint32_t* oips, uint64_t n,
                                         const sspd_params* p, void* pool, uint32_t ts_bytes,
                                         uint64_t now_wrapped, uint32_t max_blocks_per_sm,

@@ -120,6 +120,8 @@ _SIGS = {
     "sspd_scan_sliding_deferred": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP, _VP, _U64, _VP, _VP,
                                              _VP]),
     "sspd_scan_sliding_seav": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _U32, _VP, _VP, _U64, _VP, _VP]),
+    "sspd_scan_sliding_partitioned": (C.c_int, [_VP, _VP, _U64, _PP, _VP, _U32, _U64, _VP, _VP, _U64, _VP, _VP,
+                                                C.c_int, _VP, _U64, _U64, _VP]),
     "sspd_ldca_fold": (C.c_int, [_VP, _U32, _PP, _VP, _U64, _U64, _VP, _VP]),
     "sspd_ldca_window_or": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "sspd_ldca_fold_ring": (C.c_int, [_VP, _U32, _PP, _VP, _U64, _U32, _U64, _U64, _VP]),

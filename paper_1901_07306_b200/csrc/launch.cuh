@@ -54,4 +54,21 @@ static inline int validate_params(const sspd_params* p) {
   return SSPD_OK;
 }
 
+// K1b (scan_bpart.cu): the LDCA cut along its b axis, one 16-B entry per
+// packet; preferred whenever its plan applies.  `slide` (optional): the
+// sliding SEAV sink -- u16 stamps (+ view, slot log) of the sampled packets
+// instead of SEAV bits.
+struct SlideSeavSink {
+  uint16_t* pool;
+  uint32_t now;
+  uint32_t* view;
+  uint32_t* log;
+  unsigned long long* log_head;
+  uint32_t log_mask;
+};
+uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk);
+int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
+                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream,
+                      bool dst_zero = false, const SlideSeavSink* slide = nullptr);
+
 }  // namespace sspd

@@ -78,6 +78,14 @@ struct Plan {
   uint32_t* ready;       // kWarpFlag: [dst][src] = chunks of src published to dst (zeroed per launch)
   uint32_t* drained;     // kWarpFlag: [dst] = chunks dst has drained
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
+  // sliding SEAV sink (kSm == 2): u16 stamps of the sampled packets (+ the
+  // optional incremental view and slot log), as K2 (scan.cu) writes them
+  uint16_t* spool;
+  uint32_t snow;
+  uint32_t* sview;               // nullptr: no tracking
+  uint32_t* slog;
+  unsigned long long* slog_head;
+  uint32_t slog_mask;
 };
 
 __device__ __forceinline__ void red_or_g(uint32_t* addr, uint32_t v) {
@@ -97,6 +105,30 @@ __device__ __forceinline__ void seav_update(const sspd_params& p, uint32_t hip, 
 }
 __device__ __noinline__ void seav_update_ool(const sspd_params& p, uint32_t hip, uint32_t oip, uint32_t* seav) {
   seav_update(p, hip, oip, seav);
+}
+
+// Sliding SEAV half of one sampled packet (sliding.py:156-185, as K2's
+// scan_sliding_u16_fast_kernel): u16 stamp `now` into its SR slots, and with
+// tracking the view bit + the slot's log entry at ring position lpos + i.
+__device__ __forceinline__ void seav_stamp(const sspd_params& p, const Plan& P, uint32_t hip, uint32_t oip,
+                                           unsigned long long lpos) {
+  const uint32_t bit = (uint32_t)hash_range(oip, p.seed_h2, p.div_g);
+  const uint64_t rp = hip & ((1u << p.r) - 1u);
+  const uint64_t lp = ((uint64_t)hip >> p.r) & ((1ull << p.lp_bits) - 1ull);
+  for (uint32_t i = 0; i < p.sr; ++i) {
+    const uint32_t col = index_of(lp, p.isb[i], p.ibn[i], p.lp_bits);
+    const uint64_t reg = rp * p.sc[i] + col;
+    const uint64_t slot = p.slot_row_base[i] + reg * p.g + bit;
+    P.spool[slot] = (uint16_t)P.snow;
+    if (P.sview) {
+      const uint64_t vbit = (p.seav_row_off[i] + reg * p.reg_bytes) * 8 + bit;
+      atomicOr(P.sview + (vbit >> 5), 1u << (vbit & 31));
+      P.slog[(lpos + i) & P.slog_mask] = (uint32_t)slot;
+    }
+  }
+}
+__device__ __noinline__ void seav_stamp_ool(const sspd_params& p, const Plan& P, uint32_t hip, uint32_t oip) {
+  seav_stamp(p, P, hip, oip, P.sview ? atomicAdd(P.slog_head, (unsigned long long)p.sr) : 0ull);
 }
 
 // Staging row full (rare): the packet's LR bits as direct L2 reds (exact).
@@ -226,7 +258,7 @@ enum : int { kInline = 0, kWarpLdg = 1, kWarpTma = 2, kWarpFlag = 3 };
 constexpr uint32_t kConsWarpsLdg = 8;  // measured: 4 -> 5.48 ms, 6 -> 4.70, 8 -> 4.60, 10 -> 4.75
 constexpr uint32_t kConsWarpsTma = 6;
 
-template <bool kSeav, int HB, int kCons>
+template <int kSm, int HB, int kCons>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_bpart_kernel(const uint32_t* __restrict__ hips, const uint32_t* __restrict__ oips,
                       const __grid_constant__ sspd_params p, const __grid_constant__ Plan P, uint32_t* seav,
@@ -482,12 +514,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               direct_packet(P, hip, b, ldca);  // staging row full: direct (exact)
 #endif
-            if (kSeav && !(SSPD_BPART_DIAG & 8) && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
+            if (kSm && !(SSPD_BPART_DIAG & 8) && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
               const uint32_t qs = atomicAdd(sq_cnt, 1u);
               if (qs < kSeavQueue)
                 sq_base[qs] = make_uint2(hip, oip);
-              else
+              else if (kSm == 1)
                 seav_update_ool(p, hip, oip, seav);  // queue full (a skewed slice): apply now
+              else
+                seav_stamp_ool(p, P, hip, oip);
             }
           }
         }
@@ -531,14 +565,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         pbar();
       }
-      if (kSeav) {
+      if (kSm) {
         // the slice's sampled packets (0.78 % at tau = 7), queued per chunk
         // and applied here by consecutive producer lanes (full warps): a
         // per-tile pass left one warp updating while the others waited at
-        // the tile barrier (-0.3 ms per config-2 window)
+        // the tile barrier (-0.3 ms per config-2 window).  Sliding stamps
+        // with tracking reserve the chunk's log run with one atomic.
         pbar();
         const uint32_t nq = min(sq_cnt[0], kSeavQueue);
-        for (uint32_t i = tid; i < nq; i += nprod) seav_update(p, sq_base[i].x, sq_base[i].y, seav);
+        unsigned long long* lbase = reinterpret_cast<unsigned long long*>(sq_cnt + 2);
+        if (kSm == 2 && P.sview) {
+          if (tid == 0) *lbase = nq ? atomicAdd(P.slog_head, (unsigned long long)nq * p.sr) : 0ull;
+          pbar();
+        }
+        for (uint32_t i = tid; i < nq; i += nprod) {
+          if (kSm == 1)
+            seav_update(p, sq_base[i].x, sq_base[i].y, seav);
+          else
+            seav_stamp(p, P, sq_base[i].x, sq_base[i].y, P.sview ? *lbase + (unsigned long long)i * p.sr : 0ull);
+        }
         pbar();
         if (tid == 0) sq_cnt[0] = 0;
       }
@@ -684,23 +729,24 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   return true;
 }
 
-template <bool kSeav, int kCons>
+template <int kSm, int kCons>
 static void* kernel_hb(int hb) {
   switch (hb) {
-    case 0: return (void*)scan_bpart_kernel<kSeav, 0, kCons>;
-    case 1: return (void*)scan_bpart_kernel<kSeav, 1, kCons>;
-    case 2: return (void*)scan_bpart_kernel<kSeav, 2, kCons>;
-    default: return (void*)scan_bpart_kernel<kSeav, 3, kCons>;
+    case 0: return (void*)scan_bpart_kernel<kSm, 0, kCons>;
+    case 1: return (void*)scan_bpart_kernel<kSm, 1, kCons>;
+    case 2: return (void*)scan_bpart_kernel<kSm, 2, kCons>;
+    default: return (void*)scan_bpart_kernel<kSm, 3, kCons>;
   }
 }
 
-template <bool kSeav>
+template <int kSm>
 static void* kernel_for(int hb, int cons) {
+  if (kSm == 2) return cons == kInline ? kernel_hb<2, kInline>(hb) : kernel_hb<2, kWarpLdg>(hb);
   switch (cons) {
-    case kWarpTma: return kernel_hb<kSeav, kWarpTma>(hb);
-    case kWarpLdg: return kernel_hb<kSeav, kWarpLdg>(hb);
-    case kWarpFlag: return kernel_hb<kSeav, kWarpFlag>(hb);
-    default: return kernel_hb<kSeav, kInline>(hb);
+    case kWarpTma: return kernel_hb<kSm == 2 ? 0 : kSm, kWarpTma>(hb);
+    case kWarpLdg: return kernel_hb<kSm, kWarpLdg>(hb);
+    case kWarpFlag: return kernel_hb<kSm == 2 ? 0 : kSm, kWarpFlag>(hb);
+    default: return kernel_hb<kSm, kInline>(hb);
   }
 }
 
@@ -734,7 +780,7 @@ uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk) {
 // Launch; SSPD_ERR_CONFIG when not applicable (the caller tries K1p).
 int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
                       uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream,
-                      bool dst_zero) {
+                      bool dst_zero, const SlideSeavSink* slide) {
   int dev, sms, max_smem, coop = 0;
   bpart::device_limits(dev, sms, max_smem);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -745,6 +791,12 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   int cons = 0;
   if (!bpart::plan(p, n, chunk, sms, max_smem, P, smem, need, hb, cons)) return SSPD_ERR_CONFIG;
   if (!scratch || scratch_bytes < need) return SSPD_ERR_CAPACITY;
+  P.spool = nullptr, P.snow = 0, P.sview = nullptr, P.slog = nullptr, P.slog_head = nullptr, P.slog_mask = 0;
+  if (slide) {
+    P.spool = slide->pool, P.snow = slide->now, P.sview = slide->view, P.slog = slide->log;
+    P.slog_head = slide->log_head, P.slog_mask = slide->log_mask;
+    if (cons != bpart::kInline) cons = bpart::kWarpLdg;
+  }
   P.dst_zero = dst_zero ? 1u : 0u;
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
@@ -757,7 +809,7 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
               (P.chunk & 3u) == 0)
                  ? 1u
                  : 0u;
-  void* kern = seav ? bpart::kernel_for<true>(hb, cons) : bpart::kernel_for<false>(hb, cons);
+  void* kern = slide ? bpart::kernel_for<2>(hb, cons) : seav ? bpart::kernel_for<1>(hb, cons) : bpart::kernel_for<0>(hb, cons);
   // attribute/occupancy answers only change with (kernel, smem, device)
   static void* c_kern = nullptr;
   static uint64_t c_smem = 0;
@@ -783,4 +835,41 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
   return check_launch();
 }
 
+
 }  // namespace sspd
+
+using namespace sspd;
+
+// One pass of a sliding slice (u16 stamps): the LDCA half into the slice's
+// dirty bitmap (K1b's fold, `dirty_fresh`: the bitmap holds only zeros) and
+// the SEAV half -- stamps of the sampled packets, with the optional view and
+// slot log -- applied from K1b's per-chunk sampled-packet queue.  The same
+// state as sspd_scan_partitioned(_fresh)(seav = NULL, ldca = dirty) followed
+// by sspd_scan_sliding_seav, in one launch instead of two (the second
+// re-read the slice and re-hashed every packet for its 0.78 % sample).
+// SSPD_ERR_CONFIG when K1b does not apply (the caller uses the two calls).
+extern "C" int sspd_scan_sliding_partitioned(const uint32_t* hips, const uint32_t* oips, uint64_t n,
+                                             const sspd_params* p, void* pool, uint32_t ts_bytes,
+                                             uint64_t now_wrapped, uint8_t* seav_view, uint32_t* log,
+                                             uint64_t log_entries, unsigned long long* log_head, uint8_t* dirty,
+                                             int dirty_fresh, void* scratch, uint64_t scratch_bytes, uint64_t chunk,
+                                             void* stream) {
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (ts_bytes != 2) return SSPD_ERR_CONFIG;
+  if (n == 0) return SSPD_OK;
+  if (!hips || !oips || !pool || !dirty) return SSPD_ERR_DATA;
+  SlideSeavSink sink{static_cast<uint16_t*>(pool), (uint32_t)(now_wrapped & 0xFFFFu), nullptr, nullptr, nullptr, 0u};
+  if (seav_view) {
+    if (!log || !log_head || log_entries == 0 || (log_entries & (log_entries - 1)) || log_entries > (1ull << 32) ||
+        (reinterpret_cast<uintptr_t>(seav_view) & 3u) || p->slot_total >= (1ull << 32))
+      return SSPD_ERR_DATA;
+    sink.view = reinterpret_cast<uint32_t*>(seav_view);
+    sink.log = log;
+    sink.log_head = log_head;
+    sink.log_mask = (uint32_t)(log_entries - 1);
+  }
+  if (scan_bpart_scratch(p, chunk) == 0) return SSPD_ERR_CONFIG;
+  return scan_bpart_launch(hips, oips, n, p, nullptr, dirty, scratch, scratch_bytes, chunk, stream, dirty_fresh != 0,
+                           &sink);
+}

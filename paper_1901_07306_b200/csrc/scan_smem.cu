@@ -504,12 +504,6 @@ static bool plan_partitioned(const sspd_params* p, uint64_t n, uint64_t chunk, i
   return true;
 }
 
-// K1b (scan_bpart.cu): the LDCA cut along its b axis, one 16-B entry per
-// packet; preferred whenever its plan applies.
-uint64_t scan_bpart_scratch(const sspd_params* p, uint64_t chunk);
-int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, const sspd_params* p, uint8_t* seav,
-                      uint8_t* ldca, void* scratch, uint64_t scratch_bytes, uint64_t chunk, void* stream,
-                      bool dst_zero = false);
 
 }  // namespace sspd
 

@@ -612,12 +612,13 @@ class SlidingDetector:
             # + tracking) with K2 restricted to the sampled packets
             if iv is not None:
                 self._iv_check(iv)
-            self._scan_dirty_partitioned(h, o, dfr.dirty_ptr(), fresh=dfr.fresh)
-            call("sspd_scan_sliding_seav", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
-                 pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
-                 None if iv is None else iv["view"].device_buffer().data_ptr(),
-                 None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
-                 None if iv is None else iv["meta"].data_ptr(), stream_ptr())
+            if not self._scan_slice_fused(h, o, dfr, iv, pool):
+                self._scan_dirty_partitioned(h, o, dfr.dirty_ptr(), fresh=dfr.fresh)
+                call("sspd_scan_sliding_seav", h.data_ptr(), o.data_ptr(), h.numel(), self._params,
+                     pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(), cap,
+                     None if iv is None else iv["view"].device_buffer().data_ptr(),
+                     None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
+                     None if iv is None else iv["meta"].data_ptr(), stream_ptr())
             dfr.mark_scanned()
         elif iv is not None or dfr is not None:
             if iv is not None:
@@ -653,6 +654,47 @@ class SlidingDetector:
 
             ok = self._k1b_ok = int(lib().sspd_scan_partitioned_variant(self._params, 0)) > 0
         return ok
+
+    def _part_scratch_for(self, n: int, device):
+        import torch
+
+        from ._abi import lib
+
+        chunk = -(-n // 4) * 4
+        need = int(lib().sspd_scan_partitioned_scratch(self._params, chunk))
+        buf = getattr(self, "_part_scratch", None)
+        if buf is None or buf.numel() < need:
+            buf = self._part_scratch = torch.empty(need, dtype=torch.uint8, device=device)
+        return buf, chunk
+
+    def _scan_slice_fused(self, h, o, dfr, iv, pool) -> bool:
+        """Both halves of the slice in one K1b launch (LDCA half -> the
+        slice's dirty bitmap, SEAV stamps from the sampled-packet queue);
+        False when it does not apply (the caller then runs K1b + K2's SEAV
+        half).  env SSPD_SLIDE_FUSED=0 disables it."""
+        from ._abi import ERR_CONFIG, check, lib
+        from ._device import stream_ptr
+
+        if pool.ts_bytes != 2 or os.environ.get("SSPD_SLIDE_FUSED", "1") == "0":
+            return False
+        ok = getattr(self, "_k1b_fused_ok", None)
+        if ok is None:
+            ok = self._k1b_fused_ok = int(lib().sspd_scan_partitioned_variant(self._params, 0)) == 2
+        if not ok:
+            return False
+        n = int(h.numel())
+        buf, chunk = self._part_scratch_for(n, h.device)
+        rc = lib().sspd_scan_sliding_partitioned(
+            h.data_ptr(), o.data_ptr(), n, self._params, pool._buf.data_ptr(), pool.ts_bytes, pool._wrapped_now(),
+            None if iv is None else iv["view"].device_buffer().data_ptr(),
+            None if iv is None else iv["log"].data_ptr(), 0 if iv is None else iv["log"].numel(),
+            None if iv is None else iv["meta"].data_ptr(), dfr.dirty_ptr(), 1 if dfr.fresh else 0,
+            buf.data_ptr(), buf.numel(), chunk, stream_ptr())
+        if rc == ERR_CONFIG:
+            self._k1b_fused_ok = False
+            return False
+        check(rc, "sspd_scan_sliding_partitioned")
+        return True
 
     def _scan_dirty_partitioned(self, h, o, dirty_ptr: int, fresh: bool = False):
         import torch

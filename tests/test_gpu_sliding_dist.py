@@ -465,8 +465,9 @@ def test_deferred_ldca_stamps_equal_direct_stamps(cuda):
 @pytest.mark.gpu
 @pytest.mark.parametrize("async_detect", [False, True])
 @pytest.mark.parametrize("geom", [(4096, 4, 256), (64, 3, 37), (4096, 4, 256, "misaligned"),
-                                  (4096, 8, 256, "partitioned")],
-                         ids=["ldca16B", "ldca_pad8_nonpow2", "misaligned_inputs", "k1b_dirty_bitmaps"])
+                                  (4096, 8, 256, "partitioned"), (4096, 8, 256, "partitioned_unfused")],
+                         ids=["ldca16B", "ldca_pad8_nonpow2", "misaligned_inputs", "k1b_dirty_bitmaps",
+                              "k1b_dirty_bitmaps_two_launches"])
 def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom, monkeypatch):
     """Ring mode of the deferred LDCA stamps (the LDCA view as a two-stack
     sliding-window OR of per-slice bitmaps, stamps folded lazily) against
@@ -478,16 +479,19 @@ def test_ldca_ring_window_or_equals_direct_stamps(cuda, async_detect, geom, monk
     by the padded stride, not the LDCA size) and lc = 37 (the generic u16
     scan must fill the dirty bitmaps).  `misaligned_inputs`: device hips /
     oips at different 16-B offsets (no fast path either).
-    `k1b_dirty_bitmaps`: every slice's LDCA half recorded by the partitioned
-    scan K1b into the slice's bitmap, the SEAV half by K2."""
+    `k1b_dirty_bitmaps`: every slice in ONE launch of the partitioned scan
+    K1b (LDCA half into the slice's bitmap, SEAV stamps + view + log from
+    its sampled-packet queue, sspd_scan_sliding_partitioned);
+    `_two_launches`: K1b for the LDCA half, K2 for the SEAV half."""
     import torch
 
     from paper_1901_07306_b200 import DetectorParams, SlidingDetector
 
     k, lr, lc = geom[:3]
     misaligned = len(geom) > 3 and geom[3] == "misaligned"
-    if len(geom) > 3 and geom[3] == "partitioned":  # the LDCA half of every slice through K1b
+    if len(geom) > 3 and geom[3].startswith("partitioned"):  # the LDCA half of every slice through K1b
         monkeypatch.setenv("SSPD_SLIDE_PARTITIONED", "1")
+        monkeypatch.setenv("SSPD_SLIDE_FUSED", "0" if geom[3].endswith("unfused") else "1")
     params = DetectorParams(theta=256, r=8, k=k, lr=lr, lc=lc, design_n=2e5)
     w = 129
     with warnings.catch_warnings():
