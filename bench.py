@@ -606,7 +606,7 @@ def run_gpu(args) -> dict | None:
                    "ceiling_gpps_scan_launch_shape": round(hash_pps[1] / 1e9, 3) if hash_pps.get(1) else None,
                    "achieved_gpps": round(scan_pps / 1e9, 3), "frac": round(scan_pps / ceiling, 4),
                    "note": ("streaming the same pairs and computing H3 % k, the H1 test and the LR row hashes "
-                            "(10 SplitMix64 per packet) with no sketch update, at full occupancy (2 x 1,024 "
+                            "(10 SplitMix64 per packet, the scans' 32-bit-half form, rows unrolled) with no sketch update, at full occupancy (2 x 1,024 "
                             "threads per SM); the scan adds the shared-memory partition exchange to this floor")}
 
     value = world * n / (ms * 1e-3) / 1e6
