@@ -31,6 +31,7 @@
 // commutative and idempotent.  SEAV updates (0.78 % of packets at tau = 7)
 // are queued per tile and applied by all lanes as direct reds (as K1p).
 #include <algorithm>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -46,7 +47,7 @@ constexpr uint32_t kThreads = 1024;
 constexpr uint32_t kPkt = 4;  // packets per thread per tile (one uint4 of hips + oips)
 constexpr uint32_t kTile = kThreads * kPkt;
 constexpr uint32_t kLR = 8;
-constexpr uint32_t kSeavQueue = 2048;  // sampled packets per CTA per chunk (expected ~570 at tau = 7)
+constexpr uint32_t kSeavQueue = 1024;  // sampled packets per CTA per chunk (expected ~570 at tau = 7)
 constexpr uint32_t kMaxSrc = 256;     // producer CTAs (SMs) the plan supports
 
 struct Plan {
@@ -58,7 +59,10 @@ struct Plan {
   uint32_t lowm;         // rw - 1: half 0 without the bit position
   uint32_t bsh_shift;    // log2(rw): where half 0 keeps b & 31
   uint32_t rowc[4];      // per entry word: the row byte offsets of its halves (4*i*rw << 16*(i&1))
-  uint32_t stage_slots;  // 16-B entries per destination per tile
+  uint32_t stage_slots;  // 16-B entries per destination per tile (owner CTAs)
+  uint32_t stage_slots_pure;  // dbuf: the same for pure producers (their staging takes the partition's room)
+  uint32_t dbuf;         // 1: two staging buffers, one producer barrier per tile
+  uint32_t cnt_off_words;  // dbuf: shared-memory word offset of cnt[2][nparts]
   uint32_t region_cap;   // entries per (src, dst) region per chunk
   uint32_t w_owner, w_other;  // producer slice weights (owners vs pure producers)
   uint64_t chunk;        // packets per chunk
@@ -265,9 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                       uint32_t* ldca) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* part = smem;
-  uint4* stage = reinterpret_cast<uint4*>(smem + P.part_words);  // part_words % 4 == 0
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
-  uint32_t* sq_cnt = cnt + P.nparts;                        // [1] (+3 pad); nparts % 4 == 0
+  const bool owner = blockIdx.x < P.nparts;
+  // staging: [part | stage[np][S]] or, double-buffered (P.dbuf), owners
+  // [part | stage[2][np][S_o]] and pure producers [stage[2][np][S_p]] (no
+  // partition), cnt[2][np] at a common offset
+  uint4* const stage = reinterpret_cast<uint4*>(smem + (P.dbuf && !owner ? 0u : P.part_words));
+  const uint32_t slots = P.dbuf && !owner ? P.stage_slots_pure : P.stage_slots;
+  uint32_t* cnt = P.dbuf ? smem + P.cnt_off_words
+                         : reinterpret_cast<uint32_t*>(stage + (size_t)P.nparts * P.stage_slots);
+  uint32_t* sq_cnt = cnt + (P.dbuf ? 2u : 1u) * P.nparts;  // [1] (+3 pad); nparts % 4 == 0
   uint2* sq_base = reinterpret_cast<uint2*>(sq_cnt + 4);  // [kSeavQueue]
   uint4* ring = reinterpret_cast<uint4*>(sq_base + kSeavQueue);  // kWarpTma: [kRing][kSlot]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(ring + kRing * kSlot);
@@ -277,7 +287,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = kThreads >> 5;
   const uint32_t np = P.nparts, ns = P.nsrc;
-  const bool owner = self < np;
   constexpr uint32_t kHMask = (1u << HB) - 1u;
   // producer threads of this CTA and their tile (packets per tile barrier)
   constexpr bool kSpec = kCons != kInline;
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   for (uint32_t i = tid; i < P.part_words; i += kThreads) part[i] = 0;
-  for (uint32_t i = tid; i < np; i += kThreads) cnt[i] = 0;
+  for (uint32_t i = tid; i < (P.dbuf ? 2u : 1u) * np; i += kThreads) cnt[i] = 0;
   // flush role, fixed for the launch: group q = tid >> gshift of G threads
   // copies destination q's staging row (one pass covers every destination)
   uint32_t gs = P.gshift;
@@ -310,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   uint32_t ring_s = 0, ring_ph = 0;  // consumer pipeline position (kept across chunks)
+  uint32_t tb = 0;                   // dbuf: the staging buffer of the current tile (kept across chunks)
 #if SSPD_BPART_DIAG
   uint32_t diag = 0;
 #endif
@@ -474,11 +484,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // this thread's flush destination: region (self -> fq) of bucket bb,
       // filled up to `pos` (identical in the G lanes of the group)
       uint4* const dstq = P.buckets + ((size_t)bb * np + fq) * P.qstride + (size_t)self * P.region_cap;
-      const uint4* const srcq = stage + fq * P.stage_slots;
       uint32_t pos = 0;
       uint32_t nh[kPkt], no[kPkt];
       fetch(lo + (uint64_t)tid * kPkt, nh, no);
-      for (uint64_t base = lo; base < hi; base += tile) {
+      // one tile; TB = its staging buffer (compile-time: the buffer offsets fold
+      // into the addresses); single-buffered launches always use buffer 0
+      auto tile_body = [&](uint64_t base, auto tb_c) {
+        constexpr uint32_t TB = decltype(tb_c)::value;
         uint32_t ch[kPkt], co[kPkt];
 #pragma unroll
         for (uint32_t e = 0; e < kPkt; ++e) {
@@ -508,11 +520,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if SSPD_BPART_DIAG & 2
             diag ^= ent.x ^ ent.y ^ ent.z ^ ent.w ^ q;  // timing diagnostic: no staging
 #else
-            const uint32_t slot = atomicAdd(&cnt[q], 1u);
-            if (slot < P.stage_slots)
-              stage[q * P.stage_slots + slot] = ent;
+            const uint32_t slot = atomicAdd(&cnt[TB * np + q], 1u);
+            if (slot < slots)
+              stage[(TB * np + q) * slots + slot] = ent;
             else
-              direct_packet(P, hip, b, ldca);  // staging row full: direct (exact)
+              direct_entry<HB>(P, q, ent, ldca);  // staging row full: direct (exact)
 #endif
             if (kSm && !(SSPD_BPART_DIAG & 8) && (mix64_lo_fast(oip, P.ss[1]) & P.tau_mask) == 0u) {
               const uint32_t qs = atomicAdd(sq_cnt, 1u);
@@ -525,7 +537,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        // dbuf: the previous tile's bulk copies (out of the other buffer,
+        // which the next tile writes) must have read shared memory before
+        // this barrier releases the producers
+        if (P.dbuf && flusher && gl == 0) bulk_wait_read();
         pbar();
+        const uint4* const srcq = stage + (TB * np + fq) * slots;
+        uint32_t* const cntq = cnt + TB * np + fq;
         // flush: the G = 2^gshift threads of group fq copy destination fq's
         // run of 16-B entries into this CTA's own region of that bucket (no
         // global atomics); `pos` lives in registers, identical in the group
@@ -534,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // the run must have been read out of shared memory before the next
           // tile's staging writes: wait_group.read ahead of the barrier
           if (flusher && gl == 0) {
-            const uint32_t m = min(cnt[fq], P.stage_slots);
+            const uint32_t m = min(*cntq, slots);
             const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
             if (fit) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging writes -> TMA reads
@@ -543,12 +561,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (uint32_t s2 = fit; s2 < m; ++s2) direct_entry<HB>(P, fq, srcq[s2], ldca);  // region full (exact)
             pos += fit;
-            cnt[fq] = 0;
-            bulk_wait_read();
+            *cntq = 0;
+            if (!P.dbuf) bulk_wait_read();
           }
           if (flusher) pos = __shfl_sync(__activemask(), pos, 0, G);  // keep the group's copies equal
         } else if (flusher) {
-          const uint32_t m = min(cnt[fq], P.stage_slots);
+          const uint32_t m = min(*cntq, slots);
           const uint32_t fit = pos < P.region_cap ? min(m, P.region_cap - pos) : 0u;
           uint4* dst = dstq + pos;
           uint32_t s = gl;
@@ -561,9 +579,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (s = fit + gl; s < m; s += G) direct_entry<HB>(P, fq, srcq[s], ldca);  // region full (exact)
           pos += fit;
           __syncwarp();  // the group's lanes read cnt[fq] before it is reset
-          if (gl == 0) cnt[fq] = 0;
+          if (gl == 0) *cntq = 0;
         }
-        pbar();
+        if (!P.dbuf) pbar();
+      };
+      for (uint64_t base = lo; base < hi;) {
+        if (tb == 0 || !P.dbuf) {
+          tile_body(base, std::integral_constant<uint32_t, 0>{});
+        } else {
+          tile_body(base, std::integral_constant<uint32_t, 1>{});
+        }
+        tb ^= P.dbuf;
+        base += tile;
       }
       if (kSm) {
         // the slice's sampled packets (0.78 % at tau = 7), queued per chunk
@@ -662,6 +689,9 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
     const double mean = (double)kTile / np;
     P.stage_slots = (uint32_t)(mean + 4.0 * __builtin_sqrt(mean) + 8.0);
   }
+  P.stage_slots_pure = P.stage_slots;
+  P.dbuf = 0;
+  P.cnt_off_words = 0;
   smem = 4ull * P.part_words + 16ull * np * P.stage_slots + 4ull * np + 16 + 8ull * kSeavQueue;
   // consumer mode (SSPD_BPART_CONS = 0 in line / 1 warp-specialised, global
   // loads (default) / 2 warp-specialised, TMA ring)
@@ -690,6 +720,31 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   P.tma_flush = 1;
   if (const char* e = getenv("SSPD_BPART_FLUSH_TMA")) P.tma_flush = atoi(e) != 0;
   if (cons == kWarpFlag && !P.tma_flush) cons = kWarpLdg;  // flags are released by the one flushing lane
+  // double-buffered staging (warp-specialised TMA-flush launches): the
+  // flush of tile t overlaps the staging of tile t+1, one producer barrier
+  // per tile instead of two.  Two buffers fit because the rows are sized to
+  // each role's tile -- owners stage (1024 - 32 * cons_warps) * 4 packets
+  // per tile, pure producers 4,096 but hold no partition -- with a 2.5-3
+  // sigma margin (a full row sends the entry straight to L2, exact)
+  if (cons == kWarpLdg && P.tma_flush && !(getenv("SSPD_BPART_DB") && atoi(getenv("SSPD_BPART_DB")) == 0)) {
+    const double mo = (double)(kThreads - 32u * P.cons_warps) * kPkt / np, mp = (double)kTile / np;
+    const uint64_t tail = 4ull * 2 * np + 16 + 8ull * kSeavQueue;
+    const int64_t room_o = (int64_t)max_smem - (int64_t)tail - 4ll * P.part_words;
+    uint32_t so = (uint32_t)(mo + 3.0 * __builtin_sqrt(mo) + 2.0);
+    uint32_t sp = (uint32_t)(mp + 3.0 * __builtin_sqrt(mp) + 2.0);
+    if (room_o > 0) so = std::min<uint32_t>(so, (uint32_t)(room_o / (32ll * np)));
+    sp = std::min<uint32_t>(sp, (uint32_t)(((int64_t)max_smem - (int64_t)tail) / (32ll * np)));
+    const uint64_t end_o = 4ull * P.part_words + 32ull * np * so, end_p = 32ull * np * sp;
+    const uint64_t cnt_off = (std::max(end_o, end_p) + 15) & ~15ull;
+    if (room_o > 0 && so >= mo + 2.0 * __builtin_sqrt(mo) && sp >= mp + 2.5 * __builtin_sqrt(mp) &&
+        cnt_off + tail <= (uint64_t)max_smem) {
+      P.dbuf = 1;
+      P.stage_slots = so;
+      P.stage_slots_pure = sp;
+      P.cnt_off_words = (uint32_t)(cnt_off / 4);
+      smem = cnt_off + tail;
+    }
+  }
   // producer slice weights: pure producers hash with all 32 warps; owners
   // with 28 (spec) or pause to consume (in line)
   P.w_owner = 64;

@@ -236,6 +236,8 @@ PART_CASES = {
     "cons_flags_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
     # K1b flush by threads (16-B stores) instead of TMA bulk stores
     "flush_threads_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
+    # K1b with ONE staging buffer (two producer barriers per tile) instead of two
+    "single_buffer_skewed_oip": (dict(theta=1024, r=12, k=8192, lr=8, lc=1024), 2),
 }
 
 
@@ -257,6 +259,8 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
         monkeypatch.setenv("SSPD_BPART_CONS", {"cons_inline": "0", "cons_flags_skewed_oip": "3"}.get(case, "2"))
     if case.startswith("flush_threads"):
         monkeypatch.setenv("SSPD_BPART_FLUSH_TMA", "0")
+    if case.startswith("single_buffer"):
+        monkeypatch.setenv("SSPD_BPART_DB", "0")
     dp = DetectorParams(design_n=1e6, **geom)
     _, _, p = params_block(dp)
     rng = np.random.default_rng(77)
@@ -266,7 +270,8 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     if case in ("skewed", "legacy_skewed"):
         hips[: n // 2] = 0xC0A80001  # one host: its 8 cells take half of all updates
         hips[n // 2: n // 2 + 100_000] = 0x0A000001
-    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "cons_flags_skewed_oip"):
+    if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "cons_flags_skewed_oip",
+                "single_buffer_skewed_oip"):
         oips[: n // 2] = 0x08080808  # one opposite IP: one b, so one K1b partition
         oips[n // 2: n // 2 + 100_000] = 0x01010101
         perm = rng.permutation(n)
@@ -278,7 +283,7 @@ def test_partitioned_scan_vs_oracle(cuda, oracle, case, monkeypatch):
     if case == "tiny_chunks":
         st.partitioned_chunk = 1 << 14
     if case in ("skewed_oip", "cons_tma_skewed_oip", "flush_threads_skewed_oip", "cons_flags_skewed_oip",
-                "k16384_hb2"):
+                "single_buffer_skewed_oip", "k16384_hb2"):
         st.partitioned_chunk = 1 << 20  # several chunks: the warp-specialised drain overlaps production
     st.process_batch(hips[: n // 3], oips[: n // 3])
     st.process_batch(hips[n // 3:], oips[n // 3:])
