@@ -6,7 +6,7 @@
 #   `roofline.traffic`, the config-2 launch list and an `ncu --set full`
 #   capture of K1b.  Outputs land in gpurun_out/round/.
 set -u
-OUT=gpurun_out/round
+OUT=${OUT:-gpurun_out/round}
 mkdir -p "$OUT"
 export PATH=/usr/local/cuda/bin:$PATH
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
@@ -29,3 +29,7 @@ echo "launches=$?"
 # full capture of the dominant kernel
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:scan_bpart -c 1 -f -o "$OUT/k1b_full" \
   python tools/sweep_k1p.py --reps 1 "" > /dev/null 2>&1; echo "ncu_full=$?"
+# per-slide kernels of the sliding trace (slides ~50-75 of the warm-up step)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k 'regex:sspd::' -s 600 -c 300 --csv \
+  --log-file "$OUT/launches_config4.csv" python bench.py --config 4 --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1; echo "launches_c4=$?"
+
