@@ -79,6 +79,7 @@ struct Plan {
   uint32_t cons_warps;   // kWarpLdg / kWarpTma: consumer warps of an owner CTA
   uint32_t tma_flush;    // 1: staging runs leave shared memory as TMA bulk stores
   uint32_t dst_zero;     // 1: the LDCA holds only zeros on entry: the fold stores, no read-modify-write
+  uint32_t fold_red;     // 1: the fold ORs with red.or (fire and forget), 0: load-OR-store
   uint32_t* ready;       // kWarpFlag: [dst][src] = chunks of src published to dst (zeroed per launch)
   uint32_t* drained;     // kWarpFlag: [dst] = chunks dst has drained
   uint32_t slice_off[kMaxSrc + 1];  // producer s starts at chunk start + slice_off[s] (full chunks)
@@ -631,22 +632,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   // fold the partition into the global LDCA: word (row, cell, j) of
   // partition q is global word (row*lc + cell)*k/32 + q*2^HB + j.  After the
   // last barrier no direct reds are in flight and the partitions are
-  // disjoint, so a plain read-modify-write is exact -- and into an all-zero
-  // destination (a fresh sliding dirty bitmap) a plain store.
+  // disjoint, so a fire-and-forget red.or (or a load-OR-store,
+  // SSPD_BPART_FOLD_RED=0) is exact -- and into an all-zero
+  // destination (a fresh sliding dirty bitmap) a plain store.  Each CTA
+  // starts its walk at a different cell (rotated by part_words / nparts
+  // words): the 2^HB words of one cell that the partitions own share 128-B
+  // lines, and walking in lockstep sent all owners to the same lines at once
+  // (a 1.8 M-packet launch spent ~40 of its 110 us in this loop, as
+  // load-OR-store round trips queued on those lines).
 #if SSPD_BPART_DIAG
   if (diag == 0x9E3779B9u) ldca[tid] = diag;  // keep the diagnostic work alive
 #endif
   if (!owner) return;
   __syncthreads();
   const uint32_t rshift = 31 - __clz(P.row_words);  // row_words is a power of two
-  for (uint32_t i = tid; i < P.part_words; i += kThreads) {
+  const uint32_t rot = self * (P.part_words / P.nparts), wmask = P.part_words - 1u;
+  for (uint32_t k = tid; k < P.part_words; k += kThreads) {
+    const uint32_t i = (k + rot) & wmask;
     const uint32_t v = part[i];
     if (v) {
       const uint32_t row = i >> rshift, within = i & (P.row_words - 1u);
       const uint64_t cell = (uint64_t)row * P.lc + (within >> HB);
       uint32_t* dst = ldca + cell * P.kw + ((uint64_t)self << HB) + (within & kHMask);
       if (P.dst_zero)
-        *dst = v;
+        __stcg(dst, v);
+      else if (P.fold_red)
+        red_or_g(dst, v);
       else
         *dst |= v;
     }
@@ -853,6 +864,7 @@ int scan_bpart_launch(const uint32_t* hips, const uint32_t* oips, uint64_t n, co
     if (cons != bpart::kInline) cons = bpart::kWarpLdg;
   }
   P.dst_zero = dst_zero ? 1u : 0u;
+  P.fold_red = !(getenv("SSPD_BPART_FOLD_RED") && atoi(getenv("SSPD_BPART_FOLD_RED")) == 0);
   P.buckets = static_cast<uint4*>(scratch);
   P.counts = reinterpret_cast<uint32_t*>(P.buckets + 2ull * P.nparts * P.qstride);
   P.ready = P.counts + 2ull * P.nparts * P.nsrc;

@@ -51,6 +51,20 @@ __device__ __forceinline__ uint32_t v_sel(uint32_t key, const SplitSeed& s, uint
   return z2l ^ __funnelshift_r(z2l, z2h, 31);
 }
 
+__host__ __device__ constexpr SplitSeed split_seed_c(uint64_t seed) {
+  const uint32_t lo = (uint32_t)seed, hg = (uint32_t)(seed >> 32) + (uint32_t)(kGolden >> 32), h1 = hg + 1u;
+  const uint32_t t0 = (hg ^ (hg >> 30)) * (uint32_t)kMixA, t1 = (h1 ^ (h1 >> 30)) * (uint32_t)kMixA;
+  return SplitSeed{lo, hg, t1 - t0, t0 - hg * (t1 - t0)};
+}
+// compile-time seeds (the upper bound of removing every constant-bank load)
+constexpr uint64_t kSeedsC[10] = {0x9E3779B97F4A7C15ull * 3, 0x1234567ull, 0xE8AB9E9A226DF370ull, 0xD46EE1CCFC7B25FCull,
+                                  0x638C62F5C9C1EAD8ull, 0x4EC976611A9CC2F7ull, 0xA8285392D2F048D4ull,
+                                  0xAF77364105F4D5A6ull, 0xDF96F642FAF5ACBFull, 0x8AFCC3A11DFFAAD5ull};
+template <int I>
+__device__ __forceinline__ uint32_t h_imm(uint32_t key) {
+  constexpr SplitSeed s = split_seed_c(kSeedsC[I]);
+  return mix64_lo_fast(key, s.lo, s.hg, s.d, s.e);
+}
 template <int V>
 __global__ void __launch_bounds__(1024, 2) kern(const uint4* __restrict__ h4, const uint4* __restrict__ o4, uint64_t nq,
                                                 const __grid_constant__ Seeds S, uint32_t* sink, uint4 tt) {
@@ -59,6 +73,32 @@ __global__ void __launch_bounds__(1024, 2) kern(const uint4* __restrict__ h4, co
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
     const uint4 hv = __ldcs(h4 + q), ov = __ldcs(o4 + q);
     const uint32_t h[4] = {hv.x, hv.y, hv.z, hv.w}, o[4] = {ov.x, ov.y, ov.z, ov.w};
+    if (V == 4) {  // seeds as immediates
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t v = h_imm<0>(o[e]) & 8191u;
+        v ^= (h_imm<1>(o[e]) & 127u) == 0u ? 0x80000000u : 0u;
+        v += (h_imm<2>(h[e]) & 1023u) << 0; v += (h_imm<3>(h[e]) & 1023u) << 1;
+        v += (h_imm<4>(h[e]) & 1023u) << 2; v += (h_imm<5>(h[e]) & 1023u) << 3;
+        v += (h_imm<6>(h[e]) & 1023u) << 4; v += (h_imm<7>(h[e]) & 1023u) << 5;
+        v += (h_imm<8>(h[e]) & 1023u) << 6; v += (h_imm<9>(h[e]) & 1023u) << 7;
+        acc ^= v;
+      }
+      continue;
+    }
+    if (V == 5) {  // rows outer, packets inner: each seed's constants loaded once per 4 packets
+      uint32_t v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = mix64_lo_fast(o[e], S.ss[0]) & 8191u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] ^= (mix64_lo_fast(o[e], S.ss[1]) & 127u) == 0u ? 0x80000000u : 0u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] += (mix64_lo_fast(h[e], S.ss[2 + i]) & 1023u) << i;
+      acc ^= v[0] ^ v[1] ^ v[2] ^ v[3];
+      continue;
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t v;
@@ -97,11 +137,11 @@ int main() {
     delete[] tmp;
   }
   Seeds S;
-  for (int i = 0; i < 10; ++i) S.ss[i] = split_seed(mix64(0x1234567ull * (i + 1)));
+  for (int i = 0; i < 10; ++i) S.ss[i] = split_seed(kSeedsC[i]);
   uint32_t* hs = new uint32_t[grid * 1024];
   uint64_t ref = 0;
-  const char* names[4] = {"old_64bit_split", "fast_mulhi", "fast_shf", "fast_sel"};
-  for (int v = 0; v < 4; ++v) {
+  const char* names[6] = {"old_64bit_split", "fast_mulhi", "fast_shf", "fast_sel", "fast_imm_seeds", "fast_rows_outer"};
+  for (int v = 0; v < 6; ++v) {
     auto launch = [&]() {
       const uint4* H4 = reinterpret_cast<const uint4*>(h);
       const uint4* O4 = reinterpret_cast<const uint4*>(o);
@@ -110,6 +150,8 @@ int main() {
       if (v == 1) kern<1><<<grid, 1024>>>(H4, O4, nq, S, sink, tt);
       if (v == 2) kern<2><<<grid, 1024>>>(H4, O4, nq, S, sink, tt);
       if (v == 3) kern<3><<<grid, 1024>>>(H4, O4, nq, S, sink, tt);
+      if (v == 4) kern<4><<<grid, 1024>>>(H4, O4, nq, S, sink, tt);
+      if (v == 5) kern<5><<<grid, 1024>>>(H4, O4, nq, S, sink, tt);
     };
     launch();
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
