@@ -626,15 +626,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     // chunk t produced everywhere; chunk t-1 consumed everywhere -- or, with
-    // point-to-point flags, only before the fold
-    if (kCons != kWarpFlag || t == nchunks) grid.sync();
+    // point-to-point flags, only before the fold.  No barrier after the last
+    // drain when the fold is a red.or: it commutes with every other CTA's
+    // direct reds, so each owner folds as soon as its own drain is done
+    if (t < nchunks ? kCons != kWarpFlag : !P.fold_red) grid.sync();
   }
   // fold the partition into the global LDCA: word (row, cell, j) of
   // partition q is global word (row*lc + cell)*k/32 + q*2^HB + j.  After the
   // last barrier no direct reds are in flight and the partitions are
-  // disjoint, so a fire-and-forget red.or (or a load-OR-store,
-  // SSPD_BPART_FOLD_RED=0) is exact -- and into an all-zero
-  // destination (a fresh sliding dirty bitmap) a plain store.  Each CTA
+  // disjoint, so a fire-and-forget red.or is exact (with
+  // SSPD_BPART_FOLD_RED=0, after a last grid barrier: a load-OR-store, or
+  // into an all-zero destination -- a fresh sliding dirty bitmap -- a plain
+  // store).  Each CTA
   // starts its walk at a different cell (rotated by part_words / nparts
   // words): the 2^HB words of one cell that the partitions own share 128-B
   // lines, and walking in lockstep sent all owners to the same lines at once
@@ -654,10 +657,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t row = i >> rshift, within = i & (P.row_words - 1u);
       const uint64_t cell = (uint64_t)row * P.lc + (within >> HB);
       uint32_t* dst = ldca + cell * P.kw + ((uint64_t)self << HB) + (within & kHMask);
-      if (P.dst_zero)
-        __stcg(dst, v);
-      else if (P.fold_red)
+      if (P.fold_red)
         red_or_g(dst, v);
+      else if (P.dst_zero)
+        __stcg(dst, v);
       else
         *dst |= v;
     }
@@ -762,10 +765,17 @@ static bool plan(const sspd_params* p, uint64_t n, uint64_t chunk, int sms, int 
   // measured with the TMA flush, 16-tile chunks: 64-70 -> 4.27 ms, 72-73 ->
   // 4.18, 74-76 -> 4.30-4.35, 82 -> 4.58 (slices are whole tiles, so the
   // optimum is a step, not a slope)
-  P.w_other = spec ? 72 : 80;
+  // in line (one chunk: everybody produces, then the owners drain) equal
+  // slices are best -- a 1.8 M-packet launch: 80 -> 54.6 us, 64 -> 49.1
+  P.w_other = spec ? 72 : 64;
   if (const char* e = getenv("SSPD_PART_WEIGHT")) P.w_other = (uint32_t)atoi(e);
-  const double share =
-      (double)std::max(P.w_owner, P.w_other) / ((double)np * P.w_owner + (double)(P.nsrc - np) * P.w_other);
+  // the largest producer's share of a chunk -- over the weights of BOTH
+  // consumer modes, so the scratch size a caller queries (which cannot know
+  // the batch size, and plans one chunk in line) covers every launch
+  auto share_of = [&](uint32_t wo) {
+    return (double)std::max(P.w_owner, wo) / ((double)np * P.w_owner + (double)(P.nsrc - np) * wo);
+  };
+  const double share = std::max({share_of(P.w_other), share_of(72), share_of(64)});
   const double rmean = (double)P.chunk * share / np;  // largest producer -> one destination
   P.region_cap = (uint32_t)(rmean + 6.0 * __builtin_sqrt(rmean) + 32.0);
   P.region_cap = (P.region_cap + 7u) & ~7u;  // regions start on 128-B lines

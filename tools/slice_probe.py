@@ -3,8 +3,9 @@ slice is ~1.8 M pairs), launches back to back (tuning probe, not a bench).
 
     [SSPD_B200_LIB=lib.so] python tools/slice_probe.py [--packets N] [--reps R] [--tag T] SETTING ...
 
-A SETTING is `chunk=C` (packets per chunk; 0 = the whole batch as one chunk)
-plus SSPD_* environment knobs, comma separated.  R launches of
+A SETTING is `chunk=C` (packets per chunk; 0 = the whole batch as one chunk),
+`fresh=1` (sspd_scan_partitioned_fresh: the fold stores into a zeroed
+buffer, as a sliding slice's dirty bitmap) plus SSPD_* environment knobs, comma separated.  R launches of
 sspd_scan_partitioned are issued on one stream between two CUDA events, so
 the mean excludes host launch gaps; the LDCA/SEAV bytes of every setting are
 compared with the first setting's.  Also prints the hash floor
@@ -57,6 +58,7 @@ def main():
     for setting in args.settings:
         kv = dict(x.split("=", 1) for x in setting.split(",") if x)
         chunk = int(kv.pop("chunk", "0")) or (-(-n // 4) * 4)
+        fresh = kv.pop("fresh", "0") == "1"  # sspd_scan_partitioned_fresh (a zeroed sliding dirty bitmap)
         old = {k: os.environ.get(k) for k in kv}
         os.environ.update(kv)
         try:
@@ -64,8 +66,9 @@ def main():
             scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
 
             def launch():
-                rc = lib().sspd_scan_partitioned(hips.data_ptr(), oips.data_ptr(), n, p, seav.data_ptr(),
-                                                 ldca.data_ptr(), scratch.data_ptr(), need, chunk, stream)
+                fn = lib().sspd_scan_partitioned_fresh if fresh else lib().sspd_scan_partitioned
+                rc = fn(hips.data_ptr(), oips.data_ptr(), n, p, seav.data_ptr(), ldca.data_ptr(), scratch.data_ptr(),
+                        need, chunk, stream)
                 assert rc == 0, rc
 
             seav.zero_()
