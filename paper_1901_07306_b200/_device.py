@@ -40,6 +40,48 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+_get_cur = getattr(torch._C, "_cuda_getCurrentStream", None)
+_set_cur = getattr(torch._C, "_cuda_setStream", None)
+
+
+def current_stream():
+    """torch.cuda.current_stream() without its lazy-init and device-index
+    lookups (per-slide host path: ~1 us instead of ~8)."""
+    if _get_cur is None or _cur_dev is None:
+        return torch.cuda.current_stream()
+    sid, di, dt = _get_cur(_cur_dev())
+    return torch.cuda.Stream(stream_id=sid, device_index=di, device_type=dt)
+
+
+class on_stream:
+    """`with torch.cuda.stream(s)` for a stream of the current device,
+    switching with the direct C accessors (the torch context manager
+    re-resolves the device index on entry and exit, ~10 us per use)."""
+
+    __slots__ = ("s", "prev")
+
+    def __init__(self, s):
+        self.s = s
+        self.prev = None
+
+    def __enter__(self):
+        s = self.s
+        if _get_cur is None or _set_cur is None:
+            self.prev = torch.cuda.current_stream()
+            torch.cuda.set_stream(s)
+            return
+        self.prev = _get_cur(s.device_index)
+        _set_cur(stream_id=s.stream_id, device_index=s.device_index, device_type=s.device_type)
+
+    def __exit__(self, *exc):
+        prev = self.prev
+        if isinstance(prev, tuple):
+            _set_cur(stream_id=prev[0], device_index=prev[1], device_type=prev[2])
+        else:
+            torch.cuda.set_stream(prev)
+        return False
+
+
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 

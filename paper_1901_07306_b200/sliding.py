@@ -584,9 +584,10 @@ class SlidingDetector:
 
         self._iv_check(iv)
         pool = self.pool
+        meta = iv["meta"]  # int64: the kernel takes &meta[1]
         call("sspd_materialize_seav_if", pool._buf.data_ptr(), pool.ts_bytes, self._params,
              pool._wrapped_now(), pool.window_slices, iv["view"].device_buffer().data_ptr(),
-             iv["meta"][1:].data_ptr(), stream_ptr())
+             meta.data_ptr() + meta.element_size(), stream_ptr())
         return iv["view"]
 
     @traced("observe")
@@ -775,7 +776,7 @@ class SlidingDetector:
         """Materialise (K4: SEAV registers + packed LDCA) -> fused finalize
         (K5 restore, sort, K6 filter, compaction; one host round trip)
         (sliding.py:232-248)."""
-        from ._device import zeros_bytes
+        from ._device import call, current_stream, stream_ptr, zeros_bytes
 
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
@@ -802,7 +803,7 @@ class SlidingDetector:
         as `detect()` (window_id = the slice of this call)."""
         import torch
 
-        from ._device import zeros_bytes
+        from ._device import call, current_stream, stream_ptr, zeros_bytes
 
         beta = self.params.beta if beta is None else beta
         cutoff = beta * self.params.theta
@@ -824,11 +825,17 @@ class SlidingDetector:
         self._ldca_view_into(lview)  # first: fused with the fold of deferred stamps
         if self._iv() is not None:  # snapshot of the incremental view (16 MiB at r=16)
             src = self._seav_view().device_buffer()
-            seav.device_buffer()[: src.numel()].copy_(src)
+            dst = seav.device_buffer()
+            nbytes = src.numel() * src.element_size()
+            if nbytes > dst.numel() * dst.element_size():
+                raise ValueError("SEAV view snapshot larger than its view set buffer")
+            call("sspd_copy_async", dst.data_ptr(), src.data_ptr(), nbytes, stream_ptr())
         else:
             self._materialize_into(seav)
-        views_ready = torch.cuda.Event()
-        views_ready.record(torch.cuda.current_stream())
+        views_ready = st.get("views_ready")  # re-recorded per call: wait_event binds the current record
+        if views_ready is None:
+            views_ready = st["views_ready"] = torch.cuda.Event()
+        views_ready.record(current_stream())
         side = st["side"]
         side.wait_event(views_ready)
         graphs = vset[3] if self.finalize_graphs else None

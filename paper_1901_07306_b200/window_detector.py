@@ -218,7 +218,9 @@ class DeviceFinalize:
         import torch
 
         self.seav, self.ldca, self.p, self.k, self.cutoff = seav, ldca_buf, params_block, k, cutoff
-        self.stream = stream or torch.cuda.current_stream()
+        from ._device import current_stream
+
+        self.stream = stream or current_stream()
         self.on_overflow = on_overflow
         self.m = None
         self.graphs = graphs
@@ -245,6 +247,8 @@ class DeviceFinalize:
 
     def _launch(self, cap: int):
         import torch
+
+        from ._device import on_stream
 
         seav = self.seav
         self.cap = cap
@@ -278,13 +282,18 @@ class DeviceFinalize:
                 g = self.graphs["graph"] = (key, graph, out, h_tail)
             _, graph, self.out, self.h_tail = g
             self.shared = True
-            with torch.cuda.stream(self.stream):
+            # the view set's previous finalize has been resolved before this
+            # launch (detect_async), so its completion event is free to reuse
+            ev = self.graphs.get("event")
+            if ev is None:
+                ev = self.graphs["event"] = torch.cuda.Event()
+            with on_stream(self.stream):
                 if keep[1] != self.cutoff:  # stream-ordered after every earlier replay's reads
                     keep[0].copy_(device_keep_table(self.k, self.cutoff), non_blocking=True)
                     keep[1] = self.cutoff
                 graph.replay()
-                self.event = torch.cuda.Event()
-                self.event.record(self.stream)
+            ev.record(self.stream)
+            self.event = ev
             return
         with torch.cuda.stream(self.stream):
             self.out = torch.empty(shape, dtype=torch.int32, device=dev)
@@ -311,6 +320,8 @@ class DeviceFinalize:
         device arrays (async, on the finalize's stream)."""
         import torch
 
+        from ._device import call, on_stream
+
         if not self.shared or self.out is None:
             return
         self.resolve()
@@ -320,11 +331,12 @@ class DeviceFinalize:
             self.shared = False
             return
         m, cap = self.m, self.cap
-        with torch.cuda.stream(self.stream):
+        with on_stream(self.stream):  # allocated and copied on the finalize's stream
             own = torch.empty(2 * cap if m else 0, dtype=torch.int32, device=self.out.device)
             if m:
-                own[:m].copy_(self.out[:m], non_blocking=True)
-                own[cap:cap + m].copy_(self.out[cap:cap + m], non_blocking=True)
+                src, dst, sp = self.out.data_ptr(), own.data_ptr(), self.stream.cuda_stream
+                call("sspd_copy_async", dst, src, 4 * m, sp)
+                call("sspd_copy_async", dst + 4 * cap, src + 4 * cap, 4 * m, sp)
         self.out = own
         self.shared = False
 
