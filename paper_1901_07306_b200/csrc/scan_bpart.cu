@@ -837,6 +837,9 @@ static void device_limits(int& dev, int& sms, int& max_smem) {
     sms = 148;
     max_smem = 232448;
   }
+  // A/B knob: fewer CTAs than SMs (the rest stay free for kernels of other
+  // streams while the cooperative scan runs)
+  if (const char* e = getenv("SSPD_BPART_GRID")) sms = std::max(16, std::min(sms, atoi(e)));
 }
 
 }  // namespace bpart
