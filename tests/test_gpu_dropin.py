@@ -465,3 +465,35 @@ def test_host_batches_staged_bit_exact_vs_oracle(cuda, oracle, stage):
     st.process_pair(int(hips[0]), int(oips[0]))
     s1, l1 = oracle.scan(p, hips[:1], oips[:1])
     assert st.seav.payload_bytes() == s1.tobytes() and st.ldca.payload_bytes() == l1.tobytes()
+
+
+# --- device plumbing ---------------------------------------------------------------
+def test_fast_stream_helpers_match_torch(cuda):
+    """_device.current_stream / on_stream (the per-slide host path) select and
+    restore exactly what torch.cuda.current_stream / torch.cuda.stream do,
+    nested, and on an exception."""
+    import torch
+
+    from paper_1901_07306_b200._device import current_stream, on_stream
+
+    base = torch.cuda.current_stream()
+    assert current_stream() == base
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with on_stream(s1):
+        assert torch.cuda.current_stream() == s1 and current_stream() == s1
+        with on_stream(s2):
+            assert torch.cuda.current_stream() == s2
+        assert torch.cuda.current_stream() == s1
+    assert torch.cuda.current_stream() == base
+    with pytest.raises(RuntimeError):
+        with on_stream(s2):
+            raise RuntimeError("inside")
+    assert torch.cuda.current_stream() == base
+    # work issued inside lands on the selected stream
+    x = torch.zeros(1 << 20, device="cuda")
+    with on_stream(s1):
+        x.add_(1)
+        ev = torch.cuda.Event()
+        ev.record()
+    s1.synchronize()
+    assert ev.query() and float(x[0]) == 1.0
