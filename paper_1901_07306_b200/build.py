@@ -62,6 +62,28 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None) -
     return lib_path
 
 
+def build_hostfast(force: bool = False) -> Path:
+    """The CPython binding of the drop-in staging copy (csrc/hostfast.c),
+    compiled with the host C compiler next to the package (host code only;
+    Python falls back to the ctypes call when it is absent)."""
+    import sysconfig
+
+    src = CSRC / "hostfast.c"
+    out = PKG / ("_hostfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    cc = os.environ.get("CC", "gcc")
+    tmp = out.with_suffix(".tmp")
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], str(src), "-o", str(tmp)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"{cc} failed for hostfast.c:\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     outs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=Path(outs[0]) if outs else None))
+    if not outs:
+        print(build_hostfast(force="--force" in sys.argv))

@@ -200,6 +200,19 @@ _FINALIZE_SCRATCH: dict = {}  # (capacity, LR, LC) -> sspd_finalize work-space b
 _SM_COUNT: dict = {}  # device -> SMs
 
 
+def _hostfast_pack():
+    """pack_u32 of the CPython staging binding (csrc/hostfast.c) bound to the
+    loaded library's copy pool, or None when the module was not built."""
+    try:
+        from . import _hostfast
+    except ImportError:
+        return None
+    from ._abi import lib
+
+    _hostfast.set_pack(ctypes.cast(lib().sspd_host_pack_pairs, ctypes.c_void_p).value)
+    return _hostfast.pack_u32
+
+
 class DeviceFinalize:
     """One fused finalize (`sspd_finalize`: K5 restore -> sort -> K6 filter ->
     compaction) enqueued on a stream without any host round trip.
@@ -472,6 +485,20 @@ class DetectorState:
         once."""
         hs = self.__dict__.get("_hstage")
         if hs is not None and type(hips) is np.ndarray and type(oips) is np.ndarray:
+            fast = hs["fast"]
+            if (fast is not None and self.coalesce_host_batches and hs["cap"] == self.host_stage_pairs
+                    and hs["hooked"] == (id(self.seav), id(self.ldca))):
+                # the reference's call pattern through the CPython binding
+                # (buffer protocol, no ctypes objects): -1 = not a plain
+                # 1-D uint32 pair of equal length that fits -> paths below
+                b, fill = hs["b"], hs["fill"]
+                n = fast(hips, oips, hs["ph_addr"][b] + 4 * fill, hs["po_addr"][b] + 4 * fill, hs["cap"] - fill)
+                if n > 0:
+                    hs["fill"] = fill + n
+                    self.pair_count += n
+                    if hs["fill"] == hs["cap"]:
+                        self._flush_host()
+                    return
             # fast path of the reference's call pattern (uint32 numpy views
             # appended to live staging buffers): one native copy, no checks
             # beyond what the slow path would conclude for the same call
@@ -573,6 +600,7 @@ class DetectorState:
             from ._abi import lib
             hs["pack"] = lib().sspd_host_pack_pairs
             hs["po_addr"] = [t.data_ptr() for t in hs["po"]]
+            hs["fast"] = _hostfast_pack()
         hook = weakref.WeakMethod(self._flush_host)
         if self.seav._pre_read is None or self.seav._pre_read() != self._flush_host:
             self.seav._pre_read = hook

@@ -65,3 +65,31 @@ def test_pack_pairs_after_fork():
         os._exit(0 if rc == 0 and (d1 == a).all() else 3)
     _, status = os.waitpid(pid, 0)
     assert os.WEXITSTATUS(status) == 0
+
+
+def test_hostfast_binding_stages_plain_u32_and_declines_the_rest():
+    """csrc/hostfast.c (the CPython binding of the drop-in staging copy):
+    plain 1-D uint32 pairs are copied by the library's pool; anything else
+    (other widths, byte order, strides, unequal lengths, no room) returns -1
+    so DetectorState.process_batch takes its general path."""
+    from paper_1901_07306_b200.window_detector import _hostfast_pack
+
+    pack = _hostfast_pack()
+    if pack is None:
+        pytest.skip("_hostfast not built")
+    rng = np.random.default_rng(5)
+    n = 70_001
+    h = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    o = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    dh = np.zeros(n + 8, dtype=np.uint32)
+    do = np.zeros(n + 8, dtype=np.uint32)
+    assert pack(h, o, dh.ctypes.data + 4 * 8, do.ctypes.data + 4 * 8, n) == n
+    assert (dh[8:] == h).all() and (do[8:] == o).all() and not dh[:8].any()
+    room = n + 8
+    assert pack(h.astype(np.int64), o, dh.ctypes.data, do.ctypes.data, room) == -1
+    assert pack(h.astype(">u4"), o.astype(">u4"), dh.ctypes.data, do.ctypes.data, room) == -1
+    assert pack(h[::2], o[::2], dh.ctypes.data, do.ctypes.data, room) == -1
+    assert pack(h[:-1], o, dh.ctypes.data, do.ctypes.data, room) == -1
+    assert pack(h, o, dh.ctypes.data, do.ctypes.data, n - 1) == -1
+    assert pack(h[:0], o[:0], dh.ctypes.data, do.ctypes.data, room) == -1
+    assert pack(h.reshape(1, -1), o.reshape(1, -1), dh.ctypes.data, do.ctypes.data, room) == -1
