@@ -335,17 +335,22 @@ def run_dropin(st, h_host, o_host, args, timed, stream_value) -> dict:
     L = lib()
     stage = st._hstage
     pa, pb, cap = stage["ph_addr"][0], stage["po_addr"][0], stage["cap"]
+    fast = stage.get("fast")  # the CPython staging binding process_batch uses (csrc/hostfast.c)
     t0 = time.perf_counter()
     for lo in range(0, n, B):
         off = 4 * (lo % cap)
-        L.sspd_host_pack_pairs(h_np.ctypes.data + 4 * lo, o_np.ctypes.data + 4 * lo, min(B, n - lo), 4, 4,
-                               pa + off, pb + off)
+        if fast is not None:
+            fast(h_np[lo:lo + B], o_np[lo:lo + B], pa + off, pb + off, cap - lo % cap)
+        else:
+            L.sspd_host_pack_pairs(h_np.ctypes.data + 4 * lo, o_np.ctypes.data + 4 * lo, min(B, n - lo), 4, 4,
+                                   pa + off, pb + off)
     pack_s = time.perf_counter() - t0
     pack_pps = n / pack_s
     return {"value": round(v, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "calls_per_step": -(-n // B),
             "host_copy_bound": {"value": round(pack_pps / 1e6, 3), "unit": UNIT,
                                 "gbs": round(8 * n / pack_s / 1e9, 2), "threads": int(L.sspd_host_copy_threads()),
                                 "frac": round(v * 1e6 / pack_pps, 4),
+                                "binding": "cpython" if fast is not None else "ctypes",
                                 "note": "pageable -> pinned copy of the keys alone, same 65,536-pair calls"},
             "pairs_per_call": B, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * out[0] + 16,
             "frac_of_host_stream": round(v / stream_value, 4) if stream_value else None,
