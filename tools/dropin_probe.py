@@ -35,6 +35,8 @@ def main():
         off = 4 * (lo % cap)
         L.sspd_host_pack_pairs(h.ctypes.data + 4 * lo, o.ctypes.data + 4 * lo, B, 4, 4, pa + off, pb + off)
     pack_s = time.perf_counter() - t
+    if os.environ.get("SSPD_PROBE_STAGE_PAIRS"):  # pinned staging size (pairs) per buffer
+        DetectorState.host_stage_pairs = int(os.environ["SSPD_PROBE_STAGE_PAIRS"])
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         st = DetectorState.create(DetectorParams(theta=1024, r=12, k=8192, lr=8, lc=1024, design_n=80.5e6))
@@ -55,6 +57,7 @@ def main():
         best = min(best, time.perf_counter() - t)
     # python-side cost of one call alone (staging disabled: no copy, no scan)
     print(json.dumps({"threads": L.sspd_host_copy_threads(), "nt": os.environ.get("SSPD_HOST_COPY_NT", "default"),
+                      "stage_pairs": DetectorState.host_stage_pairs,
                       "pack_gbs": round(8 * n / pack_s / 1e9, 2), "pack_us_per_call": round(pack_s / (n // B) * 1e6, 2),
                       "dropin_gpps": round(n / best / 1e9, 3), "dropin_ms": round(best * 1e3, 2),
                       "cpus": os.cpu_count()}), flush=True)
