@@ -1469,6 +1469,22 @@ extern "C" int sspd_compact_reports(const uint32_t* ip, const uint32_t* z0, cons
 // the radix sort).
 constexpr uint64_t kBucketSortMaxCap = 1ull << 18;
 
+// The finalize's zero-initialised state in one launch instead of one memset
+// per region: the two counts, the per-SEA overflow flags + the bucket flag
+// byte, the bucket histogram + cursors (bucket path) and the filter's
+// work-list count -- each a graph node otherwise.
+__global__ void __launch_bounds__(256) finalize_init_kernel(unsigned long long* counts, uint8_t* overflow,
+                                                            uint32_t nflags, uint32_t* hist, uint32_t nhist,
+                                                            unsigned long long* work_n) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 2) counts[t] = 0;
+  if (t == 2 && work_n) *work_n = 0;
+  for (uint32_t i = t; i < nflags; i += stride) overflow[i] = 0;
+  if (hist)
+    for (uint32_t i = t; i < nhist; i += stride) hist[i] = 0;
+}
+
 extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p, uint64_t restore_cap,
                              const uint8_t* keep_table, uint64_t capacity, uint32_t* out_ip, uint32_t* out_z0,
                              unsigned long long* counts, uint8_t* overflow, void* scratch, size_t* scratch_bytes,
@@ -1515,11 +1531,15 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
   uint32_t* cursor = hist + nb;
   uint32_t* starts = reinterpret_cast<uint32_t*>(s8 + o_start);
   const uint32_t rp_count = 1u << p->r;
-  if (cudaMemsetAsync(counts, 0, 16, st) != cudaSuccess || cudaMemsetAsync(overflow, 0, rp_count + 1, st) != cudaSuccess)
-    return SSPD_ERR_CUDA;
+  {
+    unsigned long long* wn = cells ? reinterpret_cast<unsigned long long*>(s8 + o_wn) : nullptr;
+    const uint32_t nflags = rp_count + 1, nhist = bucket ? 2u * nb : 0u;  // hist + cursor: 8 B per bucket
+    const uint32_t work = std::max(nflags, nhist);
+    finalize_init_kernel<<<std::min<uint32_t>(148u * 4u, (work + 255) / 256), 256, 0, st>>>(
+        counts, overflow, nflags, bucket ? hist : nullptr, nhist, wn);
+  }
   const uint32_t* sorted = ip;
   if (bucket) {
-    if (cudaMemsetAsync(hist, 0, 8ull * nb, st) != cudaSuccess) return SSPD_ERR_CUDA;
     rc = restore_launch(seav, p, 0, rp_count, restore_cap, ip, aux, C, counts, overflow, hist, hshift, stream);
     if (rc) return rc;
     const uint32_t smem = 4u * nb;
@@ -1544,8 +1564,7 @@ extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const ssp
     uint32_t* cz = reinterpret_cast<uint32_t*>(s8 + o_cz);
     uint32_t* work_rows = reinterpret_cast<uint32_t*>(s8 + o_ipa);
     uint32_t* work = reinterpret_cast<uint32_t*>(s8 + 3 * vec);
-    unsigned long long* work_n = reinterpret_cast<unsigned long long*>(s8 + o_wn);
-    if (cudaMemsetAsync(work_n, 0, sizeof(unsigned long long), st) != cudaSuccess) return SSPD_ERR_CUDA;
+    unsigned long long* work_n = reinterpret_cast<unsigned long long*>(s8 + o_wn);  // zeroed by finalize_init_kernel
     cell_zeros_kernel<<<grid_for(cell_zeros_kernel, 256, cells * 32), 256, 0, st>>>(ldca, *p, cz);
     filter_summary_kernel<<<grid_for(filter_summary_kernel, 256, C), 256, 0, st>>>(
         *p, sorted, C, counts, cz, keep_table, z0, keep, work, work_rows, work_n);
