@@ -626,10 +626,12 @@ def run_gpu(args) -> dict | None:
                    "l2": "inputs (2 GiB/window) exceed the 126 MB L2; no flush needed",
                    "seav_r": dp.r, "ldca": "LR=8 LC=1024 k=8192 (8 MiB)"},
         "e2e": e2e,
-        # per step: the scan, K5 restore, bucket sort (scatter + per-bucket
-        # rank), K6 filter, compaction (count + scatter) = 7 launches of
-        # libsspd_b200.so (+ the merge kernels at N > 1)
-        "gpu_launches": args.steps * (7 + (2 if merger else 0)),
+        # per step: the scan, then the fused finalize -- state init, K5
+        # restore, bucket sort (scatter + per-bucket rank), cell summary,
+        # K6 filter (summary pass + AND pass), compaction (count + scatter)
+        # = 10 launches of libsspd_b200.so (+ the merge kernels at N > 1);
+        # matches the ncu launch list of the step (profiles/r02f_launches_config2.csv)
+        "gpu_launches": args.steps * (10 + (2 if merger else 0)),
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": hbm_gbs, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback",
@@ -1044,7 +1046,8 @@ def run_sharded(args) -> dict | None:
                    "global_batch": n_total, "shards_per_rank": len(mine),
                    "parallelism": f"dp{world} (shards folded onto ranks, OR-merge to rank 0)",
                    "l2": "inputs (8 GiB) exceed the 126 MB L2; no flush needed"},
-        "e2e": None, "gpu_launches": args.steps * (len(mine) + 6 + (2 if merger else 0)),
+        # one scan per shard + the fused finalize's 9 launches (as config 2)
+        "e2e": None, "gpu_launches": args.steps * (len(mine) + 9 + (2 if merger else 0)),
         "merge": merge,
         "clocks": clk,
         "detect": {"reports_per_window": len(first[0]), "planted_supers_found": len(set(supers.tolist()) & found),
