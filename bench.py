@@ -630,7 +630,7 @@ def run_gpu(args) -> dict | None:
         # restore, bucket sort (scatter + per-bucket rank), cell summary,
         # K6 filter (summary pass + AND pass), compaction (count + scatter)
         # = 10 launches of libsspd_b200.so (+ the merge kernels at N > 1);
-        # matches the ncu launch list of the step (profiles/r02f_launches_config2.csv)
+        # matches the ncu launch list of the step (profiles/r02f_launches_config2_final.csv)
         "gpu_launches": args.steps * (10 + (2 if merger else 0)),
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": hbm_gbs, "unit": "GB/s",
                      "frac": round(achieved_gbs / hbm_gbs, 5), "traffic": traffic,

@@ -1473,6 +1473,7 @@ constexpr uint64_t kBucketSortMaxCap = 1ull << 18;
 // per region: the two counts, the per-SEA overflow flags + the bucket flag
 // byte, the bucket histogram + cursors (bucket path) and the filter's
 // work-list count -- each a graph node otherwise.
+namespace sspd {
 __global__ void __launch_bounds__(256) finalize_init_kernel(unsigned long long* counts, uint8_t* overflow,
                                                             uint32_t nflags, uint32_t* hist, uint32_t nhist,
                                                             unsigned long long* work_n) {
@@ -1484,6 +1485,7 @@ __global__ void __launch_bounds__(256) finalize_init_kernel(unsigned long long* 
   if (hist)
     for (uint32_t i = t; i < nhist; i += stride) hist[i] = 0;
 }
+}  // namespace sspd
 
 extern "C" int sspd_finalize(const uint8_t* seav, const uint8_t* ldca, const sspd_params* p, uint64_t restore_cap,
                              const uint8_t* keep_table, uint64_t capacity, uint32_t* out_ip, uint32_t* out_z0,
